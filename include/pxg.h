@@ -1,0 +1,160 @@
+/* pxg.h — C ABI of libpxg, the sm_100a implementation of the proxy-BDPT render loop.
+ *
+ * Drop-in boundary: the reference entry point
+ *   Image proxima::render_proxy_bdpt(const Scene&, int spp, uint64_t seed,
+ *                                    const ProxyParams& = {}, ProxyDiagnostics* = nullptr,
+ *                                    const std::function<bool(int, const Image&)>& = {})
+ * (proj/include/proxima/proxy.hpp:197-200, proj/src/proxy.cpp:647-834) is replaced by
+ *   pxg_create(scene, params, seed)  -> context (scene upload, Scene::finalize, BVH, pretrace)
+ *   pxg_render_pass(ctx)             -> one progressive pass = 1 spp for every pixel
+ *   pxg_read_mean(ctx, rgb)          -> running mean image (the pass_done callback argument)
+ *   pxg_read_diag(ctx, ...)          -> ProxyDiagnostics (proj/include/proxima/proxy.hpp:175-188)
+ *   pxg_destroy(ctx)
+ * The C++ wrapper `render_proxy_bdpt_gpu` (include/pxg_proxima.hpp) and the Python mirror
+ * (paper_2503_23412_b200.render_proxy_bdpt) loop passes and call pass_done between them.
+ *
+ * Conventions: plain pointers and sizes only; every function returns 0 on success and a
+ * negative PXG_E* code on failure (no exceptions cross the ABI); the message is in
+ * pxg_last_error(ctx) (or pxg_last_error(NULL) when no context exists). The context owns
+ * all device memory; input arrays are only read during the call.
+ */
+#ifndef PXG_H
+#define PXG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PXG_ABI_VERSION 1
+
+enum {
+  PXG_OK = 0,
+  PXG_E_INVALID = -1,   /* validation error (reference: std::runtime_error from load_scene /
+                           std::invalid_argument from the statistics, exit code 2 in the CLI) */
+  PXG_E_CUDA = -2,      /* CUDA runtime failure */
+  PXG_E_RUNTIME = -3,   /* numeric failure inside the estimator (reference: std::runtime_error
+                           "reciprocal: integrand must be finite and non-negative", recip.hpp:74-75) */
+  PXG_E_NODEVICE = -4
+};
+
+/* Flattened proxima::Scene (proj/include/proxima/scene.hpp:16-96). Primitive i:
+ * shape 0 sphere (a = centre, radius[i]), 1 triangle (a, b, c vertices),
+ * 2 rectangle (a = origin, b, c = edges). Materials: 7 doubles each
+ * {base_r, base_g, base_b, metallic, roughness, transmission, ior} (bsdf.hpp:13-20). */
+typedef struct pxg_scene_desc {
+  int n_prims;
+  const int* shape;
+  const int* material;
+  const double* a; /* [n_prims*3] */
+  const double* b; /* [n_prims*3] */
+  const double* c; /* [n_prims*3] */
+  const double* radius; /* [n_prims] */
+  int n_materials;
+  const double* materials; /* [n_materials*7] */
+  int n_emitters;
+  const int* emitter_prim;       /* [n_emitters] */
+  const double* emitter_radiance;/* [n_emitters*3] */
+  double cam_position[3];
+  double cam_look_at[3];
+  double cam_up[3];
+  double fov_y;
+  int width, height;
+  int max_depth; /* Settings::max_depth (scene.hpp:50-54) */
+} pxg_scene_desc;
+
+/* proxima::ProxyParams (proj/include/proxima/proxy.hpp:162-173), same defaults. */
+typedef struct pxg_params {
+  int enabled;            /* 1 */
+  int pool_budget;        /* 400 */
+  int recip_repeats;      /* 5 */
+  int freeze_iteration;   /* 40 */
+  long long recursion_cap;/* 10000 */
+  int pretrace_paths;     /* 20000 */
+  int light_walks;        /* 0 = one per pixel */
+  double gate_high;       /* 1.0 */
+  double gate_low;        /* 0.2 */
+  double gate_threshold;  /* 0.05 */
+} pxg_params;
+
+/* Pixel-row shard of a multi-GPU render: this context renders image rows
+ * [row_begin, row_end) (multiples of the 10-pixel gate grid) and pool walks
+ * [walk_begin, walk_end). A single-GPU render uses {0, height, 0, light_walks}
+ * (pxg_create fills it when shard == NULL). */
+typedef struct pxg_shard {
+  int row_begin, row_end;
+  int walk_begin, walk_end;
+} pxg_shard;
+
+typedef struct pxg_ctx pxg_ctx;
+
+void pxg_default_params(pxg_params* p);
+int pxg_abi_version(void);
+int pxg_device_count(void);
+
+int pxg_create(const pxg_scene_desc* scene, const pxg_params* params, uint64_t seed, int device,
+               const pxg_shard* shard, pxg_ctx** out);
+void pxg_destroy(pxg_ctx* ctx);
+const char* pxg_last_error(const pxg_ctx* ctx);
+
+/* One progressive pass (Stage 1 pool + reciprocal estimates, Stage 2 per-pixel strategies
+ * with the gated proxy connection, gamma update), proj/src/proxy.cpp:683-827. */
+int pxg_render_pass(pxg_ctx* ctx);
+/* One pass that also records the sub-path primitive ids for pxg_dump_prims. */
+int pxg_render_pass_traced(pxg_ctx* ctx);
+/* Several passes back to back. */
+int pxg_render_passes(pxg_ctx* ctx, int n);
+int pxg_synchronize(pxg_ctx* ctx);
+
+/* Running mean acc/done over this context's rows, row-major fp64 RGB, y = 0 top
+ * (proj/src/proxy.cpp:822-833). rgb holds (row_end-row_begin)*width*3 doubles. */
+int pxg_read_mean(pxg_ctx* ctx, double* rgb, int* passes_done);
+/* Unnormalised accumulator (sum of per-pass values), for shard reduction. */
+int pxg_read_accum(pxg_ctx* ctx, double* rgb, int* passes_done);
+
+/* ProxyDiagnostics: rows[4000*5] = {retrace_attempts, retrace_accepts, recip_runs,
+ * recip_truncated, estimates_failed} per dense key ((u-1)*10+c)*100+s; touched[4000]
+ * marks keys present in the reference's map; pool[2] = {pool_raw, pool_kept}. */
+int pxg_read_diag(pxg_ctx* ctx, long long* rows, int* touched, long long* pool);
+
+/* Subspace statistics snapshot (SubspaceStats, subspace.hpp:88-119): per dense key
+ * {max_ratio, sum_est, sum_est_sq} and {ratio_count, est_count}; gamma rows [32*100]. */
+int pxg_read_stats(pxg_ctx* ctx, double* stats3, long long* counts2, double* gamma_rows);
+
+/* Parity replay of the last rendered pass, for this context's pixels:
+ * val[n*3] final per-pixel sample value, bdpt[n*3] standard strategies only,
+ * c[n*3] proxy_connect value before gating, flags[n] (bit0 eye cut exists, bit1 proxy
+ * connection attempted, bit2 gate passed, bit3 contributed). Any pointer may be NULL. */
+int pxg_dump_pass(pxg_ctx* ctx, double* val, double* bdpt, double* c, int* flags);
+/* Primitive ids of the last pass's sub-paths: eye[n*(max_depth+1)], light[n*(max_depth-1)],
+ * -2 past the end of a sub-path, -1 for the camera vertex. */
+int pxg_dump_prims(pxg_ctx* ctx, int* eye, int* light);
+/* Pool of the last pass: n kept entries, walk, prefix end, dense key, inverse_p,
+ * inverse_p second moment and the bound B used; raw = eligible incompletes. */
+int pxg_dump_pool(pxg_ctx* ctx, int cap, int* n, long long* raw, int* walk, int* end, int* key,
+                  double* inv_p, double* inv_p_m2, double* bound);
+
+/* Scene::intersect / Scene::occluded on the device (parity of the traversal kernel).
+ * rays[n*6] = origin, unit direction; tmax may be NULL (1e30). */
+int pxg_intersect(pxg_ctx* ctx, int n, const double* rays, const double* tmax, int* prim, double* t);
+int pxg_occluded(pxg_ctx* ctx, int n, const double* segs, int* occ);
+
+/* Reciprocal estimator on the two-point fixture f = {1,3}, q = 1/2 (the reference's own
+ * known-answer case, proj/tests/test_recip.cpp:16-23), run i on stream (seed, RECIP, 0, i). */
+int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double* est,
+                       long long* cost, int* truncated);
+
+/* Philox stream check: first n draws of stream (seed, kind, sub, stream) computed on the device. */
+int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out);
+
+/* Device time of the kernels of the last pxg_render_passes call, by stage (ms):
+ * t[0] stage-1 pool, t[1] reciprocal runs, t[2] sub-path trace, t[3] connections,
+ * t[4] proxy connection, t[5] gate+film; counts[0] kernel launches, counts[1] rays traced. */
+int pxg_read_timing(pxg_ctx* ctx, double* t, long long* counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PXG_H */

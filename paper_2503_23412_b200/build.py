@@ -1,0 +1,78 @@
+"""Builds libpxg.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+  python -m paper_2503_23412_b200.build [--force]
+
+Device code is compiled with --fmad=false: the path math must keep the reference's fp64
+operation order (no fused multiply-add), see csrc/pxg_math.cuh.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libpxg.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CU_SOURCES = ["pxg_kernels.cu"]
+CPP_SOURCES = ["pxg_host.cpp"]
+HEADERS = ["pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
+
+
+def _inputs():
+    files = [os.path.join(CSRC, f) for f in CU_SOURCES + CPP_SOURCES + HEADERS]
+    files += [os.path.join(REPO, "include", "pxg.h"), os.path.join(REPO, "include", "pxg_philox.h")]
+    return files
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    return all(os.path.getmtime(f) <= t for f in _inputs())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    bdir = os.path.join(HERE, "_build")
+    os.makedirs(bdir, exist_ok=True)
+    inc = ["-I", os.path.join(REPO, "include"), "-I", CSRC]
+    objs = []
+    for src in CPP_SOURCES:
+        obj = os.path.join(bdir, src + ".o")
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", *inc, "-c", os.path.join(CSRC, src),
+               "-o", obj]
+        _run(cmd, verbose)
+        objs.append(obj)
+    for src in CU_SOURCES:
+        obj = os.path.join(bdir, src + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "--expt-relaxed-constexpr",
+               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc, "-c", os.path.join(CSRC, src),
+               "-o", obj]
+        _run(cmd, verbose)
+        objs.append(obj)
+    tmp = OUT + ".tmp"
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], verbose)
+    os.replace(tmp, OUT)
+    return OUT
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        sys.stdout.write(r.stdout)
+        sys.stderr.write(r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (exit {r.returncode})")
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

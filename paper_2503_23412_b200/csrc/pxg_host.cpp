@@ -1,0 +1,300 @@
+// pxg_host.cpp — one-time host work of pxg_create: Scene::finalize and the BVH build.
+//
+// finalize mirrors proj/src/scene.cpp:234-252 with the reference's fp64 operation order
+// (compiled with -ffp-contract=off) so the emitter areas, their running sums, the scene
+// bbox that the subspace grid is built on, and the camera basis are bit-identical.
+//
+// The BVH is this library's own: a binned-SAH binary tree whose nodes store both child
+// boxes in fp32 (64 B per node), rounded outward and padded so that the fp32 slab test is
+// conservative for every fp64 hit (see pxg_scene.cuh). The reference's median-split BVH
+// (scene.cpp:254-295) is private and only affects its traversal order, not hit ids.
+#include "pxg_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numbers>
+#include <stdexcept>
+
+namespace pxg {
+
+namespace {
+
+struct D3 {
+  double x, y, z;
+};
+inline D3 add(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline D3 mul(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline double dot3(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline D3 cross3(D3 a, D3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+inline double len3(D3 a) { return std::sqrt(dot3(a, a)); }
+inline D3 norm3(D3 a) { return mul(a, 1.0 / len3(a)); }
+inline D3 vmin(D3 a, D3 b) { return {std::min(a.x, b.x), std::min(a.y, b.y), std::min(a.z, b.z)}; }
+inline D3 vmax(D3 a, D3 b) { return {std::max(a.x, b.x), std::max(a.y, b.y), std::max(a.z, b.z)}; }
+inline D3 ld(const double* p) { return {p[0], p[1], p[2]}; }
+inline double comp(D3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+
+// Primitive::area (scene.cpp:107-114)
+double prim_area(int shape, D3 a, D3 b, D3 c, double r) {
+  switch (shape) {
+    case 0: return 4.0 * std::numbers::pi * r * r;
+    case 1: return 0.5 * len3(cross3(sub(b, a), sub(c, a)));
+    default: return len3(cross3(b, c));
+  }
+}
+
+// primitive_bounds (scene.cpp:74-89)
+void prim_bounds(int shape, D3 a, D3 b, D3 c, double r, D3& lo, D3& hi) {
+  if (shape == 0) {
+    lo = sub(a, D3{r, r, r});
+    hi = add(a, D3{r, r, r});
+  } else if (shape == 1) {
+    lo = vmin(a, vmin(b, c));
+    hi = vmax(a, vmax(b, c));
+  } else {
+    D3 ab = add(a, b), ac = add(a, c), abc = add(add(a, b), c);
+    lo = vmin(vmin(a, ab), vmin(ac, abc));
+    hi = vmax(vmax(a, ab), vmax(ac, abc));
+  }
+}
+
+struct BPrim {
+  D3 lo, hi, cen;
+  int id;
+};
+
+struct Box {
+  D3 lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
+  void grow(const D3& l, const D3& h) {
+    lo = vmin(lo, l);
+    hi = vmax(hi, h);
+  }
+  double area() const {
+    if (hi.x < lo.x) return 0.0;
+    D3 e = sub(hi, lo);
+    return 2.0 * (e.x * e.y + e.y * e.z + e.z * e.x);
+  }
+};
+
+struct Builder {
+  std::vector<BPrim>& prims;
+  std::vector<HostNode>& nodes;
+  std::vector<int>& order;
+  double pad;
+  int max_depth_seen = 0;
+
+  static float down(double v, double pad) {
+    float f = static_cast<float>(v - pad);
+    return std::nextafter(f, -INFINITY);
+  }
+  static float up(double v, double pad) {
+    float f = static_cast<float>(v + pad);
+    return std::nextafter(f, INFINITY);
+  }
+
+  void set_child(HostNode& n, int k, const Box& b, int code) {
+    float* lo = k == 0 ? n.lo0 : n.lo1;
+    float* hi = k == 0 ? n.hi0 : n.hi1;
+    lo[0] = down(b.lo.x, pad); lo[1] = down(b.lo.y, pad); lo[2] = down(b.lo.z, pad);
+    hi[0] = up(b.hi.x, pad); hi[1] = up(b.hi.y, pad); hi[2] = up(b.hi.z, pad);
+    (k == 0 ? n.c0 : n.c1) = code;
+  }
+
+  int leaf_code(int first, int count) {
+    for (int i = 0; i < count; ++i) order.push_back(prims[first + i].id);
+    int base = static_cast<int>(order.size()) - count;
+    return ~(base * 16 + count);
+  }
+
+  // Builds [first, first+count) and returns the child code referencing it.
+  int build(int first, int count, const Box& bounds, int depth) {
+    max_depth_seen = std::max(max_depth_seen, depth);
+    if (count <= 4 || depth >= 56) {
+      if (count <= 15) return leaf_code(first, count);
+    }
+    Box cb;
+    for (int i = first; i < first + count; ++i) cb.grow(prims[i].cen, prims[i].cen);
+    int mid = -1;
+    const int kBins = 16;
+    double best_cost = INFINITY;
+    int best_axis = -1, best_bin = -1;
+    for (int axis = 0; axis < 3; ++axis) {
+      const double lo = comp(cb.lo, axis), hi = comp(cb.hi, axis);
+      if (!(hi > lo)) continue;
+      Box bb[kBins];
+      int cnt[kBins] = {0};
+      const double scale = kBins / (hi - lo);
+      for (int i = first; i < first + count; ++i) {
+        int b = std::min(kBins - 1, static_cast<int>((comp(prims[i].cen, axis) - lo) * scale));
+        bb[b].grow(prims[i].lo, prims[i].hi);
+        ++cnt[b];
+      }
+      Box left[kBins];
+      int lc[kBins];
+      Box acc;
+      int ac = 0;
+      for (int b = 0; b < kBins; ++b) {
+        if (cnt[b]) acc.grow(bb[b].lo, bb[b].hi);
+        ac += cnt[b];
+        left[b] = acc;
+        lc[b] = ac;
+      }
+      Box racc;
+      int rc = 0;
+      for (int b = kBins - 1; b >= 1; --b) {
+        if (cnt[b]) racc.grow(bb[b].lo, bb[b].hi);
+        rc += cnt[b];
+        if (lc[b - 1] == 0 || rc == 0) continue;
+        double cost = left[b - 1].area() * lc[b - 1] + racc.area() * rc;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best_axis = axis;
+          best_bin = b;
+        }
+      }
+    }
+    if (best_axis >= 0) {
+      const double lo = comp(cb.lo, best_axis), hi = comp(cb.hi, best_axis);
+      const double scale = kBins / (hi - lo);
+      auto it = std::partition(prims.begin() + first, prims.begin() + first + count, [&](const BPrim& p) {
+        int b = std::min(kBins - 1, static_cast<int>((comp(p.cen, best_axis) - lo) * scale));
+        return b < best_bin;
+      });
+      mid = static_cast<int>(it - prims.begin());
+      if (mid == first || mid == first + count) mid = -1;
+    }
+    if (mid < 0) mid = first + count / 2;  // degenerate centroids: split by position
+    Box lb, rb;
+    for (int i = first; i < mid; ++i) lb.grow(prims[i].lo, prims[i].hi);
+    for (int i = mid; i < first + count; ++i) rb.grow(prims[i].lo, prims[i].hi);
+    const int idx = static_cast<int>(nodes.size());
+    nodes.push_back(HostNode{});
+    int cl = build(first, mid - first, lb, depth + 1);
+    int cr = build(mid, first + count - mid, rb, depth + 1);
+    set_child(nodes[idx], 0, lb, cl);
+    set_child(nodes[idx], 1, rb, cr);
+    return idx;
+  }
+};
+
+}  // namespace
+
+void finalize_scene(const SceneDesc& d, SceneHost& h) {
+  const int n = d.n_prims;
+  if (n <= 0) throw std::runtime_error("scene: no primitives defined");
+  if (d.n_emitters <= 0) throw std::runtime_error("scene: scene must contain at least one emitter");
+  if (d.width <= 0 || d.height <= 0) throw std::runtime_error("scene: resolution must be positive");
+  h.prim_emitter.assign(n, -1);
+  h.prim_mat.assign(d.material, d.material + n);
+  h.prim_shape.assign(d.shape, d.shape + n);
+  for (int i = 0; i < n; ++i) {
+    if (d.material[i] < 0 || d.material[i] >= d.n_materials)
+      throw std::runtime_error("scene: unknown material");
+    if (d.shape[i] < 0 || d.shape[i] > 2) throw std::runtime_error("scene: unknown shape");
+  }
+  // emitters, areas and running sums in the reference order
+  double total = 0.0;
+  h.emitter_cum.resize(d.n_emitters);
+  for (int e = 0; e < d.n_emitters; ++e) {
+    const int p = d.emitter_prim[e];
+    if (p < 0 || p >= n) throw std::runtime_error("scene: emitter references unknown primitive");
+    h.prim_emitter[p] = e;
+    total += prim_area(d.shape[p], ld(d.a + 3 * p), ld(d.b + 3 * p), ld(d.c + 3 * p), d.radius[p]);
+  }
+  // sample_light_point re-sums areas in emitter order with its own accumulator; the
+  // running values are identical to the finalize sum's prefixes.
+  double acc = 0.0;
+  for (int e = 0; e < d.n_emitters; ++e) {
+    const int p = d.emitter_prim[e];
+    acc += prim_area(d.shape[p], ld(d.a + 3 * p), ld(d.b + 3 * p), ld(d.c + 3 * p), d.radius[p]);
+    h.emitter_cum[e] = acc;
+  }
+  // an emitter listed twice keeps the later index (emitter_of_primitive overwrite order)
+  h.total_emitter_area = total;
+  D3 bmin{1e30, 1e30, 1e30}, bmax{-1e30, -1e30, -1e30};
+  h.prim_geo.assign(3 * static_cast<size_t>(n), 0.0);
+  h.prim_center.assign(4 * static_cast<size_t>(n), 0.0);
+  h.prim_abc.assign(9 * static_cast<size_t>(n), 0.0);
+  std::vector<BPrim> bp(n);
+  double scale = 0.0;
+  for (int i = 0; i < n; ++i) {
+    D3 a = ld(d.a + 3 * i), b = ld(d.b + 3 * i), c = ld(d.c + 3 * i);
+    const double r = d.radius[i];
+    D3 lo, hi;
+    prim_bounds(d.shape[i], a, b, c, r, lo, hi);
+    bmin = vmin(bmin, lo);
+    bmax = vmax(bmax, hi);
+    bp[i] = BPrim{lo, hi, mul(add(lo, hi), 0.5), i};
+    scale = std::max({scale, std::fabs(lo.x), std::fabs(lo.y), std::fabs(lo.z), std::fabs(hi.x),
+                      std::fabs(hi.y), std::fabs(hi.z)});
+    D3 e1 = d.shape[i] == 1 ? sub(b, a) : b;
+    D3 e2 = d.shape[i] == 1 ? sub(c, a) : c;
+    double* g = &h.prim_abc[9 * static_cast<size_t>(i)];
+    if (d.shape[i] == 0) {
+      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = r;
+      double* cc = &h.prim_center[4 * static_cast<size_t>(i)];
+      cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = r;
+    } else {
+      g[0] = a.x; g[1] = a.y; g[2] = a.z;
+      g[3] = e1.x; g[4] = e1.y; g[5] = e1.z;
+      g[6] = e2.x; g[7] = e2.y; g[8] = e2.z;
+      // primitive_normal: triangle normalize(cross(b - a, c - a)); rectangle normalize(cross(b, c))
+      D3 nn = norm3(cross3(e1, e2));
+      h.prim_geo[3 * i] = nn.x; h.prim_geo[3 * i + 1] = nn.y; h.prim_geo[3 * i + 2] = nn.z;
+    }
+  }
+  h.bbox_min[0] = bmin.x; h.bbox_min[1] = bmin.y; h.bbox_min[2] = bmin.z;
+  h.bbox_max[0] = bmax.x; h.bbox_max[1] = bmax.y; h.bbox_max[2] = bmax.z;
+
+  // camera basis (scene.cpp:116-125)
+  D3 pos = ld(d.cam_position), look = ld(d.cam_look_at), up = ld(d.cam_up);
+  D3 fwd = norm3(sub(look, pos));
+  D3 right = norm3(cross3(fwd, up));
+  D3 cup = cross3(right, fwd);
+  const double v[12] = {pos.x, pos.y, pos.z, fwd.x, fwd.y, fwd.z, right.x, right.y, right.z, cup.x, cup.y, cup.z};
+  std::memcpy(h.cam, v, sizeof(v));
+  h.tan_half = std::tan(d.fov_y * std::numbers::pi / 360.0);
+  h.aspect = static_cast<double>(d.width) / d.height;
+  scale = std::max({scale, std::fabs(pos.x), std::fabs(pos.y), std::fabs(pos.z), 1.0});
+
+  // BVH
+  h.nodes.clear();
+  h.order.clear();
+  h.nodes.reserve(2 * static_cast<size_t>(n) / 3 + 2);
+  h.order.reserve(n);
+  const double pad = 1e-5 * scale;
+  Builder B{bp, h.nodes, h.order, pad};
+  Box all;
+  for (auto& p : bp) all.grow(p.lo, p.hi);
+  if (n <= 4) {
+    // the root is always an internal node: one leaf child and one empty child
+    h.nodes.push_back(HostNode{});
+    int code = B.leaf_code(0, n);
+    B.set_child(h.nodes[0], 0, all, code);
+    HostNode& r = h.nodes[0];
+    r.lo1[0] = r.lo1[1] = r.lo1[2] = 1e30f;
+    r.hi1[0] = r.hi1[1] = r.hi1[2] = -1e30f;
+    r.c1 = ~0;
+    h.bvh_depth = 1;
+  } else {
+    B.build(0, n, all, 0);  // nodes is empty, so the root lands in slot 0
+    h.bvh_depth = B.max_depth_seen;
+  }
+  // leaf-ordered exact records
+  h.recs.resize(n);
+  for (int k = 0; k < n; ++k) {
+    const int i = h.order[k];
+    HostRec& r = h.recs[k];
+    const double* g = &h.prim_abc[9 * static_cast<size_t>(i)];
+    for (int j = 0; j < 9; ++j) r.v[j] = g[j];
+    if (d.shape[i] == 0) {
+      r.v[3] = d.radius[i];
+      r.v[4] = r.v[5] = r.v[6] = r.v[7] = r.v[8] = 0.0;
+    }
+    r.shape = d.shape[i];
+    r.id = i;
+  }
+}
+
+}  // namespace pxg

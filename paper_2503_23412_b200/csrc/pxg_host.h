@@ -1,0 +1,47 @@
+// pxg_host.h — host-side scene finalisation and BVH build (pxg_host.cpp).
+#pragma once
+
+#include <vector>
+
+#include "pxg.h"
+
+namespace pxg {
+
+using SceneDesc = pxg_scene_desc;
+
+// Layout-identical to pxg::BvhNode (pxg_scene.cuh), 64 B.
+struct alignas(16) HostNode {
+  float lo0[3] = {0, 0, 0}, hi0[3] = {0, 0, 0};
+  float lo1[3] = {0, 0, 0}, hi1[3] = {0, 0, 0};
+  int c0 = ~0, c1 = ~0;
+  int pad0 = 0, pad1 = 0;
+};
+static_assert(sizeof(HostNode) == 64, "node size");
+
+// Layout-identical to pxg::PrimRec, 80 B.
+struct alignas(16) HostRec {
+  double v[9];
+  int shape;
+  int id;
+};
+static_assert(sizeof(HostRec) == 80, "record size");
+
+struct SceneHost {
+  std::vector<int> prim_mat, prim_shape, prim_emitter;
+  std::vector<double> prim_geo;     // [n][3]
+  std::vector<double> prim_center;  // [n][4]
+  std::vector<double> prim_abc;     // [n][9]
+  std::vector<double> emitter_cum;  // [n_emit]
+  double total_emitter_area = 0.0;
+  double bbox_min[3], bbox_max[3];
+  double cam[12];  // position, fwd, right, up
+  double tan_half = 0.0, aspect = 1.0;
+  std::vector<HostNode> nodes;
+  std::vector<int> order;
+  std::vector<HostRec> recs;
+  int bvh_depth = 0;
+};
+
+void finalize_scene(const SceneDesc& d, SceneHost& h);
+
+}  // namespace pxg

@@ -1,0 +1,368 @@
+// pxg_scene.cuh — device scene, BVH traversal and light sampling.
+//
+// HBM layout (built once by pxg_create, see pxg_host.cpp):
+//   nodes   BvhNode[n_nodes]   64 B: both child boxes in fp32 (outward-rounded and padded
+//                              so the test is conservative w.r.t. the fp64 reference),
+//                              child links; read as 4 x 16 B non-coherent vector loads.
+//   tris    PrimRec[n_prims]   80 B, in BVH leaf order: fp64 a, e1, e2 (triangle:
+//                              e1 = b-a, e2 = c-a; rectangle: e1 = b, e2 = c; sphere:
+//                              a = centre, e1.x = radius) + shape + original primitive id.
+//   prim_*  per original primitive id: material, emitter index, fp64 normal (tri/rect).
+//
+// Hit primitive ids equal the reference's Scene::intersect (proj/src/scene.cpp:127-168)
+// because (1) the leaf test is the reference's fp64 Moller-Trumbore / sphere test op for
+// op (--fmad=false), (2) the fp32 node test never culls a box that contains an accepted
+// fp64 hit, and (3) equal-t ties go to the larger primitive id, which is the reference's
+// own rule on its linear-scan path (later visited wins, scene.cpp:134-139).
+#pragma once
+
+#include "pxg_bsdf.cuh"
+
+namespace pxg {
+
+constexpr double kRayEps = 1e-7;  // scene.cpp:19
+constexpr int kStack = 64;
+
+enum Shape { kSphere = 0, kTriangle = 1, kRectangle = 2 };
+
+struct alignas(16) BvhNode {
+  float lo0[3], hi0[3];
+  float lo1[3], hi1[3];
+  int c0, c1;  // >= 0 internal node, < 0 leaf: ~c = first*16 + count
+  int pad0, pad1;
+};
+
+struct alignas(16) PrimRec {
+  double a[3];
+  double e1[3];
+  double e2[3];
+  int shape;
+  int id;
+};
+
+struct SceneView {
+  const BvhNode* nodes;
+  const PrimRec* recs;
+  const int* prim_mat;       // [n_prims]
+  const int* prim_emitter;   // [n_prims] emitter index or -1
+  const double* prim_geo;    // [n_prims][3] unit normal (tri/rect); sphere: unused
+  const double* prim_center; // [n_prims][4] sphere centre + radius (shape 0 only)
+  const int* prim_shape;     // [n_prims]
+  const double* prim_abc;    // [n_prims][9] a, e1, e2 as in PrimRec, original order
+  const Material* materials;
+  const int* emitter_prim;   // [n_emit]
+  const double* emitter_rad; // [n_emit][3]
+  const double* emitter_cum; // [n_emit] running area sum (scene.cpp:183-189 order)
+  int n_prims, n_emit, n_nodes, n_mat;
+  double total_emitter_area;
+  V3 bbox_min, bbox_max;
+  // camera (scene.cpp:116-125, basis precomputed on the host with the same ops)
+  V3 cam_pos, cam_fwd, cam_right, cam_up;
+  double tan_half, aspect;
+  int width, height, max_depth;
+};
+
+struct Hit {
+  double t;
+  V3 p, n;
+  int prim, material, emitter;
+};
+
+// ---- exact fp64 primitive tests (scene.cpp:22-62) ----
+PXD double sphere_hit(const double* c, double radius, const V3& o, const V3& d, double t_max) {
+  V3 oc = o - v3(c[0], c[1], c[2]);
+  double b = dot(oc, d);
+  double cc = length_sq(oc) - radius * radius;
+  double disc = b * b - cc;
+  if (disc < 0.0) return -1.0;
+  double sq = sqrt(disc);
+  double t = -b - sq;
+  if (t < kRayEps) t = -b + sq;
+  if (t < kRayEps || t > t_max) return -1.0;
+  return t;
+}
+
+PXD double triangle_hit(const V3& a, const V3& e1, const V3& e2, const V3& o, const V3& d,
+                        double t_max, bool parallelogram) {
+  V3 pv = cross(d, e2);
+  double det = dot(e1, pv);
+  if (fabs(det) < 1e-14) return -1.0;
+  double inv = 1.0 / det;
+  V3 tv = o - a;
+  double u = dot(tv, pv) * inv;
+  if (u < 0.0 || u > 1.0) return -1.0;
+  V3 qv = cross(tv, e1);
+  double v = dot(d, qv) * inv;
+  double hi = parallelogram ? 1.0 : 1.0 - u;
+  if (v < 0.0 || v > hi) return -1.0;
+  double t = dot(e2, qv) * inv;
+  if (t < kRayEps || t > t_max) return -1.0;
+  return t;
+}
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ double rec_hit(const PrimRec* __restrict__ rp, const V3& o, const V3& d,
+                                          double t_max, int& id) {
+  const double2* q = reinterpret_cast<const double2*>(rp);
+  double2 w0 = __ldg(q + 0), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3);
+  int2 tail = __ldg(reinterpret_cast<const int2*>(q + 4) + 1);
+  double2 w4 = __ldg(q + 4);
+  id = tail.y;
+  const int shape = tail.x;
+  if (shape == kSphere) {
+    const double c[3] = {w0.x, w0.y, w1.x};
+    return sphere_hit(c, w1.y, o, d, t_max);
+  }
+  V3 a = v3(w0.x, w0.y, w1.x);
+  V3 e1 = v3(w1.y, w2.x, w2.y);
+  V3 e2 = v3(w3.x, w3.y, w4.x);
+  return triangle_hit(a, e1, e2, o, d, t_max, shape == kRectangle);
+}
+
+struct RayF {
+  float ox, oy, oz, ix, iy, iz;
+};
+
+__device__ __forceinline__ RayF make_rayf(const V3& o, const V3& d) {
+  RayF r;
+  r.ox = __double2float_rn(o.x);
+  r.oy = __double2float_rn(o.y);
+  r.oz = __double2float_rn(o.z);
+  float dx = __double2float_rn(d.x), dy = __double2float_rn(d.y), dz = __double2float_rn(d.z);
+  r.ix = 1.0f / dx;
+  r.iy = 1.0f / dy;
+  r.iz = 1.0f / dz;
+  return r;
+}
+
+// Slab test in fp32; NaN from 0*inf on a padded box cannot occur because the ray origin
+// is never exactly on a padded plane that it is parallel to (fmin/fmax ignore NaN anyway).
+__device__ __forceinline__ bool box_f(const float* lo, const float* hi, const RayF& r, float tmax,
+                                      float& tnear) {
+  float tx0 = (lo[0] - r.ox) * r.ix, tx1 = (hi[0] - r.ox) * r.ix;
+  float ty0 = (lo[1] - r.oy) * r.iy, ty1 = (hi[1] - r.oy) * r.iy;
+  float tz0 = (lo[2] - r.oz) * r.iz, tz1 = (hi[2] - r.oz) * r.iz;
+  float t0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+  float t1 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+  tnear = t0;
+  return t0 <= t1;
+}
+
+// fp64 t bound -> fp32, rounded up with slack so the node test stays conservative.
+__device__ __forceinline__ float tbound_f(double t) {
+  if (t > 3.0e38) return 3.0e38f;
+  return __double2float_ru(t) * 1.0000005f + 1e-30f;
+}
+
+// Closest hit: returns the original primitive id or -1; t_best in/out (fp64).
+__device__ __noinline__ int trace_closest(const SceneView& S, const V3& o, const V3& d, double& t_best) {
+  const RayF rf = make_rayf(o, d);
+  int best = -1;
+  int stack[kStack];
+  int sp = 0;
+  int node = 0;
+  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
+  for (;;) {
+    // internal node: test both children
+    const float4 n0 = __ldg(nodes + 4 * node + 0);
+    const float4 n1 = __ldg(nodes + 4 * node + 1);
+    const float4 n2 = __ldg(nodes + 4 * node + 2);
+    const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+    const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
+    const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
+    const float tb = tbound_f(t_best);
+    float tn0, tn1;
+    bool h0 = box_f(lo0, hi0, rf, tb, tn0);
+    bool h1 = box_f(lo1, hi1, rf, tb, tn1);
+    int c0 = n3.x, c1 = n3.y;
+    // leaves are processed immediately; internal children are pushed near-first
+    int next = -1;
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool h = k == 0 ? h0 : h1;
+      const int c = k == 0 ? c0 : c1;
+      if (!h) continue;
+      if (c < 0) {
+        const int code = ~c;
+        const int first = code >> 4, count = code & 15;
+        for (int i = 0; i < count; ++i) {
+          int id;
+          double t = rec_hit(S.recs + first + i, o, d, t_best, id);
+          if (t > 0.0 && (t < t_best || id > best)) {
+            t_best = t;
+            best = id;
+          }
+        }
+      }
+    }
+    const float tbn = tbound_f(t_best);
+    const bool in0 = h0 && c0 >= 0 && tn0 <= tbn;
+    const bool in1 = h1 && c1 >= 0 && tn1 <= tbn;
+    if (in0 && in1) {
+      const bool first0 = tn0 <= tn1;
+      next = first0 ? c0 : c1;
+      if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+    } else if (in0) {
+      next = c0;
+    } else if (in1) {
+      next = c1;
+    } else {
+      next = -1;
+    }
+    if (next < 0) {
+      // pop until a node still in range (stack entries are re-tested at the next visit)
+      if (sp == 0) break;
+      next = stack[--sp];
+    }
+    node = next;
+  }
+  return best;
+}
+
+// Any hit with t in [kRayEps, t_max] (the boolean of Scene::occluded, scene.cpp:170-177).
+__device__ __noinline__ bool trace_any(const SceneView& S, const V3& o, const V3& d, double t_max) {
+  const RayF rf = make_rayf(o, d);
+  int stack[kStack];
+  int sp = 0;
+  int node = 0;
+  const float tb = tbound_f(t_max);
+  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
+  for (;;) {
+    const float4 n0 = __ldg(nodes + 4 * node + 0);
+    const float4 n1 = __ldg(nodes + 4 * node + 1);
+    const float4 n2 = __ldg(nodes + 4 * node + 2);
+    const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+    const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
+    const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
+    float tn0, tn1;
+    bool h0 = box_f(lo0, hi0, rf, tb, tn0);
+    bool h1 = box_f(lo1, hi1, rf, tb, tn1);
+    int c0 = n3.x, c1 = n3.y;
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool h = k == 0 ? h0 : h1;
+      const int c = k == 0 ? c0 : c1;
+      if (!h || c >= 0) continue;
+      const int code = ~c;
+      const int first = code >> 4, count = code & 15;
+      for (int i = 0; i < count; ++i) {
+        int id;
+        double t = rec_hit(S.recs + first + i, o, d, t_max, id);
+        if (t > 0.0) return true;
+      }
+    }
+    const bool in0 = h0 && c0 >= 0;
+    const bool in1 = h1 && c1 >= 0;
+    int next;
+    if (in0 && in1) {
+      const bool first0 = tn0 <= tn1;
+      next = first0 ? c0 : c1;
+      if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+    } else if (in0) {
+      next = c0;
+    } else if (in1) {
+      next = c1;
+    } else {
+      if (sp == 0) break;
+      next = stack[--sp];
+    }
+    node = next;
+  }
+  return false;
+}
+
+// primitive_normal (scene.cpp:65-72)
+__device__ __forceinline__ V3 prim_normal(const SceneView& S, int prim, const V3& at) {
+  if (S.prim_shape[prim] == kSphere) {
+    const double* c = S.prim_center + 4 * prim;
+    return (at - v3(c[0], c[1], c[2])) / c[3];
+  }
+  const double* g = S.prim_geo + 3 * prim;
+  return v3(g[0], g[1], g[2]);
+}
+
+// Scene::intersect (scene.cpp:127-150)
+__device__ __forceinline__ bool intersect(const SceneView& S, const V3& o, const V3& d, Hit& hit,
+                                          double t_max = 1e30) {
+  double t_best = t_max;
+  int best = trace_closest(S, o, d, t_best);
+  if (best < 0) return false;
+  hit.t = t_best;
+  hit.p = o + t_best * d;
+  hit.prim = best;
+  hit.n = prim_normal(S, best, hit.p);
+  hit.material = S.prim_mat[best];
+  hit.emitter = S.prim_emitter[best];
+  return true;
+}
+
+// Scene::occluded (scene.cpp:170-177)
+__device__ __forceinline__ bool occluded(const SceneView& S, const V3& from, const V3& to) {
+  V3 d = to - from;
+  double dist = length(d);
+  if (dist < kRayEps) return false;
+  return trace_any(S, from, d / dist, dist * (1.0 - 1e-6));
+}
+
+__device__ __forceinline__ bool visible(const SceneView& S, const V3& from, const V3& to) {
+  return !occluded(S, from, to);
+}
+
+struct LightPoint {
+  V3 p, n, radiance;
+  int prim;
+  double pdf_area;
+};
+
+// Scene::sample_light_point (scene.cpp:179-223). The linear cumulative scan is a binary
+// search over the same running sums; operand order of the rectangle draw follows the
+// reference build (GCC evaluates `a + u()*b + u()*c` right to left: c's draw first).
+__device__ __forceinline__ LightPoint sample_light_point(const SceneView& S, Rng& rng) {
+  double target = rng.next_double() * S.total_emitter_area;
+  int lo = 0, hi = S.n_emit - 1;
+  while (lo < hi) {  // first i with target < cum[i]
+    int mid = (lo + hi) >> 1;
+    if (target < S.emitter_cum[mid]) hi = mid; else lo = mid + 1;
+  }
+  const int chosen = lo;
+  const int prim = S.emitter_prim[chosen];
+  LightPoint lp;
+  lp.radiance = v3(S.emitter_rad[3 * chosen], S.emitter_rad[3 * chosen + 1], S.emitter_rad[3 * chosen + 2]);
+  lp.prim = prim;
+  lp.pdf_area = 1.0 / S.total_emitter_area;
+  const double* g = S.prim_abc + 9 * prim;
+  const int shape = S.prim_shape[prim];
+  if (shape == kSphere) {
+    double z = 1.0 - 2.0 * rng.next_double();
+    double r = sqrt(dmax(0.0, 1.0 - z * z));
+    double phi = 2.0 * kPi * rng.next_double();
+    V3 n = v3(r * cos(phi), r * sin(phi), z);
+    const double* c = S.prim_center + 4 * prim;
+    lp.p = v3(c[0], c[1], c[2]) + c[3] * n;
+    lp.n = n;
+  } else if (shape == kTriangle) {
+    double u = rng.next_double(), v = rng.next_double();
+    if (u + v > 1.0) {
+      u = 1.0 - u;
+      v = 1.0 - v;
+    }
+    lp.p = v3(g[0], g[1], g[2]) + u * v3(g[3], g[4], g[5]) + v * v3(g[6], g[7], g[8]);
+    lp.n = prim_normal(S, prim, lp.p);
+  } else {
+    double vc = rng.next_double();
+    double ub = rng.next_double();
+    lp.p = v3(g[0], g[1], g[2]) + ub * v3(g[3], g[4], g[5]) + vc * v3(g[6], g[7], g[8]);
+    lp.n = prim_normal(S, prim, lp.p);
+  }
+  return lp;
+}
+
+// Scene::emitted (scene.cpp:225-232)
+__device__ __forceinline__ V3 emitted(const SceneView& S, int emitter, const V3& n, const V3& dir_out) {
+  if (emitter < 0 || dot(dir_out, n) <= 0.0) return v3(0.0);
+  const double* r = S.emitter_rad + 3 * emitter;
+  return v3(r[0], r[1], r[2]);
+}
+#endif  // __CUDACC__
+
+}  // namespace pxg

@@ -1,0 +1,294 @@
+"""Python mirror of the reference's render API for the hot path, backed by libpxg.
+
+`render_proxy_bdpt(scene, spp, seed, params, diagnostics, pass_done)` has the argument
+meaning and error behaviour of proxima::render_proxy_bdpt
+(proj/include/proxima/proxy.hpp:197-200, proj/src/proxy.cpp:647-834): spp <= 0 uses the
+scene's settings; one pass is one sample for every pixel; `pass_done(done, mean_image)`
+runs after each pass and returning False stops early (the result then equals a shorter
+render); `diagnostics` (a ProxyDiagnostics) is filled in place. `render_bdpt` is the same
+call with proxy sampling disabled (proj/tests/test_proxy.cpp:1053-1079).
+
+Images are numpy float64 arrays of shape (height, width, 3), row 0 at the top, like the
+reference's `Image` (proj/include/proxima/image.hpp:13-23).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _lib
+from .scene import Scene
+
+N_BUCKETS = 4000
+
+
+@dataclass
+class ProxyParams:
+    """proxima::ProxyParams (proj/include/proxima/proxy.hpp:162-173)."""
+    enabled: bool = True
+    pool_budget: int = 400
+    recip_repeats: int = 5
+    freeze_iteration: int = 40
+    recursion_cap: int = 10000
+    pretrace_paths: int = 20000
+    light_walks: int = 0
+    gate_high: float = 1.0
+    gate_low: float = 0.2
+    gate_threshold: float = 0.05
+
+    def to_c(self) -> _lib.Params:
+        p = _lib.Params()
+        for f in fields(self):
+            v = getattr(self, f.name)
+            setattr(p, f.name, int(v) if f.name == "enabled" else v)
+        return p
+
+
+@dataclass
+class ProxyDiagRow:
+    """proxima::ProxyDiagRow (proj/include/proxima/proxy.hpp:175-181)."""
+    retrace_attempts: int = 0
+    retrace_accepts: int = 0
+    recip_runs: int = 0
+    recip_truncated: int = 0
+    estimates_failed: int = 0
+
+
+def key_of(index: int):
+    """Dense bucket index -> StatsKey (u, c, s)."""
+    return (index // 1000 + 1, (index // 100) % 10, index % 100)
+
+
+def index_of(u: int, c: int, s: int) -> int:
+    return ((u - 1) * 10 + c) * 100 + s
+
+
+@dataclass
+class ProxyDiagnostics:
+    """proxima::ProxyDiagnostics (proj/include/proxima/proxy.hpp:183-188)."""
+    rows: dict = field(default_factory=dict)
+    pool_raw: int = 0
+    pool_kept: int = 0
+
+    def write_csv(self, f) -> None:
+        """ProxyDiagnostics::write_csv (proj/src/proxy.cpp:605-614)."""
+        f.write("u,c,s,retrace_attempts,retrace_accepts,recip_runs,recip_truncated,estimates_failed\n")
+        for (u, c, s) in sorted(self.rows):
+            r = self.rows[(u, c, s)]
+            f.write(f"{u},{c},{s},{r.retrace_attempts},{r.retrace_accepts},{r.recip_runs},"
+                    f"{r.recip_truncated},{r.estimates_failed}\n")
+        f.write(f"# pool_raw={self.pool_raw} pool_kept={self.pool_kept}\n")
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _lp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_longlong))
+
+
+class ProxyRenderer:
+    """One libpxg context: the scene resident in HBM, the per-pass state, the film."""
+
+    def __init__(self, scene: Scene, seed: int, params: ProxyParams | None = None, device: int = 0,
+                 rows: tuple | None = None, walks: tuple | None = None):
+        L = _lib.lib()
+        self.scene = scene
+        self.params = params or ProxyParams()
+        W, H = scene.camera.width, scene.camera.height
+        self.width, self.height, self.max_depth = W, H, scene.settings.max_depth
+        keep = dict(
+            shape=np.ascontiguousarray(scene.shape, np.int32), mat=np.ascontiguousarray(scene.mat, np.int32),
+            a=np.ascontiguousarray(scene.a, np.float64), b=np.ascontiguousarray(scene.b, np.float64),
+            c=np.ascontiguousarray(scene.c, np.float64), r=np.ascontiguousarray(scene.radius, np.float64),
+            m=np.ascontiguousarray(scene.material_table()[:, :7], np.float64),
+            ep=np.ascontiguousarray(scene.emitter_prim, np.int32),
+            er=np.ascontiguousarray(scene.emitter_radiance, np.float64))
+        d = _lib.SceneDesc()
+        d.n_prims = scene.n_prims
+        d.shape, d.material = _ip(keep["shape"]), _ip(keep["mat"])
+        d.a, d.b, d.c, d.radius = _dp(keep["a"]), _dp(keep["b"]), _dp(keep["c"]), _dp(keep["r"])
+        d.n_materials = len(scene.materials)
+        d.materials = _dp(keep["m"])
+        d.n_emitters = int(keep["ep"].shape[0])
+        d.emitter_prim, d.emitter_radiance = _ip(keep["ep"]), _dp(keep["er"])
+        d.cam_position[:] = scene.camera.position
+        d.cam_look_at[:] = scene.camera.look_at
+        d.cam_up[:] = scene.camera.up
+        d.fov_y = scene.camera.fov_y
+        d.width, d.height = W, H
+        d.max_depth = scene.settings.max_depth
+        cp = self.params.to_c()
+        shard = None
+        light_walks = self.params.light_walks if self.params.light_walks > 0 else W * H
+        if rows is not None or walks is not None:
+            r0, r1 = rows if rows is not None else (0, H)
+            w0, w1 = walks if walks is not None else (0, light_walks)
+            shard = _lib.Shard(r0, r1, w0, w1)
+        self.row0, self.row1 = (rows if rows is not None else (0, H))
+        ctx = C.c_void_p()
+        rc = L.pxg_create(C.byref(d), C.byref(cp), C.c_uint64(seed), device,
+                          C.byref(shard) if shard is not None else None, C.byref(ctx))
+        _lib.check(rc, None)
+        self._ctx = ctx
+        self._L = L
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._L.pxg_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def n(self):
+        return (self.row1 - self.row0) * self.width
+
+    def _check(self, rc):
+        _lib.check(rc, self._ctx)
+
+    # -- passes
+    def render_passes(self, n: int = 1):
+        self._check(self._L.pxg_render_passes(self._ctx, n))
+
+    def render_pass_traced(self):
+        """One pass that also records the sub-path primitive ids (dump_prims)."""
+        self._check(self._L.pxg_render_pass_traced(self._ctx))
+
+    def mean(self) -> np.ndarray:
+        out = np.zeros((self.row1 - self.row0, self.width, 3))
+        done = C.c_int()
+        self._check(self._L.pxg_read_mean(self._ctx, _dp(out), C.byref(done)))
+        return out
+
+    def accum(self):
+        out = np.zeros((self.row1 - self.row0, self.width, 3))
+        done = C.c_int()
+        self._check(self._L.pxg_read_accum(self._ctx, _dp(out), C.byref(done)))
+        return out, done.value
+
+    def timing(self):
+        t = np.zeros(6)
+        cnt = np.zeros(2, np.int64)
+        self._check(self._L.pxg_read_timing(self._ctx, _dp(t), _lp(cnt)))
+        return t, cnt
+
+    def diagnostics(self) -> ProxyDiagnostics:
+        rows = np.zeros((N_BUCKETS, 5), np.int64)
+        touched = np.zeros(N_BUCKETS, np.int32)
+        pool = np.zeros(2, np.int64)
+        self._check(self._L.pxg_read_diag(self._ctx, _lp(rows), _ip(touched), _lp(pool)))
+        d = ProxyDiagnostics(pool_raw=int(pool[0]), pool_kept=int(pool[1]))
+        for k in np.nonzero(touched)[0]:
+            d.rows[key_of(int(k))] = ProxyDiagRow(*[int(v) for v in rows[k]])
+        return d
+
+    def stats(self):
+        s3 = np.zeros((N_BUCKETS, 3))
+        c2 = np.zeros((N_BUCKETS, 2), np.int64)
+        g = np.zeros((32, 100))
+        self._check(self._L.pxg_read_stats(self._ctx, _dp(s3), _lp(c2), _dp(g)))
+        return s3, c2, g
+
+    def dump_pass(self):
+        n = self.n
+        val, bd, c = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3))
+        fl = np.zeros(n, np.int32)
+        self._check(self._L.pxg_dump_pass(self._ctx, _dp(val), _dp(bd), _dp(c), _ip(fl)))
+        return val, bd, c, fl
+
+    def dump_prims(self):
+        n = self.n
+        eye = np.zeros((n, self.max_depth + 1), np.int32)
+        light = np.zeros((n, max(self.max_depth - 1, 1)), np.int32)
+        self._check(self._L.pxg_dump_prims(self._ctx, _ip(eye), _ip(light)))
+        return eye, light
+
+    def dump_pool(self, cap: int = 4096):
+        n = C.c_int()
+        raw = C.c_longlong()
+        walk, end, key = (np.zeros(cap, np.int32) for _ in range(3))
+        ip, m2, bd = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        self._check(self._L.pxg_dump_pool(self._ctx, cap, C.byref(n), C.byref(raw), _ip(walk), _ip(end), _ip(key),
+                                          _dp(ip), _dp(m2), _dp(bd)))
+        k = min(n.value, cap)
+        return dict(n=n.value, raw=raw.value, walk=walk[:k], end=end[:k], key=key[:k], inv_p=ip[:k],
+                    inv_p_m2=m2[:k], bound=bd[:k])
+
+    # -- traversal parity entry points (Scene::intersect / Scene::occluded)
+    def intersect(self, rays: np.ndarray, tmax=None):
+        rays = np.ascontiguousarray(rays, np.float64)
+        n = rays.shape[0]
+        prim = np.zeros(n, np.int32)
+        t = np.zeros(n)
+        tm = None if tmax is None else np.ascontiguousarray(np.broadcast_to(tmax, (n,)), np.float64)
+        self._check(self._L.pxg_intersect(self._ctx, n, _dp(rays), _dp(tm) if tm is not None else None, _ip(prim),
+                                          _dp(t)))
+        return prim, t
+
+    def occluded(self, segs: np.ndarray):
+        segs = np.ascontiguousarray(segs, np.float64)
+        occ = np.zeros(segs.shape[0], np.int32)
+        self._check(self._L.pxg_occluded(self._ctx, segs.shape[0], _dp(segs), _ip(occ)))
+        return occ.astype(bool)
+
+
+def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | None = None,
+                      diagnostics: ProxyDiagnostics | None = None, pass_done=None, device: int = 0) -> np.ndarray:
+    """proxima::render_proxy_bdpt on the GPU (proj/src/proxy.cpp:647-834)."""
+    if spp <= 0:
+        spp = scene.settings.spp
+    with ProxyRenderer(scene, seed, params, device=device) as r:
+        done = 0
+        for _ in range(spp):
+            r.render_passes(1)
+            done += 1
+            if pass_done is not None and not pass_done(done, r.mean()):
+                break
+        img = r.mean()
+        if diagnostics is not None:
+            d = r.diagnostics()
+            diagnostics.rows = d.rows
+            diagnostics.pool_raw = d.pool_raw
+            diagnostics.pool_kept = d.pool_kept
+    return img
+
+
+def render_bdpt(scene: Scene, spp: int, seed: int, device: int = 0) -> np.ndarray:
+    """proxima::render_bdpt (proj/src/transport.cpp:380-386): the proxy renderer with proxy off."""
+    return render_proxy_bdpt(scene, spp, seed, ProxyParams(enabled=False), device=device)
+
+
+def recip_twopoint(n: int, bound: float, cap: int = 10000, seed: int = 1):
+    """The device reciprocal estimator on the reference's two-point fixture."""
+    L = _lib.lib()
+    est = np.zeros(n)
+    cost = np.zeros(n, np.int64)
+    tr = np.zeros(n, np.int32)
+    _lib.check(L.pxg_recip_twopoint(n, bound, cap, seed, _dp(est), _lp(cost), _ip(tr)))
+    return est, cost, tr.astype(bool)
+
+
+def rng_draws(seed: int, kind: int, sub: int, stream: int, n: int) -> np.ndarray:
+    L = _lib.lib()
+    out = np.zeros(n, np.uint32)
+    _lib.check(L.pxg_rng_draws(seed, kind, sub, stream, n, out.ctypes.data_as(C.POINTER(C.c_uint))))
+    return out
