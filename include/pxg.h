@@ -148,9 +148,12 @@ int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double
 /* Philox stream check: first n draws of stream (seed, kind, sub, stream) computed on the device. */
 int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out);
 
-/* Device time of the kernels of the last pxg_render_passes call, by stage (ms):
- * t[0] stage-1 pool, t[1] reciprocal runs, t[2] sub-path trace, t[3] connections,
- * t[4] proxy connection, t[5] gate+film; counts[0] kernel launches, counts[1] rays traced. */
+/* Device timeline of the last pxg_render_passes call (ms, CUDA events on the context's
+ * stream): t[0] stage 1 (pool walks, selection, probes, reciprocal runs, incl. the host
+ * round trip of the selection), t[1] reciprocal runs alone, t[2] sub-path trace,
+ * t[3] connections + MIS, t[4] proxy connection, t[5] gate + film, t[6] the whole call
+ * (first pass start to last pass end, including host gaps), t[7] reserved.
+ * counts[0] = kernel launches, counts[1] reserved. t holds 8 doubles. */
 int pxg_read_timing(pxg_ctx* ctx, double* t, long long* counts);
 
 #ifdef __cplusplus

@@ -608,7 +608,8 @@ struct pxg_ctx {
   long long last_raw = 0;
   // timing
   cudaEvent_t ev[8];
-  double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+  cudaEvent_t ev_call[2];
+  double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
 
   template <typename T>
@@ -718,6 +719,7 @@ void stage1(pxg_ctx* c, int pass) {
   ps_host.kappa = raw > 0 ? std::min(1.0, static_cast<double>(budget) / static_cast<double>(raw)) : 1.0;
   CK(cudaMemcpyAsync(&c->d_ps->kappa, &ps_host.kappa, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   const int R = c->P.recip_repeats;
+  bool ran_recip = false;
   if (n_ent > 0) {
     k_pool_entries<<<blocks(n_ent, 64), 64, 0, c->stream>>>(c->S, c->M, c->seed, pass, n_ent, c->d_sel, c->d_inc,
                                                            c->d_inc_prefix, c->d_probe, c->d_probe_ok, R);
@@ -731,7 +733,12 @@ void stage1(pxg_ctx* c, int pass) {
           c->d_run_cost, c->d_run_trunc, c->d_frames, c->d_err);
       CK(cudaEventRecord(c->ev[3], c->stream));
       ++c->launches;
+      ran_recip = true;
     }
+  }
+  if (!ran_recip) {
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    CK(cudaEventRecord(c->ev[3], c->stream));
   }
   k_pool_finish<<<1, 1, 0, c->stream>>>(n_ent, R, c->d_inc, c->d_bound, c->d_run_est, c->d_run_trunc, c->d_sum_est,
                                         c->d_sum_sq, c->d_est_cnt, c->d_touched, c->d_diag, c->d_diag_touched,
@@ -746,6 +753,8 @@ void render_pass(pxg_ctx* c, bool record_prims) {
     stage1(c, pass);
   } else {
     CK(cudaMemsetAsync(&c->d_ps->n_kept, 0, sizeof(int), c->stream));
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    CK(cudaEventRecord(c->ev[3], c->stream));
   }
   CK(cudaEventRecord(c->ev[1], c->stream));
   Stage2 P;
@@ -807,16 +816,22 @@ void render_pass(pxg_ctx* c, bool record_prims) {
 }
 
 void accumulate_timing(pxg_ctx* c) {
-  float ms[7];
-  for (int k = 0; k < 7; ++k) {
-    ms[k] = 0.f;
-    cudaEventElapsedTime(&ms[k], c->ev[k], c->ev[k + 1]);
-  }
-  c->stage_ms[0] += ms[0];
-  c->stage_ms[2] += ms[3];
-  c->stage_ms[3] += ms[4];
-  c->stage_ms[4] += ms[5];
-  c->stage_ms[5] += ms[6];
+  // ev0 pass start, ev2/ev3 around the reciprocal runs (inside stage 1), ev1 stage-1 end,
+  // ev4 trace end, ev5 connect end, ev6 proxy end, ev7 gate end.
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    return static_cast<double>(ms);
+  };
+  c->stage_ms[0] += el(0, 1);
+  c->stage_ms[1] += el(2, 3);
+  c->stage_ms[2] += el(1, 4);
+  c->stage_ms[3] += el(4, 5);
+  c->stage_ms[4] += el(5, 6);
+  c->stage_ms[5] += el(6, 7);
 }
 
 int fail(pxg_ctx* c, int code, const std::string& msg) {
@@ -891,6 +906,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->seed = seed;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
     finalize_scene(*sd, c->host);
     SceneHost& h = c->host;
     c->width = sd->width;
@@ -1042,14 +1058,20 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
 int pxg_render_passes(pxg_ctx* c, int npass) {
   if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
   return guarded(c, [&]() {
-    for (int k = 0; k < 6; ++k) c->stage_ms[k] = 0.0;
+    for (int k = 0; k < 8; ++k) c->stage_ms[k] = 0.0;
     c->launches = 0;
+    CK(cudaEventRecord(c->ev_call[0], c->stream));
     for (int p = 0; p < npass; ++p) {
       render_pass(c, false);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(c->stream));
       accumulate_timing(c);
     }
+    CK(cudaEventRecord(c->ev_call[1], c->stream));
+    CK(cudaEventSynchronize(c->ev_call[1]));
+    float total = 0.f;
+    CK(cudaEventElapsedTime(&total, c->ev_call[0], c->ev_call[1]));
+    c->stage_ms[6] = total;
     check_err(c);
   });
 }
@@ -1256,7 +1278,7 @@ int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, i
 
 int pxg_read_timing(pxg_ctx* c, double* t, long long* counts) {
   if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
-  for (int k = 0; k < 6; ++k) t[k] = c->stage_ms[k];
+  for (int k = 0; k < 8; ++k) t[k] = c->stage_ms[k];
   if (counts) {
     counts[0] = c->launches;
     counts[1] = 0;

@@ -27,6 +27,77 @@ struct IncView {
   const PV* prefix;  // [entry][kMaxLight]
 };
 
+// Errors raised by the estimator (the reference throws std::runtime_error).
+enum { kErrNone = 0, kErrIntegrand = 1, kErrSupport = 2, kErrSplit = 3, kErrRatio = 4 };
+
+struct RecipFrame {
+  double ans;
+  double sgn;
+  long long rem;
+};
+
+// recip::estimate_reciprocal (recip.hpp:131-138) with main_tree (:89-97) unrolled onto an
+// explicit frame stack, so the DFS visits nodes, draws numbers and nests the partial sums
+// exactly like the recursion: frame d holds ans = g/B (+ sgn * child values so far) and
+// the number of children still to expand.
+template <typename DrawG>
+PXD double reciprocal_run(DrawG&& draw, double bound, long long cap, Rng& rng,
+                                                 RecipFrame* frames, long long& cost, bool& truncated, int& err) {
+  cost = 0;
+  truncated = false;
+  long long depth = 0;
+  double ret = 0.0;
+  bool entering = true;
+  for (;;) {
+    if (entering) {
+      entering = false;
+      if (depth >= cap || cost >= cap) {
+        truncated = true;
+        ret = 0.0;
+      } else {
+        double g = draw(rng);
+        ++cost;
+        if (err) return 0.0;
+        RecipFrame fr;
+        fr.ans = g / bound;
+        fr.sgn = static_cast<double>((g > 0.0) - (g < 0.0));
+        const double r = fabs(g);
+        if (!(r >= 0.0) || !isfinite(r)) {
+          err = kErrSplit;
+          return 0.0;
+        }
+        const double fl = floor(r);
+        const double frac = r - fl;
+        long long n = static_cast<long long>(fl);
+        if (frac > 0.0 && rng.bernoulli(frac)) ++n;
+        fr.rem = n;
+        frames[depth] = fr;
+        // fall through to "next child" at this depth
+        if (fr.rem > 0) {
+          frames[depth].rem = fr.rem - 1;
+          ++depth;
+          entering = true;
+          continue;
+        }
+        ret = fr.ans;
+      }
+    }
+    // return `ret` from node at `depth` to its parent
+    if (depth == 0) break;
+    --depth;
+    RecipFrame& pf = frames[depth];
+    pf.ans += pf.sgn * ret;
+    if (pf.rem > 0) {
+      pf.rem -= 1;
+      ++depth;
+      entering = true;
+      continue;
+    }
+    ret = pf.ans;
+  }
+  return 1.0 / bound + ret;
+}
+
 #if defined(__CUDACC__)
 
 __device__ __forceinline__ const PV* inc_control(const IncHdr& h, const PV* prefix) {
@@ -267,8 +338,6 @@ __device__ __forceinline__ double target_density(const SceneView& S, const IncHd
   return f;
 }
 
-// Errors raised by the estimator (the reference throws std::runtime_error).
-enum { kErrNone = 0, kErrIntegrand = 1, kErrSupport = 2, kErrSplit = 3, kErrRatio = 4 };
 
 // recip::Walk::draw_g (recip.hpp:69-77) for the proxy integrand.
 __device__ __forceinline__ double draw_g(const SceneView& S, const IncHdr& h, const PV* prefix, double bound,
@@ -280,74 +349,6 @@ __device__ __forceinline__ double draw_g(const SceneView& S, const IncHdr& h, co
   if (!isfinite(fx) || fx < 0.0) err = kErrIntegrand;
   else if (!isfinite(qx) || qx <= 0.0) err = kErrSupport;
   return 1.0 - fx / (bound * qx);
-}
-
-struct RecipFrame {
-  double ans;
-  double sgn;
-  long long rem;
-};
-
-// recip::estimate_reciprocal (recip.hpp:131-138) with main_tree (:89-97) unrolled onto an
-// explicit frame stack, so the DFS visits nodes, draws numbers and nests the partial sums
-// exactly like the recursion: frame d holds ans = g/B (+ sgn * child values so far) and
-// the number of children still to expand.
-template <typename DrawG>
-__device__ __forceinline__ double reciprocal_run(DrawG&& draw, double bound, long long cap, Rng& rng,
-                                                 RecipFrame* frames, long long& cost, bool& truncated, int& err) {
-  cost = 0;
-  truncated = false;
-  long long depth = 0;
-  double ret = 0.0;
-  bool entering = true;
-  for (;;) {
-    if (entering) {
-      if (depth >= cap || cost >= cap) {
-        truncated = true;
-        ret = 0.0;
-      } else {
-        double g = draw(rng);
-        ++cost;
-        if (err) return 0.0;
-        RecipFrame fr;
-        fr.ans = g / bound;
-        fr.sgn = static_cast<double>((g > 0.0) - (g < 0.0));
-        const double r = fabs(g);
-        if (!(r >= 0.0) || !isfinite(r)) {
-          err = kErrSplit;
-          return 0.0;
-        }
-        const double fl = floor(r);
-        const double frac = r - fl;
-        long long n = static_cast<long long>(fl);
-        if (frac > 0.0 && rng.bernoulli(frac)) ++n;
-        fr.rem = n;
-        frames[depth] = fr;
-        entering = false;
-        // fall through to "next child" at this depth
-        if (fr.rem > 0) {
-          frames[depth].rem = fr.rem - 1;
-          ++depth;
-          entering = true;
-          continue;
-        }
-        ret = fr.ans;
-      }
-    }
-    // return `ret` from node at `depth` to its parent
-    if (depth == 0) break;
-    --depth;
-    RecipFrame& pf = frames[depth];
-    pf.ans += pf.sgn * ret;
-    if (pf.rem > 0) {
-      pf.rem -= 1;
-      ++depth;
-      entering = true;
-      continue;
-    }
-    ret = pf.ans;
-  }
-  return 1.0 / bound + ret;
 }
 
 // retrace_proxy (proxy.cpp:271-319). g receives u vertices; returns density (> 0) or 0.

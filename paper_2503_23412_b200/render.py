@@ -186,7 +186,7 @@ class ProxyRenderer:
         return out, done.value
 
     def timing(self):
-        t = np.zeros(6)
+        t = np.zeros(8)
         cnt = np.zeros(2, np.int64)
         self._check(self._L.pxg_read_timing(self._ctx, _dp(t), _lp(cnt)))
         return t, cnt

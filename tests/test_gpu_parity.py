@@ -198,7 +198,8 @@ def test_pretrace_matches_oracle(pxg, oracle):
     with ProxyRenderer(sc, 3, ProxyParams(pretrace_paths=20000, light_walks=100)) as r:
         s3, c2, _ = r.stats()
     assert np.array_equal(c2[:, 0], run.pretrace_cnt)
-    assert np.array_equal(s3[:, 0], run.pretrace_max)
+    # maxima agree to rounding (sin/cos of CUDA vs glibc differ by <= 2 ulp)
+    assert np.allclose(s3[:, 0], run.pretrace_max, rtol=1e-9, atol=0)
 
 
 def test_recip_two_point_on_device(pxg, oracle):
