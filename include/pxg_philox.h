@@ -33,8 +33,18 @@ enum {
   PXG_KIND_RESERVOIR = 2,  /* stream = pass<<32 | walk, sub = prefix end      */
   PXG_KIND_PROBE = 3,      /* stream = pass<<32 | walk, sub = prefix end      */
   PXG_KIND_RECIP = 4,      /* stream = pass<<32 | walk, sub = end | run << 8  */
-  PXG_KIND_PRETRACE = 5    /* stream = walk                                   */
+  PXG_KIND_PRETRACE = 5,   /* stream = walk                                   */
+  PXG_KIND_RECIP_NODE = 6, /* sub = tree node (DFS pre-order), stream = pxg_recip_stream() */
+  PXG_KIND_RECIP_SPLIT = 7 /* sub = tree node, stream = pxg_recip_stream()     */
 };
+
+/* Stream of reciprocal run `run` of pool entry (pass, walk, end). Node k of the run's
+ * Russian-roulette-and-split tree draws its support sample from (RECIP_NODE, k) and its
+ * split decision from (RECIP_SPLIT, k), so every node can be evaluated independently of
+ * the tree shape. Limits: pass < 2^24, walk < 2^27, end < 32, run < 256, k < 2^24. */
+PXG_HD uint64_t pxg_recip_stream(uint32_t pass, uint32_t walk, uint32_t end, uint32_t run) {
+  return ((uint64_t)pass << 40) | ((uint64_t)walk << 13) | ((uint64_t)(end & 31u) << 8) | (uint64_t)(run & 255u);
+}
 
 PXG_HD uint32_t pxg_mulhilo32(uint32_t a, uint32_t b, uint32_t* hi) {
 #if defined(__CUDA_ARCH__)

@@ -491,15 +491,26 @@ ORC_API int orc_render(void* h, int spp, unsigned long long seed, const OrcParam
           recip::IntegrandOracle<SupportCandidate> f_oracle = [&](const SupportCandidate& c) {
             return c.escaped ? 0.0 : target_density(inc, c.g, scene);
           };
+          // Deviation (3): node k of the tree (DFS pre-order == k-th draw_g call) draws its
+          // support sample from stream (RECIP_NODE, k) and its split decision from
+          // (RECIP_SPLIT, k): the sampler re-keys the walk's Rng, which recip::Walk hands
+          // to stochastic_split right after draw_g (recip.hpp:69-97).
+          const uint64_t stream = pxg_recip_stream(static_cast<uint32_t>(pass), static_cast<uint32_t>(all[k]->walk),
+                                                   static_cast<uint32_t>(all[k]->end), static_cast<uint32_t>(r));
+          uint32_t node = 0;
           recip::SupportSampler<SupportCandidate> sampler{
-              [&](Rng& rr) { return support_sample(inc, scene, rr); },
+              [&](Rng& rr) {
+                Rng nr = Rng::keyed(seed, PXG_KIND_RECIP_NODE, node, stream);
+                SupportCandidate c = support_sample(inc, scene, nr);
+                rr = Rng::keyed(seed, PXG_KIND_RECIP_SPLIT, node, stream);
+                ++node;
+                return c;
+              },
               [](const SupportCandidate& c) { return c.q; }};
           recip::ReciprocalConfig cfg;
           cfg.bound = bound[k];
           cfg.recursion_cap = params.recursion_cap;
-          Rng rr = Rng::keyed(seed, PXG_KIND_RECIP,
-                              static_cast<uint32_t>(all[k]->end) | (static_cast<uint32_t>(r) << 8),
-                              unit_stream(pass, all[k]->walk));
+          Rng rr = Rng::keyed(seed, PXG_KIND_RECIP_SPLIT, 0, stream);
           runs[static_cast<size_t>(k) * R + r] = recip::estimate_reciprocal(f_oracle, sampler, cfg, rr);
         });
         for (int k = 0; k < n_ent; ++k) {
@@ -721,13 +732,21 @@ ORC_API int orc_recip_twopoint(int n, double bound, long long cap, unsigned long
                                double* est, long long* cost, int* truncated) {
   try {
     recip::IntegrandOracle<int> f = [](const int& x) { return x == 0 ? 1.0 : 3.0; };
-    recip::SupportSampler<int> q{[](Rng& rng) { return rng.next_double() < 0.5 ? 0 : 1; },
-                                 [](const int&) { return 0.5; }};
     recip::ReciprocalConfig cfg;
     cfg.bound = bound;
     cfg.recursion_cap = cap;
     for (int i = 0; i < n; ++i) {
-      Rng rng = Rng::keyed(seed, PXG_KIND_RECIP, 0, static_cast<uint64_t>(i));
+      // node-keyed streams as in the render loop (deviation 3), stream = run index
+      uint32_t node = 0;
+      recip::SupportSampler<int> q{[&](Rng& rr) {
+                                     Rng nr = Rng::keyed(seed, PXG_KIND_RECIP_NODE, node, static_cast<uint64_t>(i));
+                                     int x = nr.next_double() < 0.5 ? 0 : 1;
+                                     rr = Rng::keyed(seed, PXG_KIND_RECIP_SPLIT, node, static_cast<uint64_t>(i));
+                                     ++node;
+                                     return x;
+                                   },
+                                   [](const int&) { return 0.5; }};
+      Rng rng = Rng::keyed(seed, PXG_KIND_RECIP_SPLIT, 0, static_cast<uint64_t>(i));
       auto run = recip::estimate_reciprocal(f, q, cfg, rng);
       est[i] = run.estimate;
       cost[i] = run.cost;

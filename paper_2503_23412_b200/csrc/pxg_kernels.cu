@@ -8,7 +8,8 @@
 //     (CUB radix sort of the keys; the pool_budget smallest are kept, ordered by walk,end)
 //     k_pool_entries  one thread per kept entry: re-trace its walk, dropout, 4 probes
 //     k_pool_bounds   one thread: probes -> bucket max in entry order -> B per entry
-//     k_recip_runs    one thread per (entry, run): the reciprocal tree (variable trip count)
+//     k_recip_eval/   reciprocal runs in rounds: all pending tree nodes evaluated in parallel
+//     k_recip_dfs     (node-keyed streams), then each run's DFS resumes over them
 //     k_pool_finish   one thread: means, moments, validity, diagnostics, bucket lists
 //   Stage 2 (per pixel, proxy.cpp:738-819)
 //     k_trace         one thread per pixel: eye sub-path then light sub-path on the pixel's
@@ -22,15 +23,18 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <string>
 #include <vector>
 
 #include "pxg.h"
 #include "pxg_host.h"
-#include "pxg_proxy.cuh"
+#include "pxg_wave.cuh"
 
 using namespace pxg;
 
@@ -104,19 +108,21 @@ __device__ __forceinline__ uint64_t unit_stream(int pass, int walk) {
 __device__ __forceinline__ void set_err(int* err, int code) { atomicCAS(err, 0, code); }
 
 // ------------------------------------------------------------------ Stage 1 kernels
-__global__ void k_pool_walks(SceneView S, uint64_t seed, int pass, int walk_begin, int walk_end,
-                             unsigned long long* keys, unsigned* vals, int* count, int cap) {
-  const int w = walk_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= walk_end) return;
-  Rng rng = make_rng(seed, PXG_KIND_POOL_WALK, 0, unit_stream(pass, w));
-  PV v[kMaxLight];
-  const int n = trace_light_subpath(S, S.max_depth - 1, rng, v, 1);
+// Eligible prefix ends of the traced pool walks get a 64-bit priority key each
+// (the priority-reservoir replacement of Algorithm R, proxy.cpp:696-711).
+__global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, uint64_t seed, int pass, int walk_begin,
+                            unsigned long long* keys, unsigned* vals, int* count, int cap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_walks) return;
+  const int w = walk_begin + i;
+  const int n = wnv[i];
   int flag[kMaxLight], emitter[kMaxLight];
   double pdf[kMaxLight];
-  for (int i = 0; i < n; ++i) {
-    flag[i] = v[i].flag;
-    emitter[i] = v[i].emitter;
-    pdf[i] = v[i].pdf_fwd;
+  for (int k = 0; k < n; ++k) {
+    const PV& v = wpool[static_cast<size_t>(k) * n_walks + i];
+    flag[k] = v.flag;
+    emitter[k] = v.emitter;
+    pdf[k] = v.pdf_fwd;
   }
   for (int end = 2; end <= n; ++end) {
     if (flag[end - 1] != kSpecular) continue;
@@ -133,13 +139,13 @@ __global__ void k_pool_walks(SceneView S, uint64_t seed, int pass, int walk_begi
 }
 
 __global__ void k_pool_entries(SceneView S, Mapper M, uint64_t seed, int pass, int n_ent, const unsigned* sel,
-                               IncHdr* inc, PV* prefix, double* probe, int* probe_ok, int repeats) {
+                               const PV* wpool, int n_walks, int walk_begin, IncHdr* inc, PV* prefix,
+                               double* probe, int* probe_ok, int repeats) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_ent) return;
   const int w = static_cast<int>(sel[k] >> 5), end = static_cast<int>(sel[k] & 31u);
-  Rng rng = make_rng(seed, PXG_KIND_POOL_WALK, 0, unit_stream(pass, w));
   PV v[kMaxLight];
-  trace_light_subpath(S, S.max_depth - 1, rng, v, 1);
+  for (int q = 0; q < end; ++q) v[q] = wpool[static_cast<size_t>(q) * n_walks + (w - walk_begin)];
   IncHdr h;
   PV* pre = prefix + static_cast<size_t>(k) * kMaxLight;
   const bool ok = dropout(M, v, end, h, pre);
@@ -212,27 +218,105 @@ __global__ void k_pool_bounds(int n_ent, const IncHdr* inc, const double* probe,
   }
 }
 
-__global__ void k_recip_runs(SceneView S, uint64_t seed, int pass, int n_ent, int repeats, long long cap,
-                             const IncHdr* inc, const PV* prefix, const double* bound, double* est,
-                             long long* cost, int* trunc, RecipFrame* frames, int* err) {
+// Phase A of the reciprocal runs: evaluate nodes [avail, avail + chunk) of every active
+// run in parallel. Node k draws its support sample from (RECIP_NODE, k) and its split
+// decision from (RECIP_SPLIT, k) (include/pxg_philox.h), so its value does not depend on
+// the tree shape; draw_g (recip.hpp:69-77) and stochastic_split (recip.hpp:49-56).
+__global__ void k_recip_eval(SceneView S, uint64_t seed, int pass, int repeats, long long cap, const IncHdr* inc,
+                             const PV* prefix, const double* bound, const int* active, const int* n_active,
+                             int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long a = tid / chunk;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  const long long k = st[j].avail + tid % chunk;
+  if (k >= cap) return;
+  const int e = j / repeats, r = j % repeats;
+  const IncHdr& h = inc[e];
+  const PV* pre = prefix + static_cast<size_t>(e) * kMaxLight;
+  const double B = bound[e];
+  const uint64_t stream = pxg_recip_stream(pass, h.walk, h.end, r);
+  Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), stream);
+  int err = 0;
+  const double gv = draw_g(S, h, pre, B, nr, err);
+  long long n = 0;
+  if (!err) {
+    Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), stream);
+    n = split_count(gv, sr, err);
+  }
+  const size_t o = static_cast<size_t>(j) * cap + k;
+  g[o] = gv;
+  nsplit[o] = n;
+  nerr[o] = err;
+}
+
+// The two-point fixture f = {1, 3}, q = 1/2 (proj/tests/test_recip.cpp:16-23) as Phase A.
+__global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, const int* active, const int* n_active,
+                                int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long a = tid / chunk;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  const long long k = st[j].avail + tid % chunk;
+  if (k >= cap) return;
+  Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
+  const int x = nr.next_double() < 0.5 ? 0 : 1;
+  const double fx = x == 0 ? 1.0 : 3.0;
+  const double gv = 1.0 - fx / (bound * 0.5);
+  int err = 0;
+  Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
+  const long long n = split_count(gv, sr, err);
+  const size_t o = static_cast<size_t>(j) * cap + k;
+  g[o] = gv;
+  nsplit[o] = n;
+  nerr[o] = err;
+}
+
+__global__ void k_recip_init(int runs, int repeats, const IncHdr* inc, const double* bound, RunState* st,
+                             int* active, int* n_active, double* est, long long* cost, int* trunc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_ent * repeats) return;
-  const int k = j / repeats, r = j % repeats;
-  const double B = bound[k];
-  if (!(B > 0.0) || !inc[k].valid) return;
-  const IncHdr& h = inc[k];
-  const PV* pre = prefix + static_cast<size_t>(k) * kMaxLight;
-  Rng rng = make_rng(seed, PXG_KIND_RECIP, static_cast<uint32_t>(h.end) | (static_cast<uint32_t>(r) << 8),
-                     unit_stream(pass, h.walk));
-  int e = 0;
-  long long c = 0;
-  bool t = false;
-  auto draw = [&](Rng& rr) { return draw_g(S, h, pre, B, rr, e); };
-  double v = reciprocal_run(draw, B, cap, rng, frames + static_cast<size_t>(j) * cap, c, t, e);
-  if (e) set_err(err, e);
-  est[j] = v;
-  cost[j] = c;
-  trunc[j] = t ? 1 : 0;
+  if (j >= runs) return;
+  RunState s;
+  s.depth = s.cost = s.avail = 0;
+  s.ret = 0.0;
+  s.entering = 1;
+  s.truncated = 0;
+  s.err = 0;
+  const int e = j / repeats;
+  const bool live = inc ? (inc[e].valid && bound[e] > 0.0) : true;
+  s.done = live ? 0 : 1;
+  st[j] = s;
+  est[j] = 0.0;
+  cost[j] = 0;
+  trunc[j] = 0;
+  if (live) active[atomicAdd(n_active, 1)] = j;
+}
+
+// Phase B: resume the DFS of every active run over its newly evaluated nodes.
+__global__ void k_recip_dfs(int repeats, long long cap, const double* bound, double fixed_bound, const int* active,
+                            const int* n_active, int chunk, RunState* st, const double* g, const long long* nsplit,
+                            const int* nerr, RecipFrame* frames, double* est, long long* cost, int* trunc,
+                            int* next, int* n_next, int* err) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  RunState s = st[j];
+  s.avail = min(cap, s.avail + chunk);
+  const double B = bound ? bound[j / repeats] : fixed_bound;
+  const size_t o = static_cast<size_t>(j) * cap;
+  const bool done = dfs_resume(s, g + o, nsplit + o, nerr + o, frames + o, B, cap);
+  st[j] = s;
+  if (!done) {
+    next[atomicAdd(n_next, 1)] = j;
+    return;
+  }
+  if (s.err) {
+    set_err(err, s.err);
+    return;
+  }
+  est[j] = s.ret;
+  cost[j] = s.cost;
+  trunc[j] = s.truncated;
 }
 
 __global__ void k_pool_finish(int n_ent, int repeats, IncHdr* inc, const double* bound, const double* est,
@@ -312,35 +396,16 @@ struct Stage2 {
   int record_prims;
 };
 
-__global__ void k_trace(Stage2 P) {
+__global__ void k_record_prims(const PV* eye, const int* n_eye, const PV* light, const int* n_light, int n,
+                               int max_depth, int* eye_prims, int* light_prims) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  const int idx = P.row0 * P.width + i;  // global pixel index (reference stream id)
-  const int x = idx % P.width, y = idx / P.width;
-  Rng rng;
-  rng.r = pxg_rng_make(P.seed, PXG_KIND_REF, 0, static_cast<uint64_t>(idx));
-  rng.r.i = P.ctr[i];
-  const int ne = trace_eye_subpath(P.S, x, y, P.max_depth + 1, rng, P.eye + i, static_cast<size_t>(P.n));
-  const int nl = trace_light_subpath(P.S, P.max_depth - 1, rng, P.light + i, static_cast<size_t>(P.n));
-  P.ctr[i] = rng.r.i;
-  P.n_eye[i] = ne;
-  P.n_light[i] = nl;
-  if (P.record_prims) {
-    for (int k = 0; k <= P.max_depth; ++k)
-      P.eye_prims[static_cast<size_t>(i) * (P.max_depth + 1) + k] = k < ne ? P.eye[k * P.n + i].prim : -2;
-    for (int k = 0; k < P.max_depth - 1; ++k)
-      P.light_prims[static_cast<size_t>(i) * (P.max_depth - 1) + k] = k < nl ? P.light[k * P.n + i].prim : -2;
-  }
-}
-
-__global__ void k_connect(Stage2 P, int use_stats) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  V3 v = weighted_bdpt_value(P.S, P.M, P.st, use_stats != 0, P.eye + i, static_cast<size_t>(P.n), P.n_eye[i],
-                             P.light + i, static_cast<size_t>(P.n), P.n_light[i]);
-  P.bdpt[3 * i] = v.x;
-  P.bdpt[3 * i + 1] = v.y;
-  P.bdpt[3 * i + 2] = v.z;
+  if (i >= n) return;
+  const int ne = n_eye[i], nl = n_light[i];
+  for (int k = 0; k <= max_depth; ++k)
+    eye_prims[static_cast<size_t>(i) * (max_depth + 1) + k] = k < ne ? eye[static_cast<size_t>(k) * n + i].prim : -2;
+  for (int k = 0; k < max_depth - 1; ++k)
+    light_prims[static_cast<size_t>(i) * (max_depth - 1) + k] =
+        k < nl ? light[static_cast<size_t>(k) * n + i].prim : -2;
 }
 
 __global__ void k_proxy(Stage2 P, int pass, int n_px_total, const IncHdr* inc, const PV* prefix,
@@ -508,27 +573,6 @@ __global__ void k_occluded(SceneView S, int n, const double* segs, int* occ) {
   occ[i] = occluded(S, v3(s[0], s[1], s[2]), v3(s[3], s[4], s[5])) ? 1 : 0;
 }
 
-__global__ void k_twopoint(int n, double bound, long long cap, uint64_t seed, double* est, long long* cost,
-                           int* trunc, RecipFrame* frames, int threads) {
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= threads) return;
-  for (int i = tid; i < n; i += threads) {
-    Rng rng = make_rng(seed, PXG_KIND_RECIP, 0, static_cast<uint64_t>(i));
-    int e = 0;
-    long long c = 0;
-    bool t = false;
-    auto draw = [&](Rng& rr) {
-      const int x = rr.next_double() < 0.5 ? 0 : 1;
-      const double qx = 0.5;
-      const double fx = x == 0 ? 1.0 : 3.0;
-      return 1.0 - fx / (bound * qx);
-    };
-    est[i] = reciprocal_run(draw, bound, cap, rng, frames + static_cast<size_t>(tid) * cap, c, t, e);
-    cost[i] = c;
-    trunc[i] = t ? 1 : 0;
-  }
-}
-
 __global__ void k_rng(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   PxgRng r = pxg_rng_make(seed, kind, sub, stream);
@@ -595,6 +639,13 @@ struct pxg_ctx {
   long long* d_run_cost = nullptr;
   int* d_run_trunc = nullptr;
   RecipFrame* d_frames = nullptr;
+  RunState* d_rstate = nullptr;
+  double* d_rg = nullptr;
+  long long* d_rn = nullptr;
+  int* d_re = nullptr;
+  int* d_ract[2] = {nullptr, nullptr};
+  int* d_rnact = nullptr;
+  int recip_rounds = 0;
   int *d_kept = nullptr, *d_label_start = nullptr, *d_label_list = nullptr;
   PassState* d_ps = nullptr;
   int* d_err = nullptr;
@@ -606,6 +657,18 @@ struct pxg_ctx {
   // last pass pool (host copy for dumps)
   int last_n_ent = 0;
   long long last_raw = 0;
+  // wavefront queues and buffers
+  RayQueue qA{}, qB{}, qS{};
+  ConnBuf conn{};
+  double *d_ebeta = nullptr, *d_epdf = nullptr, *d_lbeta = nullptr, *d_lpdf = nullptr;
+  void* d_scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  int max_slots = 0;
+  PV* d_wpool = nullptr;
+  int* d_wnv = nullptr;
+  unsigned* d_wctr = nullptr;
+  double *d_wbeta = nullptr, *d_wpdf = nullptr;
+  int n_walks = 0;
   // timing
   cudaEvent_t ev[8];
   cudaEvent_t ev_call[2];
@@ -633,6 +696,7 @@ struct pxg_ctx {
   ~pxg_ctx() {
     for (void* p : allocs) cudaFree(p);
     if (d_sort_tmp) cudaFree(d_sort_tmp);
+    if (d_scan_tmp) cudaFree(d_scan_tmp);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -674,13 +738,115 @@ void gamma_end_iteration(pxg_ctx* c) {
                      c->stream));
 }
 
+// PXG_PROFILE=1: synchronise and print host-side stage timestamps (debugging aid).
+struct HostProbe {
+  pxg_ctx* c;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostProbe(pxg_ctx* c_) : c(c_), on(std::getenv("PXG_PROFILE") != nullptr) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what);
+};
+
+RayQueue make_queue(pxg_ctx* c, size_t cap) {
+  RayQueue q;
+  q.ray = c->alloc<double4>(2 * cap);
+  q.path = c->alloc<int>(cap);
+  q.hit_prim = c->alloc<int>(cap);
+  q.hit_t = c->alloc<double>(cap);
+  q.count = c->zeros<int>(1);
+  q.cap = static_cast<int>(cap);
+  return q;
+}
+
+// Sub-path wavefront: start kernel, then one (closest-hit, shade) pair per bounce.
+void trace_paths(pxg_ctx* c, const PathSet& P) {
+  RayQueue in = c->qA, out = c->qB;
+  CK(cudaMemsetAsync(in.count, 0, sizeof(int), c->stream));
+  const int T = 128;
+  if (P.eye)
+    k_eye_start<<<blocks(P.n, T), T, 0, c->stream>>>(c->S, P, in, c->row0);
+  else
+    k_light_start<<<blocks(P.n, T), T, 0, c->stream>>>(c->S, P, in);
+  ++c->launches;
+  for (int b = 0; b + 1 < P.max_vertices; ++b) {
+    k_closest<<<blocks(P.n, T), T, 0, c->stream>>>(c->S, in);
+    CK(cudaMemsetAsync(out.count, 0, sizeof(int), c->stream));
+    k_shade<<<blocks(P.n, T), T, 0, c->stream>>>(c->S, P, in, out);
+    c->launches += 2;
+    std::swap(in, out);
+  }
+}
+
+// Standard strategies of every pixel (weighted_bdpt_value, proxy.cpp:621-643).
+void connections(pxg_ctx* c, bool use_stats) {
+  const int n = c->n, D = c->max_depth, T = 128;
+  ConnBuf& C = c->conn;
+  k_conn_count<<<blocks(n, T), T, 0, c->stream>>>(c->d_neye, c->d_nlight, n, D, C.count);
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, C.count, C.offset, n + 1, c->stream);
+  if (need > c->scan_tmp_bytes) {
+    if (c->d_scan_tmp) cudaFree(c->d_scan_tmp);
+    CK(cudaMalloc(&c->d_scan_tmp, need));
+    c->scan_tmp_bytes = need;
+  }
+  CK(cub::DeviceScan::ExclusiveSum(c->d_scan_tmp, c->scan_tmp_bytes, C.count, C.offset, n + 1, c->stream));
+  k_conn_enum<<<blocks(n, T), T, 0, c->stream>>>(c->d_neye, c->d_nlight, n, D, C);
+  CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), c->stream));
+  const long long slots = static_cast<long long>(n) * c->max_slots;
+  k_conn_eval<<<blocks(slots, T), T, 0, c->stream>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
+  k_anyhit<<<blocks(slots, T), T, 0, c->stream>>>(c->S, c->qS);
+  k_conn_visibility<<<blocks(slots, T), T, 0, c->stream>>>(c->qS, C);
+  k_conn_mis<<<blocks(slots, T), T, 0, c->stream>>>(
+      c->S, c->M, StatsView{c->d_max_ratio, c->d_sum_est, c->d_sum_sq, c->d_est_cnt}, use_stats ? 1 : 0, c->d_eye,
+      c->d_light, n, C);
+  k_conn_sum<<<blocks(n, T), T, 0, c->stream>>>(n, C, c->d_bdpt);
+  c->launches += 9;
+}
+
+void HostProbe::mark(const char* what) {
+  if (!on) return;
+  cudaStreamSynchronize(c->stream);
+  auto t = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[pxg] %-14s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+  t0 = t;
+}
+
+// The reciprocal runs of one pass: rounds of (parallel node evaluation, DFS resume) with
+// the evaluated prefix doubling per round, until every run has finished.
+template <typename Eval>
+int recip_rounds(cudaStream_t stream, int runs, int* act[2], int* nact, Eval&& eval_and_dfs) {
+  int cur = 0, chunk = 16, rounds = 0;
+  for (;;) {
+    int count = 0;
+    CK(cudaMemcpyAsync(&count, nact + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (count == 0) break;
+    CK(cudaMemsetAsync(nact + (1 - cur), 0, sizeof(int), stream));
+    eval_and_dfs(cur, count, chunk);
+    cur = 1 - cur;
+    chunk = std::min(chunk * 2, 4096);
+    ++rounds;
+  }
+  (void)runs;
+  return rounds;
+}
+
 void stage1(pxg_ctx* c, int pass) {
+  HostProbe hp(c);
   const int walks = c->shard.walk_end - c->shard.walk_begin;
   CK(cudaMemsetAsync(c->d_ccount, 0, sizeof(int), c->stream));
   if (walks > 0) {
-    k_pool_walks<<<blocks(walks, 128), 128, 0, c->stream>>>(c->S, c->seed, pass, c->shard.walk_begin,
-                                                            c->shard.walk_end, c->d_ckey, c->d_cval, c->d_ccount,
-                                                            c->cand_cap);
+    CK(cudaMemsetAsync(c->d_wctr, 0, sizeof(unsigned) * walks, c->stream));
+    PathSet W{c->d_wpool, c->d_wnv, c->d_wctr, c->d_wbeta, c->d_wpdf, c->seed,
+              (static_cast<uint64_t>(pass) << 32) + static_cast<uint64_t>(c->shard.walk_begin),
+              PXG_KIND_POOL_WALK, walks, c->max_depth - 1, 0};
+    trace_paths(c, W);
+    hp.mark("walks");
+    k_pool_keys<<<blocks(walks, 128), 128, 0, c->stream>>>(c->d_wpool, c->d_wnv, walks, c->seed, pass,
+                                                           c->shard.walk_begin, c->d_ckey, c->d_cval, c->d_ccount,
+                                                           c->cand_cap);
     ++c->launches;
   }
   int raw = 0;
@@ -712,6 +878,7 @@ void stage1(pxg_ctx* c, int pass) {
     std::sort(sel.begin(), sel.end());  // (walk << 5 | end) order == (walk, end) order
     CK(cudaMemcpyAsync(c->d_sel, sel.data(), sizeof(unsigned) * n_ent, cudaMemcpyHostToDevice, c->stream));
   }
+  hp.mark("select");
   c->pool_raw_total += raw;
   c->last_raw = raw;
   c->last_n_ent = n_ent;
@@ -721,19 +888,35 @@ void stage1(pxg_ctx* c, int pass) {
   const int R = c->P.recip_repeats;
   bool ran_recip = false;
   if (n_ent > 0) {
-    k_pool_entries<<<blocks(n_ent, 64), 64, 0, c->stream>>>(c->S, c->M, c->seed, pass, n_ent, c->d_sel, c->d_inc,
-                                                           c->d_inc_prefix, c->d_probe, c->d_probe_ok, R);
+    k_pool_entries<<<blocks(n_ent, 64), 64, 0, c->stream>>>(c->S, c->M, c->seed, pass, n_ent, c->d_sel, c->d_wpool,
+                                                           walks, c->shard.walk_begin, c->d_inc, c->d_inc_prefix,
+                                                           c->d_probe, c->d_probe_ok, R);
     k_pool_bounds<<<1, 1, 0, c->stream>>>(n_ent, c->d_inc, c->d_probe, c->d_probe_ok, c->d_max_ratio,
                                           c->d_ratio_cnt, c->d_touched, c->d_bound, c->d_err);
     c->launches += 2;
+    hp.mark("entries+bounds");
     if (R >= 1) {
       CK(cudaEventRecord(c->ev[2], c->stream));
-      k_recip_runs<<<blocks(static_cast<long long>(n_ent) * R, 64), 64, 0, c->stream>>>(
-          c->S, c->seed, pass, n_ent, R, c->P.recursion_cap, c->d_inc, c->d_inc_prefix, c->d_bound, c->d_run_est,
-          c->d_run_cost, c->d_run_trunc, c->d_frames, c->d_err);
+      const int runs = n_ent * R;
+      const long long cap = c->P.recursion_cap;
+      CK(cudaMemsetAsync(c->d_rnact, 0, 2 * sizeof(int), c->stream));
+      k_recip_init<<<blocks(runs, 128), 128, 0, c->stream>>>(runs, R, c->d_inc, c->d_bound, c->d_rstate,
+                                                            c->d_ract[0], c->d_rnact, c->d_run_est, c->d_run_cost,
+                                                            c->d_run_trunc);
+      c->recip_rounds = recip_rounds(c->stream, runs, c->d_ract, c->d_rnact, [&](int cur, int count, int chunk) {
+        k_recip_eval<<<blocks(static_cast<long long>(count) * chunk, 64), 64, 0, c->stream>>>(
+            c->S, c->seed, pass, R, cap, c->d_inc, c->d_inc_prefix, c->d_bound, c->d_ract[cur], c->d_rnact + cur,
+            chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re);
+        k_recip_dfs<<<blocks(count, 64), 64, 0, c->stream>>>(
+            R, cap, c->d_bound, 0.0, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re,
+            c->d_frames, c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur], c->d_rnact + (1 - cur),
+            c->d_err);
+        c->launches += 2;
+      });
       CK(cudaEventRecord(c->ev[3], c->stream));
       ++c->launches;
       ran_recip = true;
+      hp.mark("recip");
     }
   }
   if (!ran_recip) {
@@ -744,6 +927,7 @@ void stage1(pxg_ctx* c, int pass) {
                                         c->d_sum_sq, c->d_est_cnt, c->d_touched, c->d_diag, c->d_diag_touched,
                                         c->d_kept, c->d_label_start, c->d_label_list, c->d_ps);
   ++c->launches;
+  hp.mark("finish");
 }
 
 void render_pass(pxg_ctx* c, bool record_prims) {
@@ -777,11 +961,25 @@ void render_pass(pxg_ctx* c, bool record_prims) {
   P.seed = c->seed;
   P.record_prims = record_prims ? 1 : 0;
   const int T = 128;
-  k_trace<<<blocks(c->n, T), T, 0, c->stream>>>(P);
+  HostProbe hp(c);
+  {
+    PathSet E{c->d_eye, c->d_neye, c->d_ctr, c->d_ebeta, c->d_epdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth + 1, 1};
+    trace_paths(c, E);
+    PathSet L{c->d_light, c->d_nlight, c->d_ctr, c->d_lbeta, c->d_lpdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth - 1, 0};
+    trace_paths(c, L);
+    if (record_prims) {
+      k_record_prims<<<blocks(c->n, T), T, 0, c->stream>>>(c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
+                                                          c->max_depth, c->d_eye_prims, c->d_light_prims);
+      ++c->launches;
+    }
+  }
+  hp.mark("trace");
   CK(cudaEventRecord(c->ev[4], c->stream));
-  k_connect<<<blocks(c->n, T), T, 0, c->stream>>>(P, c->proxy_on ? 1 : 0);
+  connections(c, c->proxy_on);
   CK(cudaEventRecord(c->ev[5], c->stream));
-  c->launches += 2;
+  hp.mark("connect");
   if (c->proxy_on) {
     k_proxy<<<blocks(c->n, T), T, 0, c->stream>>>(P, pass, c->n_px_total, c->d_inc, c->d_inc_prefix,
                                                   c->d_label_start, c->d_label_list, c->d_gamma, c->d_ps, c->d_prox,
@@ -796,6 +994,7 @@ void render_pass(pxg_ctx* c, bool record_prims) {
       c->d_diag_touched);
   CK(cudaEventRecord(c->ev[7], c->stream));
   ++c->launches;
+  hp.mark("proxy+gate");
   if (c->proxy_on) {
     check_err(c);
     if (c->gamma_learning) {
@@ -986,6 +1185,37 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_acc = c->zeros<double>(3 * n);
     c->d_prox = c->zeros<ProxRec>(n);
     c->d_scratch = c->alloc<PV>(n * kMaxLight);
+    c->d_ebeta = c->zeros<double>(3 * n);
+    c->d_epdf = c->zeros<double>(n);
+    c->d_lbeta = c->zeros<double>(3 * n);
+    c->d_lpdf = c->zeros<double>(n);
+    {
+      int ms = 0;
+      for (int t = 2; t <= c->max_depth + 1; ++t) ms += 1 + std::min(c->max_depth - 1, c->max_depth + 1 - t);
+      c->max_slots = ms;
+    }
+    const size_t slots = n * static_cast<size_t>(c->max_slots);
+    c->conn.count = c->zeros<int>(n + 1);
+    c->conn.offset = c->zeros<int>(n + 1);
+    c->conn.desc = c->alloc<int2>(slots);
+    c->conn.value = c->alloc<double>(3 * slots);
+    c->conn.state = c->zeros<int>(slots);
+    c->conn.total = c->zeros<int>(1);
+    c->qS = make_queue(c, slots);
+    c->n_walks = c->shard.walk_end - c->shard.walk_begin;
+    {
+      const size_t qcap = std::max<size_t>(n, static_cast<size_t>(c->n_walks));
+      c->qA = make_queue(c, qcap);
+      c->qB = make_queue(c, qcap);
+    }
+    if (c->proxy_on && c->n_walks > 0) {
+      const size_t w = c->n_walks;
+      c->d_wpool = c->alloc<PV>(w * std::max(c->max_depth - 1, 1));
+      c->d_wnv = c->zeros<int>(w);
+      c->d_wctr = c->zeros<unsigned>(w);
+      c->d_wbeta = c->zeros<double>(3 * w);
+      c->d_wpdf = c->zeros<double>(w);
+    }
     c->grid_w = (c->width + 9) / 10;
     c->grid_h = (c->rows + 9) / 10;
     c->n_cells = c->grid_w * c->grid_h;
@@ -1015,6 +1245,14 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_cval = c->alloc<unsigned>(c->cand_cap);
     c->d_cval_alt = c->alloc<unsigned>(c->cand_cap);
     c->d_ccount = c->zeros<int>(1);
+    {
+      // sort scratch sized once for the largest possible candidate count (no per-pass realloc)
+      size_t need = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_ckey, c->d_ckey_alt, c->d_cval, c->d_cval_alt,
+                                      c->cand_cap, 0, 64, c->stream);
+      CK(cudaMalloc(&c->d_sort_tmp, need));
+      c->sort_tmp_bytes = need;
+    }
     const int B = std::max(c->P.pool_budget, 1);
     const int R = std::max(c->P.recip_repeats, 1);
     c->d_sel = c->alloc<unsigned>(B);
@@ -1026,8 +1264,19 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_run_est = c->zeros<double>(static_cast<size_t>(B) * R);
     c->d_run_cost = c->zeros<long long>(static_cast<size_t>(B) * R);
     c->d_run_trunc = c->zeros<int>(static_cast<size_t>(B) * R);
-    if (c->proxy_on && c->P.recursion_cap > 0)
-      c->d_frames = c->alloc<RecipFrame>(static_cast<size_t>(B) * R * static_cast<size_t>(c->P.recursion_cap));
+    if (c->P.recursion_cap > (1 << 20) || c->P.recip_repeats > 255)
+      throw InvalidErr{"pxg: recursion_cap above 2^20 or recip_repeats above 255 is not supported"};
+    if (c->proxy_on && c->P.recursion_cap > 0) {
+      const size_t rc = static_cast<size_t>(B) * R * static_cast<size_t>(c->P.recursion_cap);
+      c->d_frames = c->alloc<RecipFrame>(rc);
+      c->d_rg = c->alloc<double>(rc);
+      c->d_rn = c->alloc<long long>(rc);
+      c->d_re = c->alloc<int>(rc);
+    }
+    c->d_rstate = c->alloc<RunState>(static_cast<size_t>(B) * R);
+    c->d_ract[0] = c->alloc<int>(static_cast<size_t>(B) * R);
+    c->d_ract[1] = c->alloc<int>(static_cast<size_t>(B) * R);
+    c->d_rnact = c->zeros<int>(2);
     c->d_kept = c->zeros<int>(B);
     c->d_label_start = c->zeros<int>(kS + 1);
     c->d_label_list = c->zeros<int>(B);
@@ -1248,20 +1497,47 @@ int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double
   return guarded(nullptr, [&]() {
     if (!(bound > 0.0)) throw RuntimeErr{"reciprocal: bound must be positive"};
     if (n <= 0) return;
-    const int threads = std::min(n, 4096);
-    double* de = dalloc<double>(n);
-    long long* dc = dalloc<long long>(n);
-    int* dt = dalloc<int>(n);
-    RecipFrame* fr = dalloc<RecipFrame>(static_cast<size_t>(threads) * std::max<long long>(cap, 1));
-    k_twopoint<<<blocks(threads, 128), 128>>>(n, bound, cap, seed, de, dc, dt, fr, threads);
-    CK(cudaGetLastError());
-    CK(cudaMemcpy(est, de, sizeof(double) * n, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(cost, dc, sizeof(long long) * n, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(truncated, dt, sizeof(int) * n, cudaMemcpyDeviceToHost));
-    cudaFree(de);
-    cudaFree(dc);
-    cudaFree(dt);
-    cudaFree(fr);
+    if (cap < 0 || cap > (1 << 20)) throw InvalidErr{"pxg_recip_twopoint: cap out of range"};
+    const long long capa = std::max<long long>(cap, 1);
+    cudaStream_t st = nullptr;
+    std::vector<void*> tmp;
+    auto A = [&](size_t bytes) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, std::max<size_t>(bytes, 1)));
+      tmp.push_back(p);
+      return p;
+    };
+    try {
+      const size_t nc = static_cast<size_t>(n) * capa;
+      auto* de = static_cast<double*>(A(sizeof(double) * n));
+      auto* dc = static_cast<long long*>(A(sizeof(long long) * n));
+      auto* dt = static_cast<int*>(A(sizeof(int) * n));
+      auto* rs = static_cast<RunState*>(A(sizeof(RunState) * n));
+      auto* g = static_cast<double*>(A(sizeof(double) * nc));
+      auto* ns = static_cast<long long*>(A(sizeof(long long) * nc));
+      auto* ne = static_cast<int*>(A(sizeof(int) * nc));
+      auto* fr = static_cast<RecipFrame*>(A(sizeof(RecipFrame) * nc));
+      int* act[2] = {static_cast<int*>(A(sizeof(int) * n)), static_cast<int*>(A(sizeof(int) * n))};
+      auto* nact = static_cast<int*>(A(sizeof(int) * 2));
+      auto* derr = static_cast<int*>(A(sizeof(int)));
+      CK(cudaMemset(nact, 0, 2 * sizeof(int)));
+      CK(cudaMemset(derr, 0, sizeof(int)));
+      k_recip_init<<<blocks(n, 128), 128>>>(n, 1, nullptr, nullptr, rs, act[0], nact, de, dc, dt);
+      recip_rounds(st, n, act, nact, [&](int cur, int count, int chunk) {
+        k_twopoint_eval<<<blocks(static_cast<long long>(count) * chunk, 128), 128>>>(seed, bound, cap, act[cur],
+                                                                                     nact + cur, chunk, rs, g, ns, ne);
+        k_recip_dfs<<<blocks(count, 128), 128>>>(1, cap, nullptr, bound, act[cur], nact + cur, chunk, rs, g, ns, ne,
+                                                 fr, de, dc, dt, act[1 - cur], nact + (1 - cur), derr);
+      });
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(est, de, sizeof(double) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(cost, dc, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(truncated, dt, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      for (void* p : tmp) cudaFree(p);
+      throw;
+    }
+    for (void* p : tmp) cudaFree(p);
   });
 }
 

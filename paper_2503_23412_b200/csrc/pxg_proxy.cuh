@@ -98,6 +98,84 @@ PXD double reciprocal_run(DrawG&& draw, double bound, long long cap, Rng& rng,
   return 1.0 / bound + ret;
 }
 
+// Resumable state of one reciprocal run (recip::estimate_reciprocal, recip.hpp:131-138).
+struct RunState {
+  long long depth, cost, avail;  // avail: nodes 0..avail-1 have precomputed (g, n)
+  double ret;
+  int entering, truncated, done, err;
+};
+
+// main_tree (recip.hpp:89-97) as an explicit-stack DFS over precomputed node values:
+// node k (the k-th draw_g call in pre-order) has g[k], split count n[k] and error code
+// e[k]. Returns false when it needs node `avail` (not yet evaluated); the state resumes.
+// The frame stack nests the partial sums exactly like the recursion, so the estimate is
+// bit-identical to the reference's.
+PXD bool dfs_resume(RunState& st, const double* g, const long long* nsplit, const int* e, RecipFrame* frames,
+                    double bound, long long cap) {
+  for (;;) {
+    if (st.entering) {
+      if (st.depth >= cap || st.cost >= cap) {
+        st.entering = 0;
+        st.truncated = 1;
+        st.ret = 0.0;
+      } else {
+        const long long k = st.cost;
+        if (k >= st.avail) return false;
+        st.entering = 0;
+        if (e[k]) {
+          st.err = e[k];
+          st.done = 1;
+          return true;
+        }
+        const double gk = g[k];
+        ++st.cost;
+        RecipFrame fr;
+        fr.ans = gk / bound;
+        fr.sgn = static_cast<double>((gk > 0.0) - (gk < 0.0));
+        fr.rem = nsplit[k];
+        if (fr.rem > 0) {
+          fr.rem -= 1;
+          frames[st.depth] = fr;
+          ++st.depth;
+          st.entering = 1;
+          continue;
+        }
+        frames[st.depth] = fr;
+        st.ret = fr.ans;
+      }
+    }
+    if (st.depth == 0) {
+      st.done = 1;
+      st.ret = 1.0 / bound + st.ret;
+      return true;
+    }
+    --st.depth;
+    RecipFrame& pf = frames[st.depth];
+    pf.ans += pf.sgn * st.ret;
+    if (pf.rem > 0) {
+      pf.rem -= 1;
+      ++st.depth;
+      st.entering = 1;
+      continue;
+    }
+    st.ret = pf.ans;
+  }
+}
+
+// stochastic_split (recip.hpp:49-56) of node k on its own split stream.
+PXD long long split_count(double g, Rng& split_rng, int& err) {
+  const double r = fabs(g);
+  if (!(r >= 0.0) || !isfinite(r)) {
+    err = kErrSplit;
+    return 0;
+  }
+  const double fl = floor(r);
+  const double frac = r - fl;
+  long long n = static_cast<long long>(fl);
+  if (frac > 0.0 && split_rng.bernoulli(frac)) ++n;
+  return n;
+}
+
 #if defined(__CUDACC__)
 
 __device__ __forceinline__ const PV* inc_control(const IncHdr& h, const PV* prefix) {

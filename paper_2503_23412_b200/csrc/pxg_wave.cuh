@@ -1,0 +1,346 @@
+// pxg_wave.cuh — wavefront kernels: sub-path tracing bounce by bounce over compacted ray
+// queues, lean closest-hit / any-hit traversal kernels, and the standard connections
+// expanded to one thread per (pixel, t, s) strategy slot.
+//
+// Why: the per-pixel megakernel version ran at 4.6/32 (trace) and 3.6/32 (connect) active
+// threads per warp instruction with 12 warps/SM resident (142 registers) — divergence- and
+// latency-bound, DRAM at 1% (profiles/r1_megakernel.md). Splitting the traversal out lets
+// every warp of the traversal kernels run the same loop with a small register footprint,
+// and the queues keep only live rays.
+//
+// Bit-exactness is kept: each path still consumes its own Philox stream in the reference
+// order (the queue order never matters), and the per-pixel sum of strategy contributions
+// is done in the reference's (t, s) order by k_conn_sum.
+#pragma once
+
+#include "pxg_proxy.cuh"
+
+namespace pxg {
+
+#if defined(__CUDACC__)
+
+// A set of sub-paths traced in lock-step bounces (eye paths, light paths or pool walks).
+struct PathSet {
+  PV* pool;          // vertex-major: vertex k of path i at pool[k * n + i]
+  int* nv;           // vertices so far
+  unsigned* ctr;     // Philox draw counter of the path's stream
+  double* beta;      // [n*3]
+  double* pdf_dir;   // [n]
+  uint64_t seed;
+  uint64_t stream_base;  // stream of path i = stream_base + i
+  uint32_t kind;
+  int n;
+  int max_vertices;
+  int eye;           // 1: eye sub-path rules (camera vertex, unit-density primary hit)
+};
+
+// Ray queue: slot j holds a ray for path[j]; traversal writes hit_prim/hit_t per slot.
+struct RayQueue {
+  double4* ray;  // [cap*2]: (ox, oy, oz, dx), (dy, dz, tmax, 0)
+  int* path;
+  int* hit_prim;
+  double* hit_t;
+  int* count;
+  int cap;
+};
+
+__device__ __forceinline__ Rng path_rng(const PathSet& P, int i) {
+  Rng r;
+  r.r = pxg_rng_make(P.seed, P.kind, 0, P.stream_base + static_cast<uint64_t>(i));
+  r.r.i = P.ctr[i];
+  return r;
+}
+
+__device__ __forceinline__ void push_ray(const RayQueue& Q, int path, const V3& o, const V3& d, double tmax) {
+  const int slot = atomicAdd(Q.count, 1);
+  Q.ray[2 * slot] = make_double4(o.x, o.y, o.z, d.x);
+  Q.ray[2 * slot + 1] = make_double4(d.y, d.z, tmax, 0.0);
+  Q.path[slot] = path;
+}
+
+// trace_eye_subpath start (transport.cpp:137-152): camera vertex + jittered pixel ray.
+__global__ void k_eye_start(SceneView S, PathSet P, RayQueue Q, int row0) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  PV z0;
+  z0.p = S.cam_pos;
+  z0.n = v3(0.0);
+  z0.wi = v3(0.0);
+  z0.flag = kCamera;
+  z0.pdf_fwd = 1.0;
+  z0.thr = v3(1.0);
+  z0.mat = -1;
+  z0.prim = -1;
+  z0.emitter = -1;
+  z0.pad = 0.0;
+  P.pool[i] = z0;
+  P.nv[i] = 1;
+  if (P.max_vertices == 1) return;
+  Rng rng = path_rng(P, i);
+  const int idx = row0 * S.width + i;
+  const int x = idx % S.width, y = idx / S.width;
+  // generate_ray's two rng arguments are evaluated right to left by the reference build
+  const double jv = rng.next_double();
+  const double ju = rng.next_double();
+  const V3 dir = camera_dir(S, x, y, ju, jv);
+  P.ctr[i] = rng.r.i;
+  P.beta[3 * i] = 1.0;
+  P.beta[3 * i + 1] = 1.0;
+  P.beta[3 * i + 2] = 1.0;
+  P.pdf_dir[i] = 1.0;
+  push_ray(Q, i, S.cam_pos, dir, 1e30);
+}
+
+// trace_light_subpath start (transport.cpp:111-135): area-sampled emitter point and a
+// cosine direction.
+__global__ void k_light_start(SceneView S, PathSet P, RayQueue Q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  P.nv[i] = 0;
+  if (P.max_vertices < 1) return;
+  Rng rng = path_rng(P, i);
+  LightPoint lp = sample_light_point(S, rng);
+  PV y0;
+  y0.p = lp.p;
+  y0.n = lp.n;
+  y0.wi = v3(0.0);
+  y0.mat = S.prim_mat[lp.prim];
+  y0.prim = lp.prim;
+  y0.emitter = S.prim_emitter[lp.prim];
+  y0.flag = kLight;
+  y0.pdf_fwd = lp.pdf_area;
+  y0.thr = v3(1.0 / lp.pdf_area);
+  y0.pad = 0.0;
+  P.pool[i] = y0;
+  P.nv[i] = 1;
+  if (P.max_vertices == 1) {
+    P.ctr[i] = rng.r.i;
+    return;
+  }
+  V3 d = sample_cosine_hemisphere(lp.n, rng);
+  P.ctr[i] = rng.r.i;
+  double pdf_dir = light_direction_pdf(lp.n, d);
+  if (pdf_dir <= 0.0) return;
+  V3 beta = y0.thr * lp.radiance * (dot(d, lp.n) / pdf_dir);
+  P.beta[3 * i] = beta.x;
+  P.beta[3 * i + 1] = beta.y;
+  P.beta[3 * i + 2] = beta.z;
+  P.pdf_dir[i] = pdf_dir;
+  push_ray(Q, i, lp.p, d, 1e30);
+}
+
+// One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
+__global__ void k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *in.count) return;
+  const int i = in.path[j];
+  const int prim = in.hit_prim[j];
+  if (prim < 0) return;  // escaped
+  const double4 r0 = in.ray[2 * j], r1 = in.ray[2 * j + 1];
+  const V3 o = v3(r0.x, r0.y, r0.z), d = v3(r0.w, r1.x, r1.y);
+  const double t = in.hit_t[j];
+  Hit hit;
+  hit.t = t;
+  hit.p = o + t * d;
+  hit.prim = prim;
+  hit.n = prim_normal(S, prim, hit.p);
+  hit.material = S.prim_mat[prim];
+  hit.emitter = S.prim_emitter[prim];
+  PV v = surface_vertex(S, hit, -d);
+  const int n = P.nv[i];
+  const bool primary = P.eye && n == 1;
+  V3 beta = v3(P.beta[3 * i], P.beta[3 * i + 1], P.beta[3 * i + 2]);
+  if (primary) {
+    v.pdf_fwd = 1.0;
+    v.thr = v3(1.0);
+  } else {
+    v.pdf_fwd = to_area_density(P.pdf_dir[i], o, v.p, v.n);
+    v.thr = beta;
+  }
+  P.pool[static_cast<size_t>(n) * P.n + i] = v;
+  P.nv[i] = n + 1;
+  if (n + 1 >= P.max_vertices) return;
+  Rng rng = path_rng(P, i);
+  BsdfSample bs = sample_bsdf(S.materials[v.mat], v.n, v.wi, rng);
+  P.ctr[i] = rng.r.i;
+  if (!bs.valid || bs.pdf <= 0.0) return;
+  beta = beta * bs.value * (fabs(dot(bs.wo, v.n)) / bs.pdf);
+  // extend_walk checks the throughput after each of its own samples; the eye walk's first
+  // sample (at the primary hit, transport.cpp:160-163) is not checked
+  if (!primary && near_zero(beta)) return;
+  P.beta[3 * i] = beta.x;
+  P.beta[3 * i + 1] = beta.y;
+  P.beta[3 * i + 2] = beta.z;
+  P.pdf_dir[i] = bs.pdf;
+  push_ray(out, i, v.p, bs.wo, 1e30);
+}
+
+// Closest hit over a queue (Scene::intersect semantics, scene.cpp:127-168).
+__global__ void __launch_bounds__(128) k_closest(SceneView S, RayQueue Q) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *Q.count) return;
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  double t_best = r1.z;
+  const int prim = trace_closest(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), t_best);
+  Q.hit_prim[j] = prim;
+  Q.hit_t[j] = t_best;
+}
+
+// Any hit over a queue (the boolean of Scene::occluded, scene.cpp:170-177): hit_prim = 1
+// when occluded.
+__global__ void __launch_bounds__(128) k_anyhit(SceneView S, RayQueue Q) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *Q.count) return;
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  Q.hit_prim[j] = trace_any(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), r1.z) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- standard connections
+// Slot layout per pixel, in the reference's accumulation order (proxy.cpp:627-641):
+// for t = 2..n_eye: s = 0 (eye-hit emission), then s = 1..min(n_light, max_depth+1-t).
+__device__ __forceinline__ int conn_slots(int ne, int nl, int max_depth) {
+  int c = 0;
+  for (int t = 2; t <= ne; ++t) c += 1 + min(nl, max_depth + 1 - t);
+  return c;
+}
+
+struct ConnBuf {
+  int* count;      // [n_px] slots per pixel
+  int* offset;     // [n_px + 1] exclusive prefix
+  int2* desc;      // [slot] pixel, t << 8 | s
+  double* value;   // [slot*3]
+  int* state;      // [slot] 0 nothing, 1 contributes, 2 waiting for visibility
+  int* shadow_slot;  // [shadow queue slot] -> connection slot
+  int* total;      // device scalar: number of slots
+};
+
+__global__ void k_conn_count(const int* n_eye, const int* n_light, int n, int max_depth, int* count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  count[i] = conn_slots(n_eye[i], n_light[i], max_depth);
+}
+
+__global__ void k_conn_enum(const int* n_eye, const int* n_light, int n, int max_depth, ConnBuf C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o = C.offset[i];
+  const int ne = n_eye[i], nl = n_light[i];
+  for (int t = 2; t <= ne; ++t) {
+    const int smax = min(nl, max_depth + 1 - t);
+    for (int s = 0; s <= smax; ++s) C.desc[o++] = make_int2(i, (t << 8) | s);
+  }
+  if (i == n - 1) *C.total = o;
+}
+
+// Unoccluded value of every slot; connections that need a shadow ray are queued.
+__global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, ConnBuf C, RayQueue shadow) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= *C.total) return;
+  const int2 dsc = C.desc[g];
+  const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
+  const size_t st = static_cast<size_t>(n);
+  V3 val = v3(0.0);
+  int state = 0;
+  if (s == 0) {
+    const PV& z = eye[(t - 1) * st + i];
+    if (z.emitter >= 0) {
+      val = z.thr * emitted(S, z.emitter, z.n, z.wi);
+      if (!near_zero(val)) state = 1;
+    }
+  } else {
+    // connection_contribution (transport.cpp:187-196) with the visibility deferred
+    const PV& y = light[(s - 1) * st + i];
+    const PV& z = eye[(t - 1) * st + i];
+    if (z.flag == kDiffuse) {
+      V3 d = z.p - y.p;
+      double len = length(d);
+      if (len > 0.0) {
+        V3 dir = d / len;
+        V3 f_light = v3(0.0);
+        bool ok = true;
+        if (s == 1) {
+          f_light = emitted(S, y.emitter, y.n, dir);
+        } else if (y.flag != kDiffuse) {
+          ok = false;
+        } else {
+          f_light = eval_bsdf(S.materials[y.mat], y.n, y.wi, dir);
+        }
+        if (ok) {
+          V3 f_eye = eval_bsdf(S.materials[z.mat], z.n, z.wi, -dir);
+          if (!near_zero(f_light) && !near_zero(f_eye)) {
+            // geometry_term (transport.cpp:168-176) without the visibility factor
+            V3 dd = z.p - y.p;
+            double dist2 = dot(dd, dd);
+            double gg = 0.0;
+            if (dist2 > 0.0) {
+              V3 gdir = dd / sqrt(dist2);
+              gg = fabs(dot(y.n, gdir)) * fabs(dot(z.n, gdir)) / dist2;
+            }
+            if (gg > 0.0) {
+              val = y.thr * f_light * gg * f_eye * z.thr;
+              // Scene::occluded(y.p, z.p)
+              V3 sd = z.p - y.p;
+              double dist = length(sd);
+              if (dist < kRayEps) {
+                state = 1;
+              } else {
+                state = 2;
+                const int q = atomicAdd(shadow.count, 1);
+                const V3 sdir = sd / dist;
+                shadow.ray[2 * q] = make_double4(y.p.x, y.p.y, y.p.z, sdir.x);
+                shadow.ray[2 * q + 1] = make_double4(sdir.y, sdir.z, dist * (1.0 - 1e-6), 0.0);
+                shadow.path[q] = g;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  C.value[3 * g] = val.x;
+  C.value[3 * g + 1] = val.y;
+  C.value[3 * g + 2] = val.z;
+  C.state[g] = state;
+}
+
+__global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= *shadow.count) return;
+  const int g = shadow.path[q];
+  C.state[g] = shadow.hit_prim[q] ? 0 : 1;  // occluded -> no contribution
+}
+
+// reciprocal_mis_weight per contributing slot; value <- value * w.
+__global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
+                           int n, ConnBuf C) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= *C.total) return;
+  if (C.state[g] != 1) return;
+  const int2 dsc = C.desc[g];
+  const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
+  const size_t st_ = static_cast<size_t>(n);
+  FullPath fp{light + i, st_, eye + i, st_, s, t};
+  const double w = reciprocal_mis_weight(S, M, st, fp, s, use_stats != 0);
+  C.value[3 * g] = C.value[3 * g] * w;
+  C.value[3 * g + 1] = C.value[3 * g + 1] * w;
+  C.value[3 * g + 2] = C.value[3 * g + 2] * w;
+}
+
+// weighted_bdpt_value's accumulation (proxy.cpp:627-641) in slot order.
+__global__ void k_conn_sum(int n, ConnBuf C, double* bdpt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 r = v3(0.0);
+  const int a = C.offset[i], b = C.offset[i + 1];
+  for (int g = a; g < b; ++g) {
+    if (C.state[g] != 1) continue;
+    r += v3(C.value[3 * g], C.value[3 * g + 1], C.value[3 * g + 2]);
+  }
+  bdpt[3 * i] = r.x;
+  bdpt[3 * i + 1] = r.y;
+  bdpt[3 * i + 2] = r.z;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace pxg
