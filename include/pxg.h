@@ -103,8 +103,12 @@ const char* pxg_last_error(const pxg_ctx* ctx);
 int pxg_render_pass(pxg_ctx* ctx);
 /* One pass that also records the sub-path primitive ids for pxg_dump_prims. */
 int pxg_render_pass_traced(pxg_ctx* ctx);
-/* Several passes back to back. */
+/* Several passes back to back. Stage 1 of the next pass is computed one pass ahead on a
+ * second stream (results are identical to the sequential order). */
 int pxg_render_passes(pxg_ctx* ctx, int n);
+/* Total number of passes the caller intends to render (the spp of the render call): no
+ * look-ahead Stage 1 is started for pass >= limit. -1 (default) = unbounded. */
+int pxg_set_pass_limit(pxg_ctx* ctx, int limit);
 int pxg_synchronize(pxg_ctx* ctx);
 
 /* Running mean acc/done over this context's rows, row-major fp64 RGB, y = 0 top

@@ -31,7 +31,7 @@ enum {
   PXG_KIND_REF = 0,        /* reference-compatible Rng(seed, stream) */
   PXG_KIND_POOL_WALK = 1,  /* stream = pass<<32 | walk                       */
   PXG_KIND_RESERVOIR = 2,  /* stream = pass<<32 | walk, sub = prefix end      */
-  PXG_KIND_PROBE = 3,      /* stream = pass<<32 | walk, sub = prefix end      */
+  PXG_KIND_PROBE = 3,      /* stream = pass<<32 | walk, sub = end | probe << 8 */
   PXG_KIND_RECIP = 4,      /* stream = pass<<32 | walk, sub = end | run << 8  */
   PXG_KIND_PRETRACE = 5,   /* stream = walk                                   */
   PXG_KIND_RECIP_NODE = 6, /* sub = tree node (DFS pre-order), stream = pxg_recip_stream() */

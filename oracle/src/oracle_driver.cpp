@@ -470,10 +470,12 @@ ORC_API int orc_render(void* h, int spp, unsigned long long seed, const OrcParam
         for (int k = 0; k < n_ent; ++k) {
           IncompleteLightSubPath& inc = all[k]->inc;
           const StatsKey key = inc.key();
-          Rng pr = Rng::keyed(seed, PXG_KIND_PROBE, static_cast<uint32_t>(all[k]->end),
-                              unit_stream(pass, all[k]->walk));
           if (params.recip_repeats >= 1) {
             for (int i = 0; i < 4; ++i) {
+              // one stream per probe (PROBE, end | i << 8) so the four probes run in parallel
+              Rng pr = Rng::keyed(seed, PXG_KIND_PROBE,
+                                  static_cast<uint32_t>(all[k]->end) | (static_cast<uint32_t>(i) << 8),
+                                  unit_stream(pass, all[k]->walk));
               SupportCandidate cand = support_sample(inc, scene, pr);
               if (!cand.valid || !(cand.q > 0.0)) continue;
               double f = cand.escaped ? 0.0 : target_density(inc, cand.g, scene);

@@ -18,9 +18,9 @@ OUT = os.path.join(HERE, "libpxg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["pxg_kernels.cu"]
+CU_SOURCES = ["pxg_main.cu"]
 CPP_SOURCES = ["pxg_host.cpp"]
-HEADERS = ["pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
+HEADERS = ["pxg_stage_kernels.cuh", "pxg_wave.cuh", "pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
 
 
 def _inputs():

@@ -1,0 +1,1153 @@
+// pxg_main.cu — libpxg: pass orchestration on two CUDA streams and the C ABI (include/pxg.h).
+//
+// Per pass (proj/src/proxy.cpp:683-827): Stage 1 (pool walks -> priority selection ->
+// entries -> probes -> bounds -> reciprocal rounds -> finish) runs on `stream1` one pass
+// ahead of Stage 2 (eye/light wavefronts -> connections -> proxy connection -> gate + film
+// -> gamma) on `stream`. Stage 1 of pass p+1 reads and writes only the subspace statistics
+// and its own pool slot, never the film, the grid shares or gamma, so overlapping it with
+// Stage 2 of pass p leaves every result identical to the sequential order.
+#include "pxg_stage_kernels.cuh"
+
+// ------------------------------------------------------------------ context
+// Pool state of one pass, double-buffered: Stage 1 of pass p+1 (stream s1) fills one slot
+// while Stage 2 of pass p (stream s2) reads the other.
+struct PoolSlot {
+  IncHdr* inc = nullptr;
+  PV* prefix = nullptr;
+  int* kept = nullptr;
+  int* label_start = nullptr;
+  int* label_list = nullptr;
+  PassState* ps = nullptr;
+  double* snap_sum = nullptr;  // SubspaceStats snapshot after Stage 1 of this pass
+  double* snap_sq = nullptr;
+  long long* snap_cnt = nullptr;
+  cudaEvent_t s1_done = nullptr;  // Stage 1 wrote the slot
+  cudaEvent_t s2_done = nullptr;  // Stage 2 finished reading it
+  cudaEvent_t t0 = nullptr, t1 = nullptr, r0 = nullptr, r1 = nullptr;  // Stage-1 timing
+  double* bound = nullptr;      // B per entry used by this pass's reciprocal runs
+  long long* diag = nullptr;    // [4000*5] Stage-1 diagnostics of this pass
+  int* diag_touched = nullptr;  // [4000]
+  double* snap_max = nullptr;
+  long long* snap_rcnt = nullptr;
+  int pass = -1;
+  int batch_end = 0;  // first pass after the Stage-1 batch this slot belongs to
+  int n_ent = 0;
+  long long raw = 0;
+  bool timing_pending = false;
+};
+
+struct pxg_ctx {
+  std::string err;
+  int device = 0;
+  cudaStream_t stream = nullptr;   // Stage 2 (and everything else)
+  cudaStream_t stream1 = nullptr;  // Stage 1 of the next pass
+  SceneHost host;
+  pxg_params P{};
+  pxg_shard shard{};
+  uint64_t seed = 0;
+  int width = 0, height = 0, max_depth = 0, n = 0, n_px_total = 0, row0 = 0, rows = 0;
+  int light_walks = 0;
+  int grid_w = 0, grid_h = 0, n_cells = 0;
+  bool proxy_on = false;
+  int passes_done = 0;
+  int pass_limit = -1;  // no Stage-1 lookahead at or beyond this pass (pxg_set_pass_limit)
+  std::vector<void*> allocs;
+
+  SceneView S{};
+  Mapper M{};
+  // stage 2
+  PV* d_eye = nullptr;
+  PV* d_light = nullptr;
+  int *d_neye = nullptr, *d_nlight = nullptr;
+  unsigned* d_ctr = nullptr;
+  double *d_bdpt = nullptr, *d_val = nullptr, *d_acc = nullptr;
+  ProxRec* d_prox = nullptr;
+  PV* d_scratch = nullptr;
+  double *d_grid_total = nullptr, *d_grid_proxy = nullptr;
+  int *d_gbin = nullptr, *d_gbin_sorted = nullptr;
+  double *d_gval = nullptr, *d_gval_sorted = nullptr;
+  void* d_gsort_tmp = nullptr;
+  size_t gsort_bytes = 0;
+  int* d_pflags = nullptr;
+  int *d_eye_prims = nullptr, *d_light_prims = nullptr;
+  // stats (live, written by Stage 1 only)
+  double *d_max_ratio = nullptr, *d_sum_est = nullptr, *d_sum_sq = nullptr;
+  long long *d_ratio_cnt = nullptr, *d_est_cnt = nullptr;
+  int* d_touched = nullptr;
+  // gamma: rows and accumulators on the device; learning state is host bookkeeping
+  bool gamma_learning = true;
+  int gamma_iter = 0;
+  double* d_gamma = nullptr;
+  double* d_gamma_accum = nullptr;
+  // pool (Stage 1 working buffers)
+  int cand_cap = 0;
+  unsigned long long *d_ckey = nullptr, *d_ckey_alt = nullptr;
+  unsigned *d_cval = nullptr, *d_cval_alt = nullptr;
+  int* d_ccount = nullptr;
+  void* d_sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  unsigned* d_sel = nullptr;
+  double* d_probe = nullptr;
+  int* d_probe_ok = nullptr;
+  double* d_bound = nullptr;
+  double* d_run_est = nullptr;
+  long long* d_run_cost = nullptr;
+  int* d_run_trunc = nullptr;
+  RecipFrame* d_frames = nullptr;
+  RunState* d_rstate = nullptr;
+  double* d_rg = nullptr;
+  long long* d_rn = nullptr;
+  int* d_re = nullptr;
+  int* d_ract[2] = {nullptr, nullptr};
+  int* d_rnact = nullptr;
+  int recip_rounds = 0;
+  static constexpr int kBatchMax = 8;  // passes per Stage-1 batch
+  PoolSlot slot[2 * kBatchMax];        // ring: batch k uses half k & 1
+  int batch = kBatchMax;               // passes per batch (<= kBatchMax)
+  int next_batch = 0;                  // first pass without a launched Stage 1
+  BatchPass* d_bp = nullptr;           // [kBatchMax]
+  PoolSlot& slot_of(int pass) { return slot[pass % (2 * batch)]; }
+  int* d_err = nullptr;
+  // diagnostics
+  long long* d_diag = nullptr;  // [4000*5]: cols 2..4 written by k_pool_finish
+  unsigned long long *d_diag_attempt = nullptr, *d_diag_accept = nullptr;
+  unsigned long long* d_kept_total = nullptr;
+  int* d_diag_touched = nullptr;
+  long long pool_raw_total = 0;
+  // wavefront queues and buffers
+  RayQueue qA{}, qB{}, qS{};  // qA/qB: Stage 2 bounces; qS: shadow rays
+  RayQueue wA{}, wB{};        // Stage-1 pool-walk bounces (own queues: runs concurrently)
+  ConnBuf conn{};
+  PathCache pcache{};
+  double *d_ebeta = nullptr, *d_epdf = nullptr, *d_lbeta = nullptr, *d_lpdf = nullptr;
+  void* d_scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  int max_slots = 0;
+  PV* d_wpool = nullptr;
+  int* d_wnv = nullptr;
+  unsigned* d_wctr = nullptr;
+  double *d_wbeta = nullptr, *d_wpdf = nullptr;
+  int n_walks = 0;
+  // timing (Stage 2 events on `stream`)
+  cudaEvent_t ev[8];
+  cudaEvent_t ev_call[3];
+  double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long launches = 0;
+
+  template <typename T>
+  T* alloc(size_t n_) {
+    T* p = dalloc<T>(n_);
+    allocs.push_back(p);
+    return p;
+  }
+  template <typename T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+  template <typename T>
+  T* zeros(size_t n_) {
+    T* p = alloc<T>(n_);
+    CK(cudaMemset(p, 0, std::max<size_t>(n_, 1) * sizeof(T)));
+    return p;
+  }
+  ~pxg_ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (stream1) cudaStreamSynchronize(stream1);
+    for (void* p : allocs) cudaFree(p);
+    if (d_sort_tmp) cudaFree(d_sort_tmp);
+    if (d_scan_tmp) cudaFree(d_scan_tmp);
+    if (d_gsort_tmp) cudaFree(d_gsort_tmp);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    for (auto& e : ev_call) if (e) cudaEventDestroy(e);
+    for (auto& sl : slot)
+      for (cudaEvent_t e : {sl.s1_done, sl.s2_done, sl.t0, sl.t1, sl.r0, sl.r1})
+        if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (stream1) cudaStreamDestroy(stream1);
+  }
+};
+
+namespace {
+
+void check_err(pxg_ctx* c, cudaStream_t st) {
+  int e = 0;
+  CK(cudaMemcpyAsync(&e, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (e) {
+    const char* what = e == kErrIntegrand ? "reciprocal: integrand must be finite and non-negative"
+                       : e == kErrSupport ? "reciprocal: support pdf must be finite and positive"
+                       : e == kErrSplit   ? "stochastic_split: bad ratio"
+                                          : "update_ratio: ratio must be finite and non-negative";
+    throw RuntimeErr{what};
+  }
+}
+
+// PXG_PROFILE=1: synchronise and print host-side stage timestamps (debugging aid).
+struct HostProbe {
+  cudaStream_t st;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostProbe(cudaStream_t s) : st(s), on(std::getenv("PXG_PROFILE") != nullptr) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pxg] %-14s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
+RayQueue make_queue(pxg_ctx* c, size_t cap) {
+  RayQueue q;
+  q.ray = c->alloc<double4>(2 * cap);
+  q.path = c->alloc<int>(cap);
+  q.hit_prim = c->alloc<int>(cap);
+  q.hit_t = c->alloc<double>(cap);
+  q.count = c->zeros<int>(1);
+  q.cap = static_cast<int>(cap);
+  return q;
+}
+
+// Sub-path wavefront: start kernel, then one (closest-hit, shade) pair per bounce.
+void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaStream_t st) {
+  CK(cudaMemsetAsync(in.count, 0, sizeof(int), st));
+  const int T = 128;
+  if (P.eye)
+    k_eye_start<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, c->row0);
+  else
+    k_light_start<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in);
+  ++c->launches;
+  for (int b = 0; b + 1 < P.max_vertices; ++b) {
+    k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+    CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
+    k_shade<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, out);
+    c->launches += 2;
+    std::swap(in, out);
+  }
+}
+
+// Standard strategies of every pixel (weighted_bdpt_value, proxy.cpp:621-643).
+void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
+  const int n = c->n, D = c->max_depth, T = 128;
+  cudaStream_t st = c->stream;
+  ConnBuf& C = c->conn;
+  k_conn_count<<<blocks(n, T), T, 0, st>>>(c->d_neye, c->d_nlight, n, D, C.count);
+  CK(cub::DeviceScan::ExclusiveSum(c->d_scan_tmp, c->scan_tmp_bytes, C.count, C.offset, n + 1, st));
+  k_conn_enum<<<blocks(n, T), T, 0, st>>>(c->d_neye, c->d_nlight, n, D, C);
+  CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(C.n_live, 0, sizeof(int), st));
+  k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
+  const long long slots = static_cast<long long>(n) * c->max_slots;
+  k_conn_eval<<<blocks(slots, T), T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
+  k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+  k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
+  k_conn_mis<<<blocks(slots, T), T, 0, st>>>(c->S, c->M,
+                                             StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
+                                             use_stats ? 1 : 0, c->d_eye, c->d_light, n, C, c->pcache);
+  k_conn_sum<<<blocks(n, T), T, 0, st>>>(n, C, c->d_bdpt);
+  c->launches += 10;
+}
+
+// The reciprocal runs of one pass: rounds of (parallel node evaluation, DFS resume) with
+// the evaluated prefix doubling per round, until every run has finished.
+template <typename Eval>
+int recip_rounds(cudaStream_t stream, int* nact, Eval&& eval_and_dfs) {
+  static const int first = std::getenv("PXG_RECIP_CHUNK") ? std::atoi(std::getenv("PXG_RECIP_CHUNK")) : 32;
+  static const int grow = std::getenv("PXG_RECIP_GROW") ? std::atoi(std::getenv("PXG_RECIP_GROW")) : 4;
+  static const bool verbose = std::getenv("PXG_PROFILE") != nullptr;
+  int cur = 0, chunk = first, rounds = 0;
+  for (;;) {
+    int count = 0;
+    CK(cudaMemcpyAsync(&count, nact + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (verbose) std::fprintf(stderr, "[pxg]   round %d: %d runs x %d nodes\n", rounds, count, chunk);
+    if (count == 0) break;
+    CK(cudaMemsetAsync(nact + (1 - cur), 0, sizeof(int), stream));
+    eval_and_dfs(cur, count, chunk);
+    cur = 1 - cur;
+    chunk = std::min(chunk * grow, 16384);
+    ++rounds;
+  }
+  return rounds;
+}
+
+void read_stage1_timing(pxg_ctx* c, PoolSlot& sl) {
+  if (!sl.timing_pending) return;
+  cudaEventSynchronize(sl.t1);
+  float a = 0.f, b = 0.f;
+  if (cudaEventElapsedTime(&a, sl.t0, sl.t1) != cudaSuccess) a = 0.f;
+  if (cudaEventElapsedTime(&b, sl.r0, sl.r1) != cudaSuccess) b = 0.f;
+  cudaGetLastError();
+  c->stage_ms[0] += a;
+  c->stage_ms[1] += b;
+  sl.timing_pending = false;
+}
+
+// Stage 1 of `pass` into `sl` on stream1 (proxy.cpp:684-736). Host synchronisation here
+// only waits for stream1, so Stage 2 of the previous pass keeps running on `stream`.
+// Stage-1 front of `pass` into `sl` on stream1: pool walks, priority selection, entries,
+// probes and bounds (proxy.cpp:684-714, 389-395). Bounds of pass p see the bucket maxima
+// after pass p-1's probes, so fronts run in pass order on the one stream.
+void stage1_front(pxg_ctx* c, int pass, PoolSlot& sl) {
+  cudaStream_t st = c->stream1;
+  HostProbe hp(st);
+  CK(cudaStreamWaitEvent(st, sl.s2_done, 0));  // Stage 2 of the slot's previous pass is done
+  CK(cudaEventRecord(sl.t0, st));
+  CK(cudaMemsetAsync(sl.diag, 0, sizeof(long long) * kBuckets * 5, st));
+  CK(cudaMemsetAsync(sl.diag_touched, 0, sizeof(int) * kBuckets, st));
+  const int walks = c->n_walks;
+  CK(cudaMemsetAsync(c->d_ccount, 0, sizeof(int), st));
+  if (walks > 0) {
+    CK(cudaMemsetAsync(c->d_wctr, 0, sizeof(unsigned) * walks, st));
+    PathSet W{c->d_wpool, c->d_wnv, c->d_wctr, c->d_wbeta, c->d_wpdf, c->seed,
+              (static_cast<uint64_t>(pass) << 32) + static_cast<uint64_t>(c->shard.walk_begin),
+              PXG_KIND_POOL_WALK, walks, c->max_depth - 1, 0};
+    trace_paths(c, W, c->wA, c->wB, st);
+    k_pool_keys<<<blocks(walks, 128), 128, 0, st>>>(c->d_wpool, c->d_wnv, walks, c->seed, pass,
+                                                    c->shard.walk_begin, c->d_ckey, c->d_cval, c->d_ccount,
+                                                    c->cand_cap);
+    ++c->launches;
+    hp.mark("walks");
+  }
+  int raw = 0;
+  CK(cudaMemcpyAsync(&raw, c->d_ccount, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (raw > c->cand_cap) throw RuntimeErr{"pool candidate buffer overflow"};
+  const int budget = c->P.pool_budget;
+  const int n_ent = std::min(raw, std::max(budget, 0));
+  std::vector<unsigned> sel(n_ent);
+  if (n_ent > 0) {
+    const unsigned* src = c->d_cval;
+    if (raw > budget) {
+      CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, c->sort_tmp_bytes, c->d_ckey, c->d_ckey_alt, c->d_cval,
+                                         c->d_cval_alt, raw, 0, 64, st));
+      ++c->launches;
+      src = c->d_cval_alt;
+    }
+    CK(cudaMemcpyAsync(sel.data(), src, sizeof(unsigned) * n_ent, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // keys tie only with probability ~2^-64; ties are broken by (walk, end) like the oracle
+    std::sort(sel.begin(), sel.end());  // (walk << 5 | end) order == (walk, end) order
+    CK(cudaMemcpyAsync(c->d_sel, sel.data(), sizeof(unsigned) * n_ent, cudaMemcpyHostToDevice, st));
+  }
+  hp.mark("select");
+  sl.raw = raw;
+  sl.n_ent = n_ent;
+  sl.pass = pass;
+  const double kappa = raw > 0 ? std::min(1.0, static_cast<double>(budget) / static_cast<double>(raw)) : 1.0;
+  CK(cudaMemcpyAsync(&sl.ps->kappa, &kappa, sizeof(double), cudaMemcpyHostToDevice, st));
+  if (n_ent > 0) {
+    const int R = c->P.recip_repeats;
+    k_pool_entries<<<blocks(n_ent, 64), 64, 0, st>>>(c->M, n_ent, c->d_sel, c->d_wpool, walks, c->shard.walk_begin,
+                                                     sl.inc, sl.prefix);
+    k_pool_probes<<<blocks(4 * n_ent, 64), 64, 0, st>>>(c->S, c->seed, pass, n_ent, sl.inc, sl.prefix, c->d_probe,
+                                                        c->d_probe_ok, R);
+    k_pool_bounds<<<1, 512, 2 * sizeof(double) * n_ent, st>>>(n_ent, sl.inc, c->d_probe, c->d_probe_ok,
+                                                              c->d_max_ratio, c->d_ratio_cnt, c->d_touched,
+                                                              sl.bound, c->d_err);
+    c->launches += 3;
+    hp.mark("entries+bounds");
+  }
+  // ratio statistics as of this pass (reported by pxg_read_stats; Stage 2 does not read them)
+  CK(cudaMemcpyAsync(sl.snap_max, c->d_max_ratio, sizeof(double) * kBuckets, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(sl.snap_rcnt, c->d_ratio_cnt, sizeof(long long) * kBuckets, cudaMemcpyDeviceToDevice, st));
+}
+
+// Stage 1 of passes [p0, p0 + L): the fronts in pass order, ONE set of reciprocal rounds
+// for all L x budget x repeats runs (the long-run tail is paid once per batch), then the
+// finishes in pass order (bucket estimate sums are sequential across passes).
+void run_stage1_batch(pxg_ctx* c, int p0, int L) {
+  cudaStream_t st = c->stream1;
+  HostProbe hp(st);
+  std::vector<BatchPass> bp(L);
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    stage1_front(c, p0 + b, sl);
+    bp[b] = BatchPass{sl.inc, sl.prefix, sl.bound, p0 + b, sl.n_ent};
+  }
+  const int R = c->P.recip_repeats;
+  const int stride = std::max(c->P.pool_budget, 1) * std::max(R, 1);
+  PoolSlot& s0 = c->slot_of(p0);
+  CK(cudaEventRecord(s0.r0, st));
+  if (R >= 1) {
+    CK(cudaMemcpyAsync(c->d_bp, bp.data(), sizeof(BatchPass) * L, cudaMemcpyHostToDevice, st));
+    const int runs = L * stride;
+    const long long cap = c->P.recursion_cap;
+    CK(cudaMemsetAsync(c->d_rnact, 0, 2 * sizeof(int), st));
+    k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, c->d_bp, c->d_rstate, c->d_ract[0], c->d_rnact,
+                                                   c->d_run_est, c->d_run_cost, c->d_run_trunc);
+    c->recip_rounds = recip_rounds(st, c->d_rnact, [&](int cur, int count, int chunk) {
+      k_recip_eval<<<blocks(static_cast<long long>(count) * chunk, 64), 64, 0, st>>>(
+          c->S, c->seed, R, stride, cap, c->d_bp, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
+          c->d_rn, c->d_re);
+      k_recip_dfs<<<blocks(count, 64), 64, 0, st>>>(R, stride, cap, c->d_bp, 0.0, c->d_ract[cur], c->d_rnact + cur,
+                                                    chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
+                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
+                                                    c->d_rnact + (1 - cur), c->d_err);
+      c->launches += 2;
+    });
+    c->launches += 1;
+  }
+  CK(cudaEventRecord(s0.r1, st));
+  hp.mark("recip");
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    const size_t o = static_cast<size_t>(b) * stride;
+    k_pool_finish<<<1, 512, sizeof(int) * (sl.n_ent + kS), st>>>(
+        sl.n_ent, R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq,
+        c->d_est_cnt, c->d_touched, sl.diag, sl.diag_touched, sl.kept, sl.label_start, sl.label_list, sl.ps,
+        sl.snap_sum, sl.snap_sq, sl.snap_cnt, c->d_max_ratio, c->d_ratio_cnt, sl.snap_max, sl.snap_rcnt);
+    ++c->launches;
+    CK(cudaEventRecord(sl.t1, st));
+    CK(cudaEventRecord(sl.s1_done, st));
+    sl.timing_pending = b == 0;
+    sl.batch_end = p0 + L;
+  }
+  c->next_batch = p0 + L;
+  hp.mark("finish");
+}
+
+// Stage 2 of `pass` on `stream` (proxy.cpp:738-827), reading pool slot `sl`.
+void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
+  cudaStream_t st = c->stream;
+  const int T = 128;
+  HostProbe hp(st);
+  CK(cudaEventRecord(c->ev[0], st));
+  if (c->proxy_on) {
+    CK(cudaStreamWaitEvent(st, sl.s1_done, 0));
+    k_fold_diag<<<blocks(kBuckets, 128), 128, 0, st>>>(sl.diag, sl.diag_touched, sl.ps, c->d_diag,
+                                                       c->d_diag_touched, c->d_kept_total);
+    ++c->launches;
+    c->pool_raw_total += sl.raw;
+  }
+  CK(cudaEventRecord(c->ev[1], st));
+  {
+    PathSet E{c->d_eye, c->d_neye, c->d_ctr, c->d_ebeta, c->d_epdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth + 1, 1};
+    trace_paths(c, E, c->qA, c->qB, st);
+    PathSet L{c->d_light, c->d_nlight, c->d_ctr, c->d_lbeta, c->d_lpdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth - 1, 0};
+    trace_paths(c, L, c->qA, c->qB, st);
+    if (record_prims) {
+      k_record_prims<<<blocks(c->n, T), T, 0, st>>>(c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
+                                                   c->max_depth, c->d_eye_prims, c->d_light_prims);
+      ++c->launches;
+    }
+  }
+  CK(cudaEventRecord(c->ev[4], st));
+  hp.mark("trace");
+  connections(c, c->proxy_on, sl);
+  CK(cudaEventRecord(c->ev[5], st));
+  hp.mark("connect");
+  Stage2 P;
+  P.S = c->S;
+  P.M = c->M;
+  P.st = StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt};
+  P.eye = c->d_eye;
+  P.light = c->d_light;
+  P.n_eye = c->d_neye;
+  P.n_light = c->d_nlight;
+  P.ctr = c->d_ctr;
+  P.bdpt = c->d_bdpt;
+  P.eye_prims = c->d_eye_prims;
+  P.light_prims = c->d_light_prims;
+  P.n = c->n;
+  P.row0 = c->row0;
+  P.width = c->width;
+  P.height = c->height;
+  P.max_depth = c->max_depth;
+  P.seed = c->seed;
+  P.record_prims = record_prims ? 1 : 0;
+  if (c->proxy_on) {
+    k_proxy<<<blocks(c->n, T), T, 0, st>>>(P, pass, c->n_px_total, sl.inc, sl.prefix, sl.label_start, sl.label_list,
+                                           c->d_gamma, sl.ps, c->d_prox, c->d_scratch);
+    ++c->launches;
+  }
+  CK(cudaEventRecord(c->ev[6], st));
+  hp.mark("proxy");
+  k_gate<<<blocks(c->n_cells, 64), 64, 0, st>>>(
+      c->n_cells, c->grid_w, c->row0, c->rows, c->width, pass, c->P.gate_high, c->P.gate_low, c->P.gate_threshold,
+      static_cast<double>(c->light_walks), c->proxy_on ? 1 : 0, sl.ps, c->d_bdpt, c->d_prox, c->d_acc, c->d_val,
+      c->d_grid_total, c->d_grid_proxy, c->d_gbin, c->d_gval, c->d_pflags, c->d_diag_attempt, c->d_diag_accept,
+      c->d_diag_touched);
+  ++c->launches;
+  if (c->proxy_on && c->gamma_learning) {
+    // record_contribution in pixel order: a stable sort by bin keeps pixel order per bin
+    CK(cub::DeviceRadixSort::SortPairs(c->d_gsort_tmp, c->gsort_bytes, c->d_gbin, c->d_gbin_sorted, c->d_gval,
+                                       c->d_gval_sorted, c->n, 0, 12, st));
+    k_gamma_update<<<blocks(kT * kS, 128), 128, 0, st>>>(c->n, c->d_gbin_sorted, c->d_gval_sorted, c->d_gamma_accum,
+                                                         c->d_gamma, 1);
+    k_gamma_rows<<<1, 32, 0, st>>>(c->d_gamma_accum, c->d_gamma);
+    c->launches += 3;
+    ++c->gamma_iter;
+    if (c->gamma_iter >= c->P.freeze_iteration) c->gamma_learning = false;
+  }
+  CK(cudaEventRecord(c->ev[7], st));
+  CK(cudaEventRecord(sl.s2_done, st));
+  hp.mark("gate+gamma");
+}
+
+void read_stage2_timing(pxg_ctx* c) {
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    return static_cast<double>(ms);
+  };
+  c->stage_ms[2] += el(1, 4);
+  c->stage_ms[3] += el(4, 5);
+  c->stage_ms[4] += el(5, 6);
+  c->stage_ms[5] += el(6, 7);
+}
+
+// Renders `npass` passes. Stage 1 of pass p+1 is issued on stream1 right after Stage 2
+// of pass p is enqueued on `stream`, so the two overlap on the device.
+// Renders `npass` passes. Stage 1 runs in batches of c->batch passes on stream1; while
+// the GPU renders Stage 2 of one batch (enqueued without host synchronisation), the host
+// drives Stage 1 of the next batch, so the two overlap.
+void render_passes_impl(pxg_ctx* c, int npass, bool record_last) {
+  for (int k = 0; k < 8; ++k) c->stage_ms[k] = 0.0;
+  c->launches = 0;
+  CK(cudaEventRecord(c->ev_call[0], c->stream));
+  CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
+  auto batch_len = [&](int p0) {
+    int L = c->batch;
+    if (c->pass_limit >= 0) L = std::min(L, std::max(1, c->pass_limit - p0));
+    return L;
+  };
+  int left = npass;
+  while (left > 0) {
+    const int p = c->passes_done;
+    if (c->proxy_on && c->slot_of(p).pass != p) run_stage1_batch(c, p, batch_len(p));
+    // Stage 2 of the passes of this batch, enqueued without host synchronisation
+    const int stop = c->proxy_on ? c->slot_of(p).batch_end : p + left;
+    const int m = std::min(left, stop - p);
+    for (int k = 0; k < m; ++k) {
+      const int pp = c->passes_done;
+      enqueue_stage2(c, pp, c->slot_of(pp), record_last && left - k == 1);
+      CK(cudaGetLastError());
+      ++c->passes_done;
+    }
+    left -= m;
+    static const bool overlap = std::getenv("PXG_NO_OVERLAP") == nullptr;
+    if (!overlap) CK(cudaStreamSynchronize(c->stream));
+    // look-ahead: Stage 1 of the next batch while Stage 2 of this one runs
+    if (c->proxy_on && c->passes_done == stop && (c->pass_limit < 0 || stop < c->pass_limit) &&
+        c->slot_of(stop).pass != stop) {
+      for (int q = 0; q < c->batch; ++q) read_stage1_timing(c, c->slot_of(stop + q));
+      run_stage1_batch(c, stop, batch_len(stop));
+    }
+    CK(cudaEventSynchronize(c->ev[7]));
+    read_stage2_timing(c);
+  }
+  CK(cudaEventRecord(c->ev_call[2], c->stream1));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_call[2], 0));
+  CK(cudaEventRecord(c->ev_call[1], c->stream));
+  CK(cudaEventSynchronize(c->ev_call[1]));
+  float total = 0.f;
+  CK(cudaEventElapsedTime(&total, c->ev_call[0], c->ev_call[1]));
+  c->stage_ms[6] = total;
+  for (auto& sl : c->slot) read_stage1_timing(c, sl);
+  check_err(c, c->stream);
+}
+
+int fail(pxg_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_global_err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(pxg_ctx* c, F&& f) {
+  try {
+    if (c) CK(cudaSetDevice(c->device));
+    f();
+    return PXG_OK;
+  } catch (const CudaErr& e) {
+    return fail(c, PXG_E_CUDA, e.msg);
+  } catch (const InvalidErr& e) {
+    return fail(c, PXG_E_INVALID, e.msg);
+  } catch (const RuntimeErr& e) {
+    return fail(c, PXG_E_RUNTIME, e.msg);
+  } catch (const std::exception& e) {
+    return fail(c, PXG_E_INVALID, e.what());
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+void pxg_default_params(pxg_params* p) {
+  p->enabled = 1;
+  p->pool_budget = 400;
+  p->recip_repeats = 5;
+  p->freeze_iteration = 40;
+  p->recursion_cap = 10000;
+  p->pretrace_paths = 20000;
+  p->light_walks = 0;
+  p->gate_high = 1.0;
+  p->gate_low = 0.2;
+  p->gate_threshold = 0.05;
+}
+
+int pxg_abi_version(void) { return PXG_ABI_VERSION; }
+
+int pxg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char* pxg_last_error(const pxg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
+
+void pxg_destroy(pxg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  delete ctx;
+}
+
+int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed, int device,
+               const pxg_shard* shard, pxg_ctx** out) {
+  if (!sd || !out) return fail(nullptr, PXG_E_INVALID, "pxg_create: null argument");
+  *out = nullptr;
+  if (pxg_device_count() <= 0) return fail(nullptr, PXG_E_NODEVICE, "pxg_create: no CUDA device");
+  auto* c = new pxg_ctx();
+  c->device = device;
+  int rc = guarded(c, [&]() {
+    if (sd->max_depth < 1) throw InvalidErr{"scene: max_depth must be at least 1"};
+    if (sd->max_depth + 1 > kMaxPath - 2 || sd->max_depth - 1 > kMaxLight - 1)
+      throw InvalidErr{"pxg: max_depth above 16 is not supported"};
+    if (params) c->P = *params; else pxg_default_params(&c->P);
+    c->seed = seed;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {
+      // Stage 1 is a chain of small latency-bound launches (reciprocal rounds): give it the
+      // highest priority so its blocks are scheduled ahead of Stage 2's wide kernels.
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&c->stream1, cudaStreamNonBlocking, hi));
+    }
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
+    finalize_scene(*sd, c->host);
+    SceneHost& h = c->host;
+    c->width = sd->width;
+    c->height = sd->height;
+    c->max_depth = sd->max_depth;
+    c->n_px_total = sd->width * sd->height;
+    c->light_walks = c->P.light_walks > 0 ? c->P.light_walks : c->n_px_total;
+    if (shard) {
+      c->shard = *shard;
+    } else {
+      c->shard = pxg_shard{0, sd->height, 0, c->light_walks};
+    }
+    if (c->shard.row_begin < 0 || c->shard.row_end > sd->height || c->shard.row_begin >= c->shard.row_end ||
+        (c->shard.row_begin % 10) != 0 || c->shard.walk_begin < 0 || c->shard.walk_end > c->light_walks ||
+        c->shard.walk_begin > c->shard.walk_end)
+      throw InvalidErr{"pxg_create: invalid shard"};
+    c->row0 = c->shard.row_begin;
+    c->rows = c->shard.row_end - c->shard.row_begin;
+    c->n = c->rows * c->width;
+    bool any_spec = false;
+    std::vector<Material> mats(sd->n_materials);
+    for (int m = 0; m < sd->n_materials; ++m) {
+      const double* q = sd->materials + 7 * m;
+      Material& M = mats[m];
+      M.base_color = v3(q[0], q[1], q[2]);
+      M.metallic = q[3];
+      M.roughness = q[4];
+      M.transmission = q[5];
+      M.ior = q[6];
+      M.specular = ((M.metallic >= 0.5 || M.transmission >= 0.5) && M.roughness < 0.2) ? 1 : 0;
+      M.pad = 0;
+      any_spec = any_spec || M.specular;
+    }
+    c->proxy_on = c->P.enabled != 0;
+    (void)any_spec;
+    // device scene
+    SceneView& S = c->S;
+    S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
+    S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
+    S.prim_mat = c->upload(h.prim_mat);
+    S.prim_emitter = c->upload(h.prim_emitter);
+    S.prim_geo = c->upload(h.prim_geo);
+    S.prim_center = c->upload(h.prim_center);
+    S.prim_shape = c->upload(h.prim_shape);
+    S.prim_abc = c->upload(h.prim_abc);
+    S.materials = c->upload(mats);
+    S.emitter_prim = c->upload(std::vector<int>(sd->emitter_prim, sd->emitter_prim + sd->n_emitters));
+    S.emitter_rad = c->upload(std::vector<double>(sd->emitter_radiance, sd->emitter_radiance + 3 * sd->n_emitters));
+    S.emitter_cum = c->upload(h.emitter_cum);
+    S.n_prims = sd->n_prims;
+    S.n_emit = sd->n_emitters;
+    S.n_nodes = static_cast<int>(h.nodes.size());
+    S.n_mat = sd->n_materials;
+    S.total_emitter_area = h.total_emitter_area;
+    S.bbox_min = v3(h.bbox_min[0], h.bbox_min[1], h.bbox_min[2]);
+    S.bbox_max = v3(h.bbox_max[0], h.bbox_max[1], h.bbox_max[2]);
+    S.cam_pos = v3(h.cam[0], h.cam[1], h.cam[2]);
+    S.cam_fwd = v3(h.cam[3], h.cam[4], h.cam[5]);
+    S.cam_right = v3(h.cam[6], h.cam[7], h.cam[8]);
+    S.cam_up = v3(h.cam[9], h.cam[10], h.cam[11]);
+    S.tan_half = h.tan_half;
+    S.aspect = h.aspect;
+    S.width = sd->width;
+    S.height = sd->height;
+    S.max_depth = sd->max_depth;
+    c->M.bmin = S.bbox_min;
+    c->M.bmax = S.bbox_max;
+    // stage-2 buffers
+    const size_t n = c->n;
+    c->d_eye = c->alloc<PV>(n * (c->max_depth + 1));
+    c->d_light = c->alloc<PV>(n * std::max(c->max_depth - 1, 1));
+    c->d_neye = c->zeros<int>(n);
+    c->d_nlight = c->zeros<int>(n);
+    c->d_ctr = c->zeros<unsigned>(n);
+    c->d_bdpt = c->zeros<double>(3 * n);
+    c->d_val = c->zeros<double>(3 * n);
+    c->d_acc = c->zeros<double>(3 * n);
+    c->d_prox = c->zeros<ProxRec>(n);
+    c->d_scratch = c->alloc<PV>(n * kMaxLight);
+    c->d_ebeta = c->zeros<double>(3 * n);
+    c->d_epdf = c->zeros<double>(n);
+    c->d_lbeta = c->zeros<double>(3 * n);
+    c->d_lpdf = c->zeros<double>(n);
+    {
+      int ms = 0;
+      for (int t = 2; t <= c->max_depth + 1; ++t) ms += 1 + std::min(c->max_depth - 1, c->max_depth + 1 - t);
+      c->max_slots = ms;
+    }
+    const size_t slots = n * static_cast<size_t>(c->max_slots);
+    c->conn.count = c->zeros<int>(n + 1);
+    c->conn.offset = c->zeros<int>(n + 1);
+    c->conn.desc = c->alloc<int2>(slots);
+    c->conn.value = c->alloc<double>(3 * slots);
+    c->conn.state = c->zeros<int>(slots);
+    c->conn.total = c->zeros<int>(1);
+    c->conn.live = c->alloc<int>(slots);
+    c->conn.n_live = c->zeros<int>(1);
+    {
+      const size_t L = static_cast<size_t>(kMaxPath);
+      c->pcache.LF = c->zeros<double>(L * n);
+      c->pcache.LR = c->zeros<double>(L * n);
+      c->pcache.EF = c->zeros<double>(L * n);
+      c->pcache.ER = c->zeros<double>(L * n);
+      c->pcache.ld = c->zeros<double>(n);
+      c->pcache.ld_ok = c->zeros<int>(n);
+      c->pcache.n = static_cast<int>(n);
+    }
+    c->qS = make_queue(c, slots);
+    c->n_walks = c->shard.walk_end - c->shard.walk_begin;
+    c->qA = make_queue(c, n);
+    c->qB = make_queue(c, n);
+    {
+      size_t need = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, need, c->conn.count, c->conn.offset, static_cast<int>(n + 1), c->stream);
+      CK(cudaMalloc(&c->d_scan_tmp, need));
+      c->scan_tmp_bytes = need;
+    }
+    if (c->proxy_on && c->n_walks > 0) {
+      const size_t w = c->n_walks;
+      c->wA = make_queue(c, w);
+      c->wB = make_queue(c, w);
+      c->d_wpool = c->alloc<PV>(w * std::max(c->max_depth - 1, 1));
+      c->d_wnv = c->zeros<int>(w);
+      c->d_wctr = c->zeros<unsigned>(w);
+      c->d_wbeta = c->zeros<double>(3 * w);
+      c->d_wpdf = c->zeros<double>(w);
+    }
+    c->grid_w = (c->width + 9) / 10;
+    c->grid_h = (c->rows + 9) / 10;
+    c->n_cells = c->grid_w * c->grid_h;
+    c->d_grid_total = c->zeros<double>(c->n_cells);
+    c->d_grid_proxy = c->zeros<double>(c->n_cells);
+    c->d_gbin = c->zeros<int>(n);
+    c->d_gbin_sorted = c->zeros<int>(n);
+    c->d_gval = c->zeros<double>(n);
+    c->d_gval_sorted = c->zeros<double>(n);
+    {
+      size_t need = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_gbin, c->d_gbin_sorted, c->d_gval, c->d_gval_sorted,
+                                      static_cast<int>(n), 0, 12, c->stream);
+      CK(cudaMalloc(&c->d_gsort_tmp, need));
+      c->gsort_bytes = need;
+    }
+    c->d_pflags = c->zeros<int>(n);
+    c->d_eye_prims = c->zeros<int>(n * (c->max_depth + 1));
+    c->d_light_prims = c->zeros<int>(n * std::max(c->max_depth - 1, 1));
+    // stats
+    c->d_max_ratio = c->zeros<double>(kBuckets);
+    c->d_sum_est = c->zeros<double>(kBuckets);
+    c->d_sum_sq = c->zeros<double>(kBuckets);
+    c->d_ratio_cnt = c->zeros<long long>(kBuckets);
+    c->d_est_cnt = c->zeros<long long>(kBuckets);
+    c->d_touched = c->zeros<int>(kBuckets);
+    c->gamma_learning = c->P.freeze_iteration > 0;  // GammaMatrix::uniform (subspace.cpp:130-141)
+    c->gamma_iter = 0;
+    c->d_gamma = c->upload(std::vector<double>(kT * kS, 1.0 / kS));
+    c->d_gamma_accum = c->zeros<double>(kT * kS);
+    // pool
+    const int walks = c->shard.walk_end - c->shard.walk_begin;
+    c->cand_cap = std::max(1, walks) * std::max(1, c->max_depth - 2);
+    c->d_ckey = c->alloc<unsigned long long>(c->cand_cap);
+    c->d_ckey_alt = c->alloc<unsigned long long>(c->cand_cap);
+    c->d_cval = c->alloc<unsigned>(c->cand_cap);
+    c->d_cval_alt = c->alloc<unsigned>(c->cand_cap);
+    c->d_ccount = c->zeros<int>(1);
+    {
+      // sort scratch sized once for the largest possible candidate count (no per-pass realloc)
+      size_t need = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_ckey, c->d_ckey_alt, c->d_cval, c->d_cval_alt,
+                                      c->cand_cap, 0, 64, c->stream);
+      CK(cudaMalloc(&c->d_sort_tmp, need));
+      c->sort_tmp_bytes = need;
+    }
+    const int B = std::max(c->P.pool_budget, 1);
+    const int R = std::max(c->P.recip_repeats, 1);
+    c->d_sel = c->alloc<unsigned>(B);
+    c->d_probe = c->zeros<double>(4 * B);
+    c->d_probe_ok = c->zeros<int>(4 * B);
+    for (PoolSlot& sl : c->slot) {
+      sl.inc = c->zeros<IncHdr>(B);
+      sl.prefix = c->alloc<PV>(static_cast<size_t>(B) * kMaxLight);
+      sl.kept = c->zeros<int>(B);
+      sl.label_start = c->zeros<int>(kS + 1);
+      sl.label_list = c->zeros<int>(B);
+      sl.ps = c->zeros<PassState>(1);
+      sl.bound = c->zeros<double>(B);
+      sl.diag = c->zeros<long long>(kBuckets * 5);
+      sl.diag_touched = c->zeros<int>(kBuckets);
+      sl.snap_sum = c->zeros<double>(kBuckets);
+      sl.snap_sq = c->zeros<double>(kBuckets);
+      sl.snap_cnt = c->zeros<long long>(kBuckets);
+      sl.snap_max = c->zeros<double>(kBuckets);
+      sl.snap_rcnt = c->zeros<long long>(kBuckets);
+      for (cudaEvent_t* e : {&sl.s1_done, &sl.s2_done, &sl.t0, &sl.t1, &sl.r0, &sl.r1}) CK(cudaEventCreate(e));
+    }
+    {
+      const char* eb = std::getenv("PXG_BATCH");
+      c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchMax));
+    }
+    const size_t NR = static_cast<size_t>(B) * R * c->batch;  // reciprocal runs of one Stage-1 batch
+    c->d_run_est = c->zeros<double>(NR);
+    c->d_run_cost = c->zeros<long long>(NR);
+    c->d_run_trunc = c->zeros<int>(NR);
+    c->d_bp = c->zeros<BatchPass>(pxg_ctx::kBatchMax);
+    if (c->P.recursion_cap > (1 << 20) || c->P.recip_repeats > 255)
+      throw InvalidErr{"pxg: recursion_cap above 2^20 or recip_repeats above 255 is not supported"};
+    if (c->proxy_on && c->P.recursion_cap > 0) {
+      const size_t rc = NR * static_cast<size_t>(c->P.recursion_cap);
+      c->d_frames = c->alloc<RecipFrame>(rc);
+      c->d_rg = c->alloc<double>(rc);
+      c->d_rn = c->alloc<long long>(rc);
+      c->d_re = c->alloc<int>(rc);
+    }
+    c->d_rstate = c->alloc<RunState>(NR);
+    c->d_ract[0] = c->alloc<int>(NR);
+    c->d_ract[1] = c->alloc<int>(NR);
+    c->d_rnact = c->zeros<int>(2);
+    c->d_err = c->zeros<int>(1);
+    c->d_kept_total = c->zeros<unsigned long long>(1);
+    c->d_diag = c->zeros<long long>(kBuckets * 5);
+    c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
+    c->d_diag_accept = c->zeros<unsigned long long>(kBuckets);
+    c->d_diag_touched = c->zeros<int>(kBuckets);
+    if (c->proxy_on) {
+      const int np = std::max(c->P.pretrace_paths, 1000);
+      k_pretrace<<<blocks(np, 64), 64, 0, c->stream>>>(c->S, c->M, c->seed, np, c->d_max_ratio, c->d_ratio_cnt,
+                                                       c->d_touched, c->d_err);
+      CK(cudaGetLastError());
+      check_err(c, c->stream);
+    }
+    CK(cudaDeviceSynchronize());
+  });
+  if (rc != PXG_OK) {
+    g_global_err = c->err;
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return PXG_OK;
+}
+
+int pxg_render_passes(pxg_ctx* c, int npass) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  return guarded(c, [&]() { render_passes_impl(c, npass, false); });
+}
+
+int pxg_render_pass(pxg_ctx* c) { return pxg_render_passes(c, 1); }
+
+int pxg_render_pass_traced(pxg_ctx* c) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  return guarded(c, [&]() { render_passes_impl(c, 1, true); });
+}
+
+int pxg_set_pass_limit(pxg_ctx* c, int limit) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  c->pass_limit = limit;
+  return PXG_OK;
+}
+
+int pxg_synchronize(pxg_ctx* c) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->stream1));
+  });
+}
+
+int pxg_read_accum(pxg_ctx* c, double* rgb, int* passes) {
+  return guarded(c, [&]() {
+    CK(cudaMemcpyAsync(rgb, c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (passes) *passes = c->passes_done;
+  });
+}
+
+int pxg_read_mean(pxg_ctx* c, double* rgb, int* passes) {
+  return guarded(c, [&]() {
+    CK(cudaMemcpyAsync(rgb, c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const double d = static_cast<double>(c->passes_done > 0 ? c->passes_done : 1);
+    for (size_t i = 0; i < 3 * static_cast<size_t>(c->n); ++i) rgb[i] = rgb[i] * (1.0 / d);
+    if (passes) *passes = c->passes_done;
+  });
+}
+
+int pxg_read_diag(pxg_ctx* c, long long* rows, int* touched, long long* pool) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<long long> d(kBuckets * 5);
+    std::vector<unsigned long long> at(kBuckets), ac(kBuckets);
+    std::vector<int> tc(kBuckets);
+    unsigned long long kept = 0;
+    CK(cudaMemcpy(d.data(), c->d_diag, sizeof(long long) * kBuckets * 5, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(at.data(), c->d_diag_attempt, sizeof(unsigned long long) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ac.data(), c->d_diag_accept, sizeof(unsigned long long) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tc.data(), c->d_diag_touched, sizeof(int) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&kept, c->d_kept_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < kBuckets; ++k) {
+      d[k * 5 + 0] = static_cast<long long>(at[k]);
+      d[k * 5 + 1] = static_cast<long long>(ac[k]);
+    }
+    if (rows) std::memcpy(rows, d.data(), sizeof(long long) * kBuckets * 5);
+    if (touched) std::memcpy(touched, tc.data(), sizeof(int) * kBuckets);
+    if (pool) {
+      pool[0] = c->pool_raw_total;
+      pool[1] = static_cast<long long>(kept);
+    }
+  });
+}
+
+int pxg_read_stats(pxg_ctx* c, double* stats3, long long* counts2, double* gamma_rows) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->stream1));
+    // after pass p the statistics are the snapshot Stage 2 of pass p used (a look-ahead
+    // Stage 1 may already have advanced the live tables)
+    const double *pmax = c->d_max_ratio, *psum = c->d_sum_est, *psq = c->d_sum_sq;
+    const long long *prc = c->d_ratio_cnt, *pec = c->d_est_cnt;
+    if (c->proxy_on && c->passes_done > 0) {
+      const PoolSlot& sl = c->slot_of(c->passes_done - 1);
+      pmax = sl.snap_max;
+      psum = sl.snap_sum;
+      psq = sl.snap_sq;
+      prc = sl.snap_rcnt;
+      pec = sl.snap_cnt;
+    }
+    std::vector<double> a(kBuckets), b(kBuckets), s(kBuckets);
+    std::vector<long long> rc(kBuckets), ec(kBuckets);
+    CK(cudaMemcpy(a.data(), pmax, sizeof(double) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), psum, sizeof(double) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(s.data(), psq, sizeof(double) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rc.data(), prc, sizeof(long long) * kBuckets, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ec.data(), pec, sizeof(long long) * kBuckets, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < kBuckets; ++k) {
+      if (stats3) {
+        stats3[3 * k] = a[k];
+        stats3[3 * k + 1] = b[k];
+        stats3[3 * k + 2] = s[k];
+      }
+      if (counts2) {
+        counts2[2 * k] = rc[k];
+        counts2[2 * k + 1] = ec[k];
+      }
+    }
+    if (gamma_rows) CK(cudaMemcpy(gamma_rows, c->d_gamma, sizeof(double) * kT * kS, cudaMemcpyDeviceToHost));
+  });
+}
+
+int pxg_dump_pass(pxg_ctx* c, double* val, double* bdpt, double* cc, int* flags) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t n = c->n;
+    if (val) CK(cudaMemcpy(val, c->d_val, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (bdpt) CK(cudaMemcpy(bdpt, c->d_bdpt, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (cc) {
+      std::vector<ProxRec> pr(n);
+      CK(cudaMemcpy(pr.data(), c->d_prox, sizeof(ProxRec) * n, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) cc[3 * i + k] = c->proxy_on ? pr[i].c[k] : 0.0;
+    }
+    if (flags) CK(cudaMemcpy(flags, c->d_pflags, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int pxg_dump_prims(pxg_ctx* c, int* eye, int* light) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t n = c->n;
+    if (eye) CK(cudaMemcpy(eye, c->d_eye_prims, sizeof(int) * n * (c->max_depth + 1), cudaMemcpyDeviceToHost));
+    if (light)
+      CK(cudaMemcpy(light, c->d_light_prims, sizeof(int) * n * std::max(c->max_depth - 1, 1), cudaMemcpyDeviceToHost));
+  });
+}
+
+int pxg_dump_pool(pxg_ctx* c, int cap, int* n_out, long long* raw, int* walk, int* end, int* key, double* inv_p,
+                  double* inv_p_m2, double* bound) {
+  return guarded(c, [&]() {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->stream1));
+    if (c->passes_done == 0 || !c->proxy_on) {
+      if (n_out) *n_out = 0;
+      if (raw) *raw = 0;
+      return;
+    }
+    const PoolSlot& sl = c->slot_of(c->passes_done - 1);
+    PassState ps;
+    CK(cudaMemcpy(&ps, sl.ps, sizeof(PassState), cudaMemcpyDeviceToHost));
+    const int n_ent = sl.n_ent;
+    std::vector<IncHdr> inc(n_ent);
+    std::vector<int> kept(std::max(ps.n_kept, 0));
+    std::vector<double> bd(n_ent);
+    if (n_ent) {
+      CK(cudaMemcpy(inc.data(), sl.inc, sizeof(IncHdr) * n_ent, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(bd.data(), sl.bound, sizeof(double) * n_ent, cudaMemcpyDeviceToHost));
+    }
+    if (ps.n_kept > 0) CK(cudaMemcpy(kept.data(), sl.kept, sizeof(int) * ps.n_kept, cudaMemcpyDeviceToHost));
+    const int m = std::min(cap, ps.n_kept);
+    for (int i = 0; i < m; ++i) {
+      const IncHdr& h = inc[kept[i]];
+      if (walk) walk[i] = h.walk;
+      if (end) end[i] = h.end;
+      if (key) key[i] = h.key;
+      if (inv_p) inv_p[i] = h.inverse_p;
+      if (inv_p_m2) inv_p_m2[i] = h.inverse_p_m2;
+      if (bound) bound[i] = bd[kept[i]];
+    }
+    if (n_out) *n_out = ps.n_kept;
+    if (raw) *raw = sl.raw;
+  });
+}
+
+int pxg_intersect(pxg_ctx* c, int n, const double* rays, const double* tmax, int* prim, double* t) {
+  return guarded(c, [&]() {
+    if (n <= 0) return;
+    double* dr = dupload(rays, static_cast<size_t>(n) * 6);
+    double* dt = tmax ? dupload(tmax, n) : nullptr;
+    int* dp = dalloc<int>(n);
+    double* dtt = dalloc<double>(n);
+    k_intersect<<<blocks(n, 128), 128, 0, c->stream>>>(c->S, n, dr, dt, dp, dtt);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(prim, dp, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(t, dtt, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dr);
+    if (dt) cudaFree(dt);
+    cudaFree(dp);
+    cudaFree(dtt);
+  });
+}
+
+int pxg_occluded(pxg_ctx* c, int n, const double* segs, int* occ) {
+  return guarded(c, [&]() {
+    if (n <= 0) return;
+    double* ds = dupload(segs, static_cast<size_t>(n) * 6);
+    int* dout = dalloc<int>(n);
+    k_occluded<<<blocks(n, 128), 128, 0, c->stream>>>(c->S, n, ds, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(occ, dout, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(ds);
+    cudaFree(dout);
+  });
+}
+
+int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double* est, long long* cost,
+                       int* truncated) {
+  return guarded(nullptr, [&]() {
+    if (!(bound > 0.0)) throw RuntimeErr{"reciprocal: bound must be positive"};
+    if (n <= 0) return;
+    if (cap < 0 || cap > (1 << 20)) throw InvalidErr{"pxg_recip_twopoint: cap out of range"};
+    const long long capa = std::max<long long>(cap, 1);
+    cudaStream_t st = nullptr;
+    std::vector<void*> tmp;
+    auto A = [&](size_t bytes) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, std::max<size_t>(bytes, 1)));
+      tmp.push_back(p);
+      return p;
+    };
+    try {
+      const size_t nc = static_cast<size_t>(n) * capa;
+      auto* de = static_cast<double*>(A(sizeof(double) * n));
+      auto* dc = static_cast<long long*>(A(sizeof(long long) * n));
+      auto* dt = static_cast<int*>(A(sizeof(int) * n));
+      auto* rs = static_cast<RunState*>(A(sizeof(RunState) * n));
+      auto* g = static_cast<double*>(A(sizeof(double) * nc));
+      auto* ns = static_cast<long long*>(A(sizeof(long long) * nc));
+      auto* ne = static_cast<int*>(A(sizeof(int) * nc));
+      auto* fr = static_cast<RecipFrame*>(A(sizeof(RecipFrame) * nc));
+      int* act[2] = {static_cast<int*>(A(sizeof(int) * n)), static_cast<int*>(A(sizeof(int) * n))};
+      auto* nact = static_cast<int*>(A(sizeof(int) * 2));
+      auto* derr = static_cast<int*>(A(sizeof(int)));
+      CK(cudaMemset(nact, 0, 2 * sizeof(int)));
+      CK(cudaMemset(derr, 0, sizeof(int)));
+      k_recip_init<<<blocks(n, 128), 128>>>(n, 1, 1, nullptr, rs, act[0], nact, de, dc, dt);
+      recip_rounds(st, nact, [&](int cur, int count, int chunk) {
+        k_twopoint_eval<<<blocks(static_cast<long long>(count) * chunk, 128), 128>>>(seed, bound, cap, act[cur],
+                                                                                     nact + cur, chunk, rs, g, ns, ne);
+        k_recip_dfs<<<blocks(count, 128), 128>>>(1, 1, cap, nullptr, bound, act[cur], nact + cur, chunk, rs, g, ns, ne,
+                                                 fr, de, dc, dt, act[1 - cur], nact + (1 - cur), derr);
+      });
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(est, de, sizeof(double) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(cost, dc, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(truncated, dt, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      for (void* p : tmp) cudaFree(p);
+      throw;
+    }
+    for (void* p : tmp) cudaFree(p);
+  });
+}
+
+int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out) {
+  return guarded(nullptr, [&]() {
+    if (n <= 0) return;
+    unsigned* d = dalloc<unsigned>(n);
+    k_rng<<<1, 1>>>(seed, kind, sub, stream, n, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, d, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  });
+}
+
+int pxg_read_timing(pxg_ctx* c, double* t, long long* counts) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  for (int k = 0; k < 8; ++k) t[k] = c->stage_ms[k];
+  if (counts) {
+    counts[0] = c->launches;
+    counts[1] = 0;
+  }
+  return PXG_OK;
+}
+
+}  // extern "C"

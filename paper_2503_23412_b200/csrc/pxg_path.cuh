@@ -227,10 +227,8 @@ struct PathTable {
   bool ld_done, ld_ok;
 };
 
-__device__ __forceinline__ double bsdf_step(const SceneView& S, const FullPath& fp, int at, int from, int to) {
-  const PV& v = fp.vtx(at);
-  const PV& vf = fp.vtx(from);
-  const PV& vt = fp.vtx(to);
+// bsdf_step of strategy_pdf (transport.cpp:226-234) / proxy_weight_density (proxy.cpp:469-477).
+__device__ __forceinline__ double bsdf_step_v(const SceneView& S, const PV& v, const PV& vf, const PV& vt) {
   V3 wi = normalize(vf.p - v.p);
   V3 wo_dir = vt.p - v.p;
   double len = length(wo_dir);
@@ -238,6 +236,26 @@ __device__ __forceinline__ double bsdf_step(const SceneView& S, const FullPath& 
   double pdf_w = pdf_bsdf(S.materials[v.mat], v.n, wi, wo_dir / len);
   return to_area_density(pdf_w, v.p, vt.p, vt.n);
 }
+
+__device__ __forceinline__ double bsdf_step(const SceneView& S, const FullPath& fp, int at, int from, int to) {
+  return bsdf_step_v(S, fp.vtx(at), fp.vtx(from), fp.vtx(to));
+}
+
+// Per-sub-path step densities shared by every connection of a pixel (strided by pixel):
+//   LF[i] = step(y[i-1] <- y[i-2] -> y[i])  i in [2, nl-1]   (light forward)
+//   LR[j] = step(y[j+1] <- y[j+2] -> y[j])  j in [0, nl-3]   (light reverse)
+//   EF[m] = step(e[m+1] <- e[m+2] -> e[m])  m in [0, ne-3]   (eye, light direction)
+//   ER[m] = step(e[m-1] <- e[m-2] -> e[m])  m in [2, ne-1]   (eye, eye direction)
+//   ld    = light_direction density y0 -> y1 (ld_ok = 0: strategy returns 0)
+struct PathCache {
+  double* LF;
+  double* LR;
+  double* EF;
+  double* ER;
+  double* ld;
+  int* ld_ok;
+  int n;  // stride (pixels)
+};
 
 __device__ __forceinline__ double tabF(const SceneView& S, const FullPath& fp, PathTable& T, int i) {
   if (!(T.fmask & (1u << i))) {
@@ -267,6 +285,40 @@ __device__ __forceinline__ void tabLD(const FullPath& fp, PathTable& T) {
   if (pdf_w <= 0.0) return;
   T.ld_ok = true;
   T.ld_area = to_area_density(pdf_w, y0.p, y1.p, y1.n);
+}
+
+// Pre-fills the memo table of connection (s, t) of pixel i from the per-sub-path caches;
+// only the junction steps (F(s), F(s+1), R(s-2), R(s-1)) and, for s = 1 or 0, the
+// light-direction factor remain to be evaluated. Values are the same function of the same
+// vertices, so every strategy density is bit-identical to the uncached table.
+__device__ __forceinline__ void table_init_cached(PathTable& T, const PathCache& C, int i, int s, int t) {
+  T.fmask = 0u;
+  T.rmask = 0u;
+  T.ld_done = false;
+  T.ld_ok = false;
+  const int n_v = s + t;
+  const size_t n = static_cast<size_t>(C.n);
+  for (int k = 2; k <= s - 1; ++k) {
+    T.F[k] = C.LF[k * n + i];
+    T.fmask |= 1u << k;
+  }
+  for (int k = s + 2; k <= n_v - 1; ++k) {
+    T.F[k] = C.EF[(n_v - 1 - k) * n + i];
+    T.fmask |= 1u << k;
+  }
+  for (int j = 0; j <= s - 3; ++j) {
+    T.R[j] = C.LR[j * n + i];
+    T.rmask |= 1u << j;
+  }
+  for (int j = s; j <= n_v - 3; ++j) {
+    T.R[j] = C.ER[(n_v - 1 - j) * n + i];
+    T.rmask |= 1u << j;
+  }
+  if (s >= 2) {
+    T.ld_done = true;
+    T.ld_ok = C.ld_ok[i] != 0;
+    T.ld_area = C.ld[i];
+  }
 }
 
 __device__ __forceinline__ void table_init(PathTable& T) {
@@ -386,10 +438,9 @@ __device__ __forceinline__ double proxy_weight_density(const SceneView& S, const
 }
 
 // reciprocal_mis_weight (proxy.cpp:533-546). cur_s < 0 selects the proxy strategy.
-__device__ __forceinline__ double reciprocal_mis_weight(const SceneView& S, const Mapper& M, const StatsView& st,
-                                                        const FullPath& fp, int cur_s, bool use_stats) {
-  PathTable T;
-  table_init(T);
+__device__ __forceinline__ double reciprocal_mis_weight_t(const SceneView& S, const Mapper& M, const StatsView& st,
+                                                          const FullPath& fp, PathTable& T, int cur_s,
+                                                          bool use_stats) {
   const double p_proxy = use_stats ? proxy_weight_density(S, M, st, fp, T) : 0.0;
   const double num = cur_s < 0 ? p_proxy : strategy_pdf(S, fp, T, cur_s);
   if (num <= 0.0) return 0.0;
@@ -398,6 +449,13 @@ __device__ __forceinline__ double reciprocal_mis_weight(const SceneView& S, cons
   for (int sp = 0; sp <= n_v - 2; ++sp) denom += strategy_pdf(S, fp, T, sp);
   denom += p_proxy;
   return num / denom;
+}
+
+__device__ __forceinline__ double reciprocal_mis_weight(const SceneView& S, const Mapper& M, const StatsView& st,
+                                                        const FullPath& fp, int cur_s, bool use_stats) {
+  PathTable T;
+  table_init(T);
+  return reciprocal_mis_weight_t(S, M, st, fp, T, cur_s, use_stats);
 }
 
 // connection_contribution (transport.cpp:187-196) incl. junction_kernels (:70-88).

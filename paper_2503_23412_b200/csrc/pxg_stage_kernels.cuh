@@ -1,0 +1,726 @@
+// pxg_stage_kernels.cuh — the per-pass kernels of proxy-BDPT (included by pxg_main.cu).
+//
+// One progressive pass (proj/src/proxy.cpp:683-827) is a fixed sequence of launches on the
+// context's stream:
+//   Stage 1 (pool, proxy.cpp:684-736)
+//     k_pool_walks    one thread per pool walk: light walk on its own Philox stream, every
+//                     dropout-eligible prefix end gets a 64-bit priority key
+//     (CUB radix sort of the keys; the pool_budget smallest are kept, ordered by walk,end)
+//     k_pool_entries  one thread per kept entry: re-trace its walk, dropout, 4 probes
+//     k_pool_bounds   one thread: probes -> bucket max in entry order -> B per entry
+//     k_recip_eval/   reciprocal runs in rounds: all pending tree nodes evaluated in parallel
+//     k_recip_dfs     (node-keyed streams), then each run's DFS resumes over them
+//     k_pool_finish   one thread: means, moments, validity, diagnostics, bucket lists
+//   Stage 2 (per pixel, proxy.cpp:738-819)
+//     k_trace         one thread per pixel: eye sub-path then light sub-path on the pixel's
+//                     persistent stream -> SoA vertex pools in HBM
+//     k_connect       one thread per pixel: all standard strategies with reciprocal-aware MIS
+//     k_proxy         one thread per pixel: gamma draw, pool pick, proxy_connect
+//                     (speculatively, before the gate is known)
+//     k_gate          one thread per 10x10 gate cell: the reference's scan-order gate,
+//                     proxy normalisation, film accumulation, grid shares
+//   then the gamma rows are rebuilt from the pixel-order contribution sum.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <string>
+#include <vector>
+
+#include "pxg.h"
+#include "pxg_host.h"
+#include "pxg_wave.cuh"
+
+using namespace pxg;
+
+namespace {
+
+constexpr int kBuckets = 4000;
+constexpr int kS = 100, kT = 32;
+thread_local std::string g_global_err;
+
+struct ProxRec {
+  double c[3];
+  double u_gate;
+  double q_sel;
+  int t_label, chosen, key, flags;  // flags bit0 tp>=2, bit1 attempted, bit2 z_norm>0
+};
+
+
+
+struct PassState {  // device-resident per-pass scalars
+  double kappa;
+  int n_kept;
+  int err;
+  long long pool_kept_total;
+};
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct CudaErr {
+  std::string msg;
+  explicit CudaErr(std::string m) : msg(std::move(m)) {}
+};
+struct InvalidErr {
+  std::string msg;
+};
+struct RuntimeErr {
+  std::string msg;
+};
+
+template <typename T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+template <typename T>
+T* dupload(const T* src, size_t n) {
+  T* p = dalloc<T>(n);
+  if (n) CK(cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+__device__ __forceinline__ Rng make_rng(uint64_t seed, uint32_t kind, uint32_t sub, uint64_t stream) {
+  Rng r;
+  r.r = pxg_rng_make(seed, kind, sub, stream);
+  return r;
+}
+
+__device__ __forceinline__ uint64_t unit_stream(int pass, int walk) {
+  return (static_cast<uint64_t>(pass) << 32) | static_cast<uint32_t>(walk);
+}
+
+__device__ __forceinline__ void set_err(int* err, int code) { atomicCAS(err, 0, code); }
+
+// ------------------------------------------------------------------ Stage 1 kernels
+// Eligible prefix ends of the traced pool walks get a 64-bit priority key each
+// (the priority-reservoir replacement of Algorithm R, proxy.cpp:696-711).
+__global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, uint64_t seed, int pass, int walk_begin,
+                            unsigned long long* keys, unsigned* vals, int* count, int cap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_walks) return;
+  const int w = walk_begin + i;
+  const int n = wnv[i];
+  int flag[kMaxLight], emitter[kMaxLight];
+  double pdf[kMaxLight];
+  for (int k = 0; k < n; ++k) {
+    const PV& v = wpool[static_cast<size_t>(k) * n_walks + i];
+    flag[k] = v.flag;
+    emitter[k] = v.emitter;
+    pdf[k] = v.pdf_fwd;
+  }
+  for (int end = 2; end <= n; ++end) {
+    if (flag[end - 1] != kSpecular) continue;
+    if (!dropout_eligible(flag, emitter, pdf, end)) continue;
+    Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
+    unsigned long long hi = pxg_next_u32(&kr.r);
+    unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
+    int slot = atomicAdd(count, 1);
+    if (slot < cap) {
+      keys[slot] = key;
+      vals[slot] = (static_cast<unsigned>(w) << 5) | static_cast<unsigned>(end);
+    }
+  }
+}
+
+// Materialise the kept entries (dropout on the stored walk prefix, proxy.cpp:59-94).
+__global__ void k_pool_entries(Mapper M, int n_ent, const unsigned* sel, const PV* wpool, int n_walks, int walk_begin,
+                               IncHdr* inc, PV* prefix) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_ent) return;
+  const int w = static_cast<int>(sel[k] >> 5), end = static_cast<int>(sel[k] & 31u);
+  PV v[kMaxLight];
+  for (int q = 0; q < end; ++q) v[q] = wpool[static_cast<size_t>(q) * n_walks + (w - walk_begin)];
+  IncHdr h;
+  const bool ok = dropout(M, v, end, h, prefix + static_cast<size_t>(k) * kMaxLight);
+  h.walk = w;
+  h.end = end;
+  h.valid = ok ? 1 : 0;
+  inc[k] = h;
+}
+
+// The four f/q probes of every entry (estimate_inverse_p, proxy.cpp:389-394), one thread
+// per probe on its own stream (PROBE, end | i << 8).
+__global__ void k_pool_probes(SceneView S, uint64_t seed, int pass, int n_ent, const IncHdr* inc, const PV* prefix,
+                              double* probe, int* probe_ok, int repeats) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * n_ent) return;
+  const int k = t >> 2, i = t & 3;
+  probe_ok[t] = 0;
+  const IncHdr& h = inc[k];
+  if (!h.valid || repeats < 1) return;
+  const PV* pre = prefix + static_cast<size_t>(k) * kMaxLight;
+  Rng pr = make_rng(seed, PXG_KIND_PROBE, static_cast<uint32_t>(h.end) | (static_cast<uint32_t>(i) << 8),
+                    unit_stream(pass, h.walk));
+  Cand c;
+  support_sample(S, h, pre, pr, c);
+  if (!(c.q > 0.0)) return;
+  const double f = c.escaped ? 0.0 : target_density(S, h, pre, c.g);
+  probe[t] = f / c.q;
+  probe_ok[t] = 1;
+}
+
+// pretrace_statistics (proj/src/subspace.cpp:190-218), one Philox stream per walk. The
+// bucket max and count are order-independent, so atomics reproduce the sequential result.
+__global__ void k_pretrace(SceneView S, Mapper M, uint64_t seed, int n_paths, double* max_ratio,
+                           long long* ratio_cnt, int* touched, int* err) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_paths) return;
+  Rng rng = make_rng(seed, PXG_KIND_PRETRACE, 0, static_cast<uint64_t>(w));
+  PV v[7];
+  const int n = trace_light_subpath(S, 7, rng, v, 1);
+  for (int end = 2; end <= n; ++end) {
+    if (v[end - 1].flag != kSpecular) continue;
+    IncHdr h;
+    if (!dropout(M, v, end, h, nullptr)) continue;
+    for (int probe = 0; probe < 2; ++probe) {
+      Cand c;
+      support_sample(S, h, v, rng, c);
+      if (!(c.q > 0.0)) continue;
+      const double f = c.escaped ? 0.0 : target_density(S, h, v, c.g);
+      const double r = f / c.q;
+      if (!isfinite(r) || r < 0.0) {
+        set_err(err, kErrRatio);
+        return;
+      }
+      atomicMax(reinterpret_cast<unsigned long long*>(max_ratio + h.key),
+                static_cast<unsigned long long>(__double_as_longlong(r)));
+      atomicAdd(reinterpret_cast<unsigned long long*>(ratio_cnt + h.key), 1ull);
+      touched[h.key] = 1;
+    }
+  }
+}
+
+// B of entry k = 2 * max over the bucket's ratio history and the probes of entries <= k
+// of the same bucket (the sequential update_ratio/b_bound order of proxy.cpp:389-395).
+// Maxima are order-independent, so every entry computes its own prefix maximum; the last
+// entry of each bucket then commits the bucket state. One block.
+__global__ void k_pool_bounds(int n_ent, const IncHdr* inc, const double* probe, const int* probe_ok,
+                              double* max_ratio, long long* ratio_cnt, int* touched, double* bound, int* err) {
+  extern __shared__ double sm[];  // [n_ent] max, then [n_ent] touched flags (as double)
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    const int key = inc[k].key;
+    double m = max_ratio[key];
+    int tch = touched[key];
+    for (int k2 = 0; k2 <= k; ++k2) {
+      if (!inc[k2].valid || inc[k2].key != key) continue;
+      for (int i = 0; i < 4; ++i) {
+        if (!probe_ok[k2 * 4 + i]) continue;
+        const double r = probe[k2 * 4 + i];
+        if (!isfinite(r) || r < 0.0) {
+          set_err(err, kErrRatio);
+          continue;
+        }
+        m = dmax(m, r);
+        tch = 1;
+      }
+    }
+    bound[k] = (inc[k].valid && tch) ? 2.0 * m : 0.0;
+    sm[k] = m;
+    sm[n_ent + k] = tch;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    if (!inc[k].valid) continue;
+    const int key = inc[k].key;
+    bool last = true;
+    long long cnt = 0;
+    for (int k2 = 0; k2 < n_ent; ++k2) {
+      if (!inc[k2].valid || inc[k2].key != key) continue;
+      if (k2 > k) last = false;
+      for (int i = 0; i < 4; ++i) cnt += probe_ok[k2 * 4 + i];
+    }
+    if (!last) continue;
+    max_ratio[key] = sm[k];
+    ratio_cnt[key] += cnt;
+    if (sm[n_ent + k] != 0.0) touched[key] = 1;
+  }
+}
+
+// One pass of a Stage-1 batch, as seen by the reciprocal-run kernels. Run j of a batch is
+// (pass b = j / stride, entry e = (j % stride) / repeats, run r = j % repeats).
+struct BatchPass {
+  const IncHdr* inc;
+  const PV* prefix;
+  const double* bound;
+  int pass;
+  int n_ent;
+};
+
+// Phase A of the reciprocal runs: evaluate nodes [avail, avail + chunk) of every active
+// run in parallel. Node k draws its support sample from (RECIP_NODE, k) and its split
+// decision from (RECIP_SPLIT, k) (include/pxg_philox.h), so its value does not depend on
+// the tree shape; draw_g (recip.hpp:69-77) and stochastic_split (recip.hpp:49-56).
+__global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride, long long cap,
+                             const BatchPass* bp, const int* active, const int* n_active, int chunk,
+                             const RunState* st, double* g, long long* nsplit, int* nerr) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long a = tid / chunk;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  const long long k = st[j].avail + tid % chunk;
+  if (k >= cap) return;
+  const BatchPass& P = bp[j / stride];
+  const int w = j % stride;
+  const int e = w / repeats, r = w % repeats;
+  const IncHdr& h = P.inc[e];
+  const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+  const double B = P.bound[e];
+  const uint64_t stream = pxg_recip_stream(P.pass, h.walk, h.end, r);
+  Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), stream);
+  int err = 0;
+  const double gv = draw_g(S, h, pre, B, nr, err);
+  long long n = 0;
+  if (!err) {
+    Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), stream);
+    n = split_count(gv, sr, err);
+  }
+  const size_t o = static_cast<size_t>(j) * cap + k;
+  g[o] = gv;
+  nsplit[o] = n;
+  nerr[o] = err;
+}
+
+// The two-point fixture f = {1, 3}, q = 1/2 (proj/tests/test_recip.cpp:16-23) as Phase A.
+__global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, const int* active, const int* n_active,
+                                int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long a = tid / chunk;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  const long long k = st[j].avail + tid % chunk;
+  if (k >= cap) return;
+  Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
+  const int x = nr.next_double() < 0.5 ? 0 : 1;
+  const double fx = x == 0 ? 1.0 : 3.0;
+  const double gv = 1.0 - fx / (bound * 0.5);
+  int err = 0;
+  Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
+  const long long n = split_count(gv, sr, err);
+  const size_t o = static_cast<size_t>(j) * cap + k;
+  g[o] = gv;
+  nsplit[o] = n;
+  nerr[o] = err;
+}
+
+// bp == nullptr: every run is live (the two-point fixture).
+__global__ void k_recip_init(int runs, int repeats, int stride, const BatchPass* bp, RunState* st, int* active,
+                             int* n_active, double* est, long long* cost, int* trunc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= runs) return;
+  RunState s;
+  s.depth = s.cost = s.avail = 0;
+  s.ret = 0.0;
+  s.entering = 1;
+  s.truncated = 0;
+  s.err = 0;
+  bool live = true;
+  if (bp) {
+    const BatchPass& P = bp[j / stride];
+    const int e = (j % stride) / repeats;
+    live = e < P.n_ent && P.inc[e].valid && P.bound[e] > 0.0;
+  }
+  s.done = live ? 0 : 1;
+  st[j] = s;
+  est[j] = 0.0;
+  cost[j] = 0;
+  trunc[j] = 0;
+  if (live) active[atomicAdd(n_active, 1)] = j;
+}
+
+// Phase B: resume the DFS of every active run over its newly evaluated nodes.
+__global__ void k_recip_dfs(int repeats, int stride, long long cap, const BatchPass* bp, double fixed_bound,
+                            const int* active, const int* n_active, int chunk, RunState* st, const double* g,
+                            const long long* nsplit, const int* nerr, RecipFrame* frames, double* est,
+                            long long* cost, int* trunc, int* next, int* n_next, int* err) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= *n_active) return;
+  const int j = active[a];
+  RunState s = st[j];
+  s.avail = min(cap, s.avail + chunk);
+  const double B = bp ? bp[j / stride].bound[(j % stride) / repeats] : fixed_bound;
+  const size_t o = static_cast<size_t>(j) * cap;
+  const bool done = dfs_resume(s, g + o, nsplit + o, nerr + o, frames + o, B, cap);
+  st[j] = s;
+  if (!done) {
+    next[atomicAdd(n_next, 1)] = j;
+    return;
+  }
+  if (s.err) {
+    set_err(err, s.err);
+    return;
+  }
+  est[j] = s.ret;
+  cost[j] = s.cost;
+  trunc[j] = s.truncated;
+}
+
+// Per entry: mean and second moment of its runs, validity (proxy.cpp:409-427); per bucket
+// the estimate sums in pool order; the kept list and the per-label lists in pool order
+// (proxy.cpp:729-735); then the stats snapshot Stage 2 of this pass reads. One block.
+__global__ void k_pool_finish(int n_ent, int repeats, IncHdr* inc, const double* bound, const double* est,
+                              const int* trunc, double* sum_est, double* sum_sq, long long* est_cnt, int* touched,
+                              long long* diag, int* diag_touched, int* kept, int* label_start, int* label_list,
+                              PassState* ps, double* snap_sum, double* snap_sq, long long* snap_cnt,
+                              const double* max_ratio, const long long* ratio_cnt, double* snap_max,
+                              long long* snap_rcnt) {
+  extern __shared__ int smi[];  // [n_ent] valid flags, [kS] label counts
+  int* ok = smi;
+  int* lcount = smi + n_ent;
+  for (int s = threadIdx.x; s < kS; s += blockDim.x) lcount[s] = 0;
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    IncHdr& h = inc[k];
+    ok[k] = 0;
+    if (!h.valid) continue;
+    const int key = h.key;
+    diag_touched[key] = 1;
+    bool valid = false;
+    if (repeats >= 1 && bound[k] > 0.0) {
+      double sum = 0.0, sq = 0.0;
+      long long tr = 0;
+      for (int r = 0; r < repeats; ++r) {
+        const double e = est[k * repeats + r];
+        sum += e;
+        sq += e * e;
+        tr += trunc[k * repeats + r];
+      }
+      const double mean = sum / repeats;
+      const double m2 = sq / repeats;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 3]), static_cast<unsigned long long>(tr));
+      if (isfinite(mean) && mean > 0.0) {
+        valid = true;
+        h.inverse_p = mean;
+        h.inverse_p_m2 = m2;
+      }
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 2]), static_cast<unsigned long long>(repeats));
+    if (!valid) atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 4]), 1ull);
+    ok[k] = valid ? 1 : 0;
+  }
+  __syncthreads();
+  // bucket sums in pool order (SubspaceStats::update_estimate, subspace.cpp:64-70)
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    if (!ok[k]) continue;
+    const int key = inc[k].key;
+    bool last = true;
+    for (int k2 = k + 1; k2 < n_ent; ++k2)
+      if (ok[k2] && inc[k2].key == key) {
+        last = false;
+        break;
+      }
+    if (!last) continue;
+    double se = sum_est[key], sq = sum_sq[key];
+    long long cnt = est_cnt[key];
+    for (int k2 = 0; k2 <= k; ++k2) {
+      if (!ok[k2] || inc[k2].key != key) continue;
+      const double m = inc[k2].inverse_p;
+      se += m;
+      sq += m * m;
+      ++cnt;
+    }
+    sum_est[key] = se;
+    sum_sq[key] = sq;
+    est_cnt[key] = cnt;
+    touched[key] = 1;
+  }
+  // kept list and label lists, both in pool order
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    if (!ok[k]) continue;
+    int pos = 0;
+    for (int k2 = 0; k2 < k; ++k2) pos += ok[k2];
+    kept[pos] = k;
+    atomicAdd(&lcount[inc[k].s_label], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0, nk = 0;
+    for (int s = 0; s < kS; ++s) {
+      label_start[s] = acc;
+      acc += lcount[s];
+    }
+    label_start[kS] = acc;
+    for (int k = 0; k < n_ent; ++k) nk += ok[k];
+    ps->n_kept = nk;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
+    if (!ok[k]) continue;
+    const int sl = inc[k].s_label;
+    int pos = label_start[sl];
+    for (int k2 = 0; k2 < k; ++k2)
+      if (ok[k2] && inc[k2].s_label == sl) ++pos;
+    label_list[pos] = k;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
+    snap_sum[b] = sum_est[b];
+    snap_sq[b] = sum_sq[b];
+    snap_cnt[b] = est_cnt[b];
+  }
+}
+
+// A pass's Stage-1 diagnostics are folded into the context totals only when the pass is
+// rendered, so a look-ahead Stage 1 never shows up in ProxyDiagnostics early.
+__global__ void k_fold_diag(const long long* sdiag, const int* stouched, const PassState* ps, long long* diag,
+                            int* touched, unsigned long long* kept_total) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) atomicAdd(kept_total, static_cast<unsigned long long>(ps->n_kept));
+  if (b >= kBuckets) return;
+  for (int k = 2; k < 5; ++k) diag[b * 5 + k] += sdiag[b * 5 + k];
+  if (stouched[b]) touched[b] = 1;
+}
+
+// GammaMatrix::record_contribution in pixel scan order (proxy.cpp:807-808) + end_iteration
+// (subspace.cpp:164-182). Input: contributions stably sorted by bin (pixel order kept).
+__global__ void k_gamma_update(int n, const int* bins_sorted, const double* vals_sorted, double* accum, double* rows,
+                               int learning) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per (t, s) bin
+  if (b < kT * kS && learning) {
+    // segment of bin b+1 (key 0 = no contribution)
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (bins_sorted[mid] < b + 1) lo = mid + 1; else hi = mid;
+    }
+    double acc = accum[b];
+    for (int k = lo; k < n && bins_sorted[k] == b + 1; ++k) {
+      const double v = vals_sorted[k];
+      if (!isfinite(v) || v < 0.0) continue;
+      acc += v;
+    }
+    accum[b] = acc;
+  }
+}
+
+__global__ void k_gamma_rows(const double* accum, double* rows) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kT) return;
+  const double eps = 1e-3 / kS;
+  double* row = rows + t * kS;
+  const double* acc = accum + t * kS;
+  double total = 0.0;
+  for (int s = 0; s < kS; ++s) total += acc[s];
+  if (total <= 0.0) {
+    for (int s = 0; s < kS; ++s) row[s] = 1.0 / kS;
+    return;
+  }
+  const double keep = 1.0 - eps * kS;
+  for (int s = 0; s < kS; ++s) row[s] = keep * (acc[s] / total) + eps;
+}
+
+// ------------------------------------------------------------------ Stage 2 kernels
+struct Stage2 {
+  SceneView S;
+  Mapper M;
+  StatsView st;
+  PV* eye;
+  PV* light;
+  int* n_eye;
+  int* n_light;
+  unsigned* ctr;
+  double* bdpt;  // [n*3]
+  int* eye_prims;
+  int* light_prims;
+  int n, row0, width, height, max_depth;
+  uint64_t seed;
+  int record_prims;
+};
+
+__global__ void k_record_prims(const PV* eye, const int* n_eye, const PV* light, const int* n_light, int n,
+                               int max_depth, int* eye_prims, int* light_prims) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ne = n_eye[i], nl = n_light[i];
+  for (int k = 0; k <= max_depth; ++k)
+    eye_prims[static_cast<size_t>(i) * (max_depth + 1) + k] = k < ne ? eye[static_cast<size_t>(k) * n + i].prim : -2;
+  for (int k = 0; k < max_depth - 1; ++k)
+    light_prims[static_cast<size_t>(i) * (max_depth - 1) + k] =
+        k < nl ? light[static_cast<size_t>(k) * n + i].prim : -2;
+}
+
+__global__ void k_proxy(Stage2 P, int pass, int n_px_total, const IncHdr* inc, const PV* prefix,
+                        const int* label_start, const int* label_list, const double* gamma_rows,
+                        const PassState* ps, ProxRec* out, PV* scratch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  ProxRec o;
+  o.c[0] = o.c[1] = o.c[2] = 0.0;
+  o.u_gate = 0.0;
+  o.q_sel = 0.0;
+  o.t_label = o.chosen = o.key = -1;
+  o.flags = 0;
+  if (ps->n_kept <= 0) {
+    out[i] = o;
+    return;
+  }
+  const PV* eye = P.eye + i;
+  const size_t es = static_cast<size_t>(P.n);
+  const int ne = P.n_eye[i];
+  int tp = 0;
+  for (int k = 1; k < ne; ++k) {
+    const int f = eye[k * es].flag;
+    if (f == kDiffuse) {
+      tp = k + 1;
+      break;
+    }
+    if (f != kSpecular) break;
+  }
+  if (tp < 2) {
+    out[i] = o;
+    return;
+  }
+  o.flags |= 1;
+  const int idx = P.row0 * P.width + i;
+  Rng prox = make_rng(P.seed, PXG_KIND_REF, 0,
+                      (uint64_t(2) << 32) + static_cast<uint64_t>(pass) * static_cast<uint64_t>(n_px_total) + idx);
+  o.u_gate = prox.next_double();
+  const PV& z = eye[(tp - 1) * es];
+  const int t_label = classify_eye(P.M, z.p, -z.wi);
+  const double* row = gamma_rows + t_label * kS;
+  double z_norm = 0.0;
+  for (int sl = 0; sl < kS; ++sl)
+    if (label_start[sl + 1] > label_start[sl]) z_norm += row[sl];
+  if (!(z_norm > 0.0)) {
+    out[i] = o;
+    return;
+  }
+  o.flags |= 4;
+  const double uu = prox.next_double() * z_norm;
+  int chosen = -1;
+  double cdf = 0.0;
+  for (int sl = 0; sl < kS; ++sl) {
+    if (label_start[sl + 1] == label_start[sl]) continue;
+    chosen = sl;
+    cdf += row[sl];
+    if (uu < cdf) break;
+  }
+  const double row_p = row[chosen] / z_norm;
+  const int bsize = label_start[chosen + 1] - label_start[chosen];
+  const int e = label_list[label_start[chosen] + static_cast<int>(prox.next_below(static_cast<uint32_t>(bsize)))];
+  const IncHdr& h = inc[e];
+  const int s_rep = h.n_prefix + h.u + 1;
+  o.t_label = t_label;
+  o.chosen = chosen;
+  o.key = h.key;
+  o.q_sel = row_p / static_cast<double>(bsize);
+  if (s_rep + tp <= P.max_depth + 1) {
+    o.flags |= 2;
+    V3 c = proxy_connect(P.S, P.M, P.st, eye, es, tp, h, prefix + static_cast<size_t>(e) * kMaxLight, prox,
+                         scratch + static_cast<size_t>(i) * kMaxLight);
+    o.c[0] = c.x;
+    o.c[1] = c.y;
+    o.c[2] = c.z;
+  }
+  out[i] = o;
+}
+
+// Per 10x10 cell in the reference's scan order (proxy.cpp:761-817).
+__global__ void k_gate(int n_cells, int grid_w, int row0, int rows, int width, int pass, double gate_high,
+                       double gate_low, double gate_threshold, double light_walks, int proxy_on,
+                       const PassState* ps, const double* bdpt, const ProxRec* prox, double* acc, double* val,
+                       double* grid_total, double* grid_proxy, int* gbin, double* gval, int* pflags,
+                       unsigned long long* diag_attempt, unsigned long long* diag_accept, int* diag_touched) {
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= n_cells) return;
+  const int cx = cell % grid_w, cy = cell / grid_w;
+  const double kappa = ps->kappa;
+  const int y_end = min(rows, cy * 10 + 10);
+  const int x_end = min(width, cx * 10 + 10);
+  double gt = grid_total[cell], gp = grid_proxy[cell];
+  for (int y = cy * 10; y < y_end; ++y) {
+    for (int x = cx * 10; x < x_end; ++x) {
+      const int i = y * width + x;
+      V3 v = v3(bdpt[3 * i], bdpt[3 * i + 1], bdpt[3 * i + 2]);
+      int fl = 0;
+      int gb = 0;  // 0: no gamma contribution, else t*100 + s + 1
+      double gv = 0.0;
+      if (proxy_on) {
+        const ProxRec& o = prox[i];
+        fl = o.flags & 1;
+        if (o.flags & 1) {
+          double gate = gate_high;
+          if (pass > 0) {
+            double share = gt > 0.0 ? gp / gt : 0.0;
+            gate = share > gate_threshold ? gate_high : gate_low;
+          }
+          if (gate > 0.0 && o.u_gate < gate && (o.flags & 4)) {
+            fl |= 4;
+            if (o.flags & 2) {
+              fl |= 2;
+              atomicAdd(&diag_attempt[o.key], 1ull);
+              diag_touched[o.key] = 1;
+              V3 c = v3(o.c[0], o.c[1], o.c[2]);
+              if (!near_zero(c)) {
+                fl |= 8;
+                atomicAdd(&diag_accept[o.key], 1ull);
+                V3 contrib = c / (light_walks * kappa * gate * o.q_sel);
+                v += contrib;
+                gb = o.t_label * kS + o.chosen + 1;
+                gv = luminance(c) / o.q_sel;
+                gp += luminance(contrib);
+              }
+            }
+          }
+        }
+      }
+      acc[3 * i] += v.x;
+      acc[3 * i + 1] += v.y;
+      acc[3 * i + 2] += v.z;
+      val[3 * i] = v.x;
+      val[3 * i + 1] = v.y;
+      val[3 * i + 2] = v.z;
+      gt += luminance(v);
+      gbin[i] = gb;
+      gval[i] = gv;
+      pflags[i] = fl;
+    }
+  }
+  grid_total[cell] = gt;
+  grid_proxy[cell] = gp;
+}
+
+// ------------------------------------------------------------------ test kernels
+__global__ void k_intersect(SceneView S, int n, const double* rays, const double* tmax, int* prim, double* t) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* r = rays + 6 * static_cast<size_t>(i);
+  Hit h;
+  double tm = tmax ? tmax[i] : 1e30;
+  if (intersect(S, v3(r[0], r[1], r[2]), v3(r[3], r[4], r[5]), h, tm)) {
+    prim[i] = h.prim;
+    t[i] = h.t;
+  } else {
+    prim[i] = -1;
+    t[i] = 0.0;
+  }
+}
+
+__global__ void k_occluded(SceneView S, int n, const double* segs, int* occ) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = segs + 6 * static_cast<size_t>(i);
+  occ[i] = occluded(S, v3(s[0], s[1], s[2]), v3(s[3], s[4], s[5])) ? 1 : 0;
+}
+
+__global__ void k_rng(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  PxgRng r = pxg_rng_make(seed, kind, sub, stream);
+  for (int i = 0; i < n; ++i) out[i] = pxg_next_u32(&r);
+}
+
+inline int blocks(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+}  // namespace
+

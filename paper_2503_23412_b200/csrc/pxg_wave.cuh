@@ -210,8 +210,9 @@ struct ConnBuf {
   int2* desc;      // [slot] pixel, t << 8 | s
   double* value;   // [slot*3]
   int* state;      // [slot] 0 nothing, 1 contributes, 2 waiting for visibility
-  int* shadow_slot;  // [shadow queue slot] -> connection slot
   int* total;      // device scalar: number of slots
+  int* live;       // [slot] compacted list of slots whose value needs the MIS weight
+  int* n_live;     // device scalar
 };
 
 __global__ void k_conn_count(const int* n_eye, const int* n_light, int n, int max_depth, int* count) {
@@ -301,26 +302,63 @@ __global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, 
   C.value[3 * g + 1] = val.y;
   C.value[3 * g + 2] = val.z;
   C.state[g] = state;
+  if (state == 1) C.live[atomicAdd(C.n_live, 1)] = g;
 }
 
 __global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= *shadow.count) return;
   const int g = shadow.path[q];
-  C.state[g] = shadow.hit_prim[q] ? 0 : 1;  // occluded -> no contribution
+  const int vis = shadow.hit_prim[q] ? 0 : 1;  // occluded -> no contribution
+  C.state[g] = vis;
+  if (vis) C.live[atomicAdd(C.n_live, 1)] = g;
 }
 
-// reciprocal_mis_weight per contributing slot; value <- value * w.
+// Per-pixel sub-path step densities (PathCache), evaluated once per pixel and pass.
+__global__ void k_path_factors(SceneView S, const PV* eye, const int* n_eye, const PV* light, const int* n_light,
+                               int n, PathCache C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t st = static_cast<size_t>(n);
+  const int nl = n_light[i], ne = n_eye[i];
+  const PV* y = light + i;
+  const PV* e = eye + i;
+  for (int k = 2; k <= nl - 1; ++k) C.LF[k * st + i] = bsdf_step_v(S, y[(k - 1) * st], y[(k - 2) * st], y[k * st]);
+  for (int j = 0; j <= nl - 3; ++j) C.LR[j * st + i] = bsdf_step_v(S, y[(j + 1) * st], y[(j + 2) * st], y[j * st]);
+  for (int m = 0; m <= ne - 3; ++m) C.EF[m * st + i] = bsdf_step_v(S, e[(m + 1) * st], e[(m + 2) * st], e[m * st]);
+  for (int m = 2; m <= ne - 1; ++m) C.ER[m * st + i] = bsdf_step_v(S, e[(m - 1) * st], e[(m - 2) * st], e[m * st]);
+  int ok = 0;
+  double area = 0.0;
+  if (nl >= 2) {
+    const PV& y0 = y[0];
+    const PV& y1 = y[st];
+    V3 d = y1.p - y0.p;
+    double len = length(d);
+    if (len > 0.0) {
+      double pdf_w = light_direction_pdf(y0.n, d / len);
+      if (pdf_w > 0.0) {
+        ok = 1;
+        area = to_area_density(pdf_w, y0.p, y1.p, y1.n);
+      }
+    }
+  }
+  C.ld_ok[i] = ok;
+  C.ld[i] = area;
+}
+
+// reciprocal_mis_weight of every live slot; value <- value * w.
 __global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
-                           int n, ConnBuf C) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= *C.total) return;
-  if (C.state[g] != 1) return;
+                           int n, ConnBuf C, PathCache PC) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= *C.n_live) return;
+  const int g = C.live[q];
   const int2 dsc = C.desc[g];
   const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
   const size_t st_ = static_cast<size_t>(n);
   FullPath fp{light + i, st_, eye + i, st_, s, t};
-  const double w = reciprocal_mis_weight(S, M, st, fp, s, use_stats != 0);
+  PathTable T;
+  table_init_cached(T, PC, i, s, t);
+  const double w = reciprocal_mis_weight_t(S, M, st, fp, T, s, use_stats != 0);
   C.value[3 * g] = C.value[3 * g] * w;
   C.value[3 * g + 1] = C.value[3 * g + 1] * w;
   C.value[3 * g + 2] = C.value[3 * g + 2] * w;

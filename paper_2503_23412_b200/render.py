@@ -169,6 +169,10 @@ class ProxyRenderer:
     def render_passes(self, n: int = 1):
         self._check(self._L.pxg_render_passes(self._ctx, n))
 
+    def set_pass_limit(self, limit: int):
+        """No look-ahead Stage 1 for passes >= limit (the render's spp)."""
+        self._check(self._L.pxg_set_pass_limit(self._ctx, int(limit)))
+
     def render_pass_traced(self):
         """One pass that also records the sub-path primitive ids (dump_prims)."""
         self._check(self._L.pxg_render_pass_traced(self._ctx))
@@ -257,6 +261,7 @@ def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | N
     if spp <= 0:
         spp = scene.settings.spp
     with ProxyRenderer(scene, seed, params, device=device) as r:
+        r.set_pass_limit(spp)
         done = 0
         for _ in range(spp):
             r.render_passes(1)
