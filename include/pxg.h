@@ -109,6 +109,12 @@ int pxg_render_passes(pxg_ctx* ctx, int n);
 /* Total number of passes the caller intends to render (the spp of the render call): no
  * look-ahead Stage 1 is started for pass >= limit. -1 (default) = unbounded. */
 int pxg_set_pass_limit(pxg_ctx* ctx, int limit);
+/* Renders `n` passes in measurement mode: every traversal launch (closest hit / any hit)
+ * is bracketed by CUDA events on its stream and followed by an instrumented copy on the
+ * same rays that counts BVH node visits (64 B each) and primitive tests (80 B each).
+ * out[10] = {closest: ms, launches, rays, node visits, prim tests,
+ *            any-hit: ms, launches, rays, node visits, prim tests}. */
+int pxg_measure_traversal(pxg_ctx* ctx, int n, double* out);
 int pxg_synchronize(pxg_ctx* ctx);
 
 /* Running mean acc/done over this context's rows, row-major fp64 RGB, y = 0 top

@@ -133,6 +133,24 @@ struct pxg_ctx {
   cudaEvent_t ev_call[3];
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
+  // traversal roofline measurement (pxg_measure_traversal)
+  bool measure = false;
+  unsigned long long* d_tcnt = nullptr;  // closest {rays, nodes, prims}, any-hit {rays, nodes, prims}
+  struct TimedLaunch {
+    cudaEvent_t a, b;
+    int kind;  // 0 closest, 1 any-hit
+  };
+  std::vector<TimedLaunch> tl;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t take_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
 
   template <typename T>
   T* alloc(size_t n_) {
@@ -161,6 +179,7 @@ struct pxg_ctx {
     if (d_gsort_tmp) cudaFree(d_gsort_tmp);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& e : ev_call) if (e) cudaEventDestroy(e);
+    for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& sl : slot)
       for (cudaEvent_t e : {sl.s1_done, sl.s2_done, sl.t0, sl.t1, sl.r0, sl.r1})
         if (e) cudaEventDestroy(e);
@@ -222,7 +241,16 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
     k_light_start<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in);
   ++c->launches;
   for (int b = 0; b + 1 < P.max_vertices; ++b) {
-    k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+    if (c->measure) {
+      pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 0};
+      CK(cudaEventRecord(t.a, st));
+      k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+      CK(cudaEventRecord(t.b, st));
+      k_closest_count<<<blocks(P.n, T), T, 0, st>>>(c->S, in, c->d_tcnt);
+      c->tl.push_back(t);
+    } else {
+      k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+    }
     CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
     k_shade<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, out);
     c->launches += 2;
@@ -243,7 +271,16 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
   const long long slots = static_cast<long long>(n) * c->max_slots;
   k_conn_eval<<<blocks(slots, T), T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
-  k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+  if (c->measure) {
+    pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 1};
+    CK(cudaEventRecord(t.a, st));
+    k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+    CK(cudaEventRecord(t.b, st));
+    k_anyhit_count<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS, c->d_tcnt + 3);
+    c->tl.push_back(t);
+  } else {
+    k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+  }
   k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
   k_conn_mis<<<blocks(slots, T), T, 0, st>>>(c->S, c->M,
                                              StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
@@ -856,6 +893,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_rnact = c->zeros<int>(2);
     c->d_err = c->zeros<int>(1);
     c->d_kept_total = c->zeros<unsigned long long>(1);
+    c->d_tcnt = c->zeros<unsigned long long>(6);
     c->d_diag = c->zeros<long long>(kBuckets * 5);
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
     c->d_diag_accept = c->zeros<unsigned long long>(kBuckets);
@@ -888,6 +926,41 @@ int pxg_render_pass(pxg_ctx* c) { return pxg_render_passes(c, 1); }
 int pxg_render_pass_traced(pxg_ctx* c) {
   if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
   return guarded(c, [&]() { render_passes_impl(c, 1, true); });
+}
+
+int pxg_measure_traversal(pxg_ctx* c, int npass, double* out) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  return guarded(c, [&]() {
+    CK(cudaMemset(c->d_tcnt, 0, 6 * sizeof(unsigned long long)));
+    c->tl.clear();
+    c->ev_used = 0;
+    c->measure = true;
+    try {
+      render_passes_impl(c, npass, false);
+    } catch (...) {
+      c->measure = false;
+      throw;
+    }
+    c->measure = false;
+    CK(cudaDeviceSynchronize());
+    double ms[2] = {0.0, 0.0};
+    long long nl[2] = {0, 0};
+    for (const auto& t : c->tl) {
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, t.a, t.b));
+      ms[t.kind] += e;
+      nl[t.kind] += 1;
+    }
+    unsigned long long h[6];
+    CK(cudaMemcpy(h, c->d_tcnt, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 2; ++k) {
+      out[5 * k + 0] = ms[k];
+      out[5 * k + 1] = static_cast<double>(nl[k]);
+      out[5 * k + 2] = static_cast<double>(h[3 * k + 0]);
+      out[5 * k + 3] = static_cast<double>(h[3 * k + 1]);
+      out[5 * k + 4] = static_cast<double>(h[3 * k + 2]);
+    }
+  });
 }
 
 int pxg_set_pass_limit(pxg_ctx* c, int limit) {

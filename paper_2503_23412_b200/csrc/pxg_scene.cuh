@@ -129,14 +129,18 @@ __device__ __forceinline__ RayF make_rayf(const V3& o, const V3& d) {
   r.oy = __double2float_rn(o.y);
   r.oz = __double2float_rn(o.z);
   float dx = __double2float_rn(d.x), dy = __double2float_rn(d.y), dz = __double2float_rn(d.z);
+  // a zero component becomes +-1e-30: no 0 * inf = NaN when the origin lies exactly on a
+  // slab plane, and the slab is still effectively unbounded along that axis
+  if (fabsf(dx) < 1e-30f) dx = copysignf(1e-30f, dx);
+  if (fabsf(dy) < 1e-30f) dy = copysignf(1e-30f, dy);
+  if (fabsf(dz) < 1e-30f) dz = copysignf(1e-30f, dz);
   r.ix = 1.0f / dx;
   r.iy = 1.0f / dy;
   r.iz = 1.0f / dz;
   return r;
 }
 
-// Slab test in fp32; NaN from 0*inf on a padded box cannot occur because the ray origin
-// is never exactly on a padded plane that it is parallel to (fmin/fmax ignore NaN anyway).
+// Slab test in fp32 (boxes padded outward on the host, directions never exactly zero).
 __device__ __forceinline__ bool box_f(const float* lo, const float* hi, const RayF& r, float tmax,
                                       float& tnear) {
   float tx0 = (lo[0] - r.ox) * r.ix, tx1 = (hi[0] - r.ox) * r.ix;
@@ -154,8 +158,15 @@ __device__ __forceinline__ float tbound_f(double t) {
   return __double2float_ru(t) * 1.0000005f + 1e-30f;
 }
 
+// Traversal work counters (instrumented variant only): node visits and primitive tests.
+struct TravCount {
+  unsigned long long nodes, prims;
+};
+
 // Closest hit: returns the original primitive id or -1; t_best in/out (fp64).
-__device__ __noinline__ int trace_closest(const SceneView& S, const V3& o, const V3& d, double& t_best) {
+template <bool kCount = false>
+__device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, const V3& d, double& t_best,
+                                            TravCount* cnt = nullptr) {
   const RayF rf = make_rayf(o, d);
   int best = -1;
   int stack[kStack];
@@ -168,6 +179,7 @@ __device__ __noinline__ int trace_closest(const SceneView& S, const V3& o, const
     const float4 n1 = __ldg(nodes + 4 * node + 1);
     const float4 n2 = __ldg(nodes + 4 * node + 2);
     const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+    if (kCount) cnt->nodes += 1;
     const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
     const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
     const float tb = tbound_f(t_best);
@@ -185,6 +197,7 @@ __device__ __noinline__ int trace_closest(const SceneView& S, const V3& o, const
       if (c < 0) {
         const int code = ~c;
         const int first = code >> 4, count = code & 15;
+        if (kCount) cnt->prims += count;
         for (int i = 0; i < count; ++i) {
           int id;
           double t = rec_hit(S.recs + first + i, o, d, t_best, id);
@@ -219,8 +232,14 @@ __device__ __noinline__ int trace_closest(const SceneView& S, const V3& o, const
   return best;
 }
 
+__device__ __forceinline__ int trace_closest(const SceneView& S, const V3& o, const V3& d, double& t_best) {
+  return trace_closest_t<false>(S, o, d, t_best);
+}
+
 // Any hit with t in [kRayEps, t_max] (the boolean of Scene::occluded, scene.cpp:170-177).
-__device__ __noinline__ bool trace_any(const SceneView& S, const V3& o, const V3& d, double t_max) {
+template <bool kCount = false>
+__device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const V3& d, double t_max,
+                                         TravCount* cnt = nullptr) {
   const RayF rf = make_rayf(o, d);
   int stack[kStack];
   int sp = 0;
@@ -232,6 +251,7 @@ __device__ __noinline__ bool trace_any(const SceneView& S, const V3& o, const V3
     const float4 n1 = __ldg(nodes + 4 * node + 1);
     const float4 n2 = __ldg(nodes + 4 * node + 2);
     const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+    if (kCount) cnt->nodes += 1;
     const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
     const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
     float tn0, tn1;
@@ -247,6 +267,7 @@ __device__ __noinline__ bool trace_any(const SceneView& S, const V3& o, const V3
       const int first = code >> 4, count = code & 15;
       for (int i = 0; i < count; ++i) {
         int id;
+        if (kCount) cnt->prims += 1;
         double t = rec_hit(S.recs + first + i, o, d, t_max, id);
         if (t > 0.0) return true;
       }
@@ -269,6 +290,10 @@ __device__ __noinline__ bool trace_any(const SceneView& S, const V3& o, const V3
     node = next;
   }
   return false;
+}
+
+__device__ __forceinline__ bool trace_any(const SceneView& S, const V3& o, const V3& d, double t_max) {
+  return trace_any_t<false>(S, o, d, t_max);
 }
 
 // primitive_normal (scene.cpp:65-72)

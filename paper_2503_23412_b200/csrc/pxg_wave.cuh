@@ -195,6 +195,32 @@ __global__ void __launch_bounds__(128) k_anyhit(SceneView S, RayQueue Q) {
   Q.hit_prim[j] = trace_any(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), r1.z) ? 1 : 0;
 }
 
+// Instrumented copies of the traversal kernels for the roofline measurement: the same
+// traversal code on the same queue, counting node visits (64 B each) and primitive tests
+// (80 B each). Launched after the timed launch; results are identical and discarded.
+__global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, unsigned long long* acc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *Q.count) return;
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  double t_best = r1.z;
+  TravCount c{0, 0};
+  trace_closest_t<true>(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), t_best, &c);
+  atomicAdd(acc + 0, 1ull);
+  atomicAdd(acc + 1, c.nodes);
+  atomicAdd(acc + 2, c.prims);
+}
+
+__global__ void __launch_bounds__(128) k_anyhit_count(SceneView S, RayQueue Q, unsigned long long* acc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *Q.count) return;
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  TravCount c{0, 0};
+  trace_any_t<true>(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), r1.z, &c);
+  atomicAdd(acc + 0, 1ull);
+  atomicAdd(acc + 1, c.nodes);
+  atomicAdd(acc + 2, c.prims);
+}
+
 // ---------------------------------------------------------------- standard connections
 // Slot layout per pixel, in the reference's accumulation order (proxy.cpp:627-641):
 // for t = 2..n_eye: s = 0 (eye-hit emission), then s = 1..min(n_light, max_depth+1-t).

@@ -173,6 +173,14 @@ class ProxyRenderer:
         """No look-ahead Stage 1 for passes >= limit (the render's spp)."""
         self._check(self._L.pxg_set_pass_limit(self._ctx, int(limit)))
 
+    def measure_traversal(self, n: int = 1) -> dict:
+        """Render n passes with every traversal launch timed by CUDA events and its work
+        counted by an instrumented copy on the same rays (roofline numerator)."""
+        out = np.zeros(10)
+        self._check(self._L.pxg_measure_traversal(self._ctx, n, _dp(out)))
+        keys = ["ms", "launches", "rays", "nodes", "prims"]
+        return {"closest": dict(zip(keys, out[:5].tolist())), "anyhit": dict(zip(keys, out[5:].tolist()))}
+
     def render_pass_traced(self):
         """One pass that also records the sub-path primitive ids (dump_prims)."""
         self._check(self._L.pxg_render_pass_traced(self._ctx))
