@@ -268,7 +268,6 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   k_conn_enum<<<blocks(n, T), T, 0, st>>>(c->d_neye, c->d_nlight, n, D, C);
   CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
   CK(cudaMemsetAsync(C.n_live, 0, sizeof(int), st));
-  k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
   const long long slots = static_cast<long long>(n) * c->max_slots;
   k_conn_eval<<<blocks(slots, T), T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
   if (c->measure) {
@@ -282,6 +281,7 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
     k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
   }
   k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
+  k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
   k_conn_mis<<<blocks(slots, T), T, 0, st>>>(c->S, c->M,
                                              StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
                                              use_stats ? 1 : 0, c->d_eye, c->d_light, n, C, c->pcache);

@@ -207,16 +207,22 @@ __device__ __forceinline__ double geometry_term(const SceneView& S, const PV& a,
 }
 
 // A full path light[0..s-1] + eye[t-1..0] (transport.hpp:37-44) read through strided views.
+// Strides are in bytes so the vertices can also live in shared memory at a padded stride.
 struct FullPath {
-  const PV* L;
+  const char* L;
   size_t ls;
-  const PV* E;
+  const char* E;
   size_t es;
   int s, t;
   __device__ __forceinline__ const PV& vtx(int i) const {
-    return i < s ? L[i * ls] : E[(s + t - 1 - i) * es];
+    return i < s ? *reinterpret_cast<const PV*>(L + i * ls) : *reinterpret_cast<const PV*>(E + (s + t - 1 - i) * es);
   }
 };
+
+__device__ __forceinline__ FullPath make_fp(const PV* L, size_t ls, const PV* E, size_t es, int s, int t) {
+  return FullPath{reinterpret_cast<const char*>(L), ls * sizeof(PV), reinterpret_cast<const char*>(E),
+                  es * sizeof(PV), s, t};
+}
 
 // Memoised step densities of one full path (see header comment).
 struct PathTable {
@@ -321,11 +327,57 @@ __device__ __forceinline__ void table_init_cached(PathTable& T, const PathCache&
   }
 }
 
+// Same as table_init_cached with the per-sub-path steps held in (shared-memory) arrays of
+// one pixel: LF/LR indexed by light vertex, EF/ER by eye vertex.
+__device__ __forceinline__ void table_init_local(PathTable& T, const double* LF, const double* LR, const double* EF,
+                                                 const double* ER, double ld, int ld_ok, int s, int t) {
+  T.fmask = 0u;
+  T.rmask = 0u;
+  T.ld_done = false;
+  T.ld_ok = false;
+  const int n_v = s + t;
+  for (int k = 2; k <= s - 1; ++k) {
+    T.F[k] = LF[k];
+    T.fmask |= 1u << k;
+  }
+  for (int k = s + 2; k <= n_v - 1; ++k) {
+    T.F[k] = EF[n_v - 1 - k];
+    T.fmask |= 1u << k;
+  }
+  for (int j = 0; j <= s - 3; ++j) {
+    T.R[j] = LR[j];
+    T.rmask |= 1u << j;
+  }
+  for (int j = s; j <= n_v - 3; ++j) {
+    T.R[j] = ER[n_v - 1 - j];
+    T.rmask |= 1u << j;
+  }
+  if (s >= 2) {
+    T.ld_done = true;
+    T.ld_ok = ld_ok != 0;
+    T.ld_area = ld;
+  }
+}
+
 __device__ __forceinline__ void table_init(PathTable& T) {
   T.fmask = 0u;
   T.rmask = 0u;
   T.ld_done = false;
   T.ld_ok = false;
+}
+
+// Evaluates the junction steps of connection (s, t) eagerly, at one point of the code for
+// every lane: F(s), F(s+1), R(s-2), R(s-1) and the light-direction factor when it involves
+// an eye vertex (s <= 1). Together with the cached sub-path steps the table is then
+// complete, so the strategy loops below never branch into a pdf evaluation (the lazy
+// version ran at 2/32 active lanes). Same function, same inputs: bit-identical values.
+__device__ __forceinline__ void table_fill_junctions(const SceneView& S, const FullPath& fp, PathTable& T) {
+  const int s = fp.s, n_v = fp.s + fp.t;
+  if (s >= 2 && s <= n_v - 1) tabF(S, fp, T, s);
+  if (s >= 1 && s + 1 <= n_v - 1) tabF(S, fp, T, s + 1);
+  if (s >= 2 && s - 2 <= n_v - 3) tabR(S, fp, T, s - 2);
+  if (s >= 1 && s - 1 <= n_v - 3) tabR(S, fp, T, s - 1);
+  if (n_v >= 2) tabLD(fp, T);
 }
 
 // strategy_pdf (transport.cpp:206-253) on the memoised factors.
@@ -451,6 +503,51 @@ __device__ __forceinline__ double reciprocal_mis_weight_t(const SceneView& S, co
   return num / denom;
 }
 
+// reciprocal_mis_weight on a COMPLETE table (cached sub-path steps + table_fill_junctions),
+// written without early exits so a warp's lanes (different (s, t), different n_v) stay
+// converged: every strategy density is the same left-to-right product as strategy_pdf
+// (transport.cpp:218-253) and is replaced by 0 when a flag check fails or a factor is
+// <= 0, exactly where strategy_pdf returns 0. Sum order and the final division are the
+// reference's (proxy.cpp:536-545), so the weight is bit-identical.
+__device__ __forceinline__ double mis_weight_full(const SceneView& S, const Mapper& M, const StatsView& st,
+                                                  const FullPath& fp, PathTable& T, int cur_s, bool use_stats) {
+  const double p_proxy = use_stats ? proxy_weight_density(S, M, st, fp, T) : 0.0;
+  const int n_v = fp.s + fp.t;
+  unsigned diffuse = 0u;
+  for (int i = 0; i < n_v; ++i) diffuse |= (fp.vtx(i).flag == kDiffuse ? 1u : 0u) << i;
+  const bool emit0 = fp.vtx(0).emitter >= 0;
+  const double inv_area = 1.0 / S.total_emitter_area;
+  const double ld = T.ld_ok ? T.ld_area : 0.0;
+  double num = 0.0, denom = 0.0;
+  for (int sp = 0; sp <= n_v - 2; ++sp) {
+    bool ok = true;
+    if (sp >= 1) ok = ((diffuse >> sp) & 1u) && (sp < 2 || ((diffuse >> (sp - 1)) & 1u)) && emit0;
+    double p = 1.0;
+    if (sp >= 1) p *= inv_area;
+    if (sp >= 2) {
+      ok = ok && T.ld_ok;
+      p *= ld;
+    }
+    for (int i = 2; i < sp; ++i) {
+      const double v = T.F[i];
+      ok = ok && v > 0.0;
+      p *= v;
+    }
+    for (int j = n_v - 3; j >= sp; --j) {
+      const double v = T.R[j];
+      ok = ok && v > 0.0;
+      p *= v;
+    }
+    p = ok ? p : 0.0;
+    if (sp == cur_s) num = p;
+    denom += p;
+  }
+  if (cur_s < 0) num = p_proxy;
+  if (num <= 0.0) return 0.0;
+  denom += p_proxy;
+  return num / denom;
+}
+
 __device__ __forceinline__ double reciprocal_mis_weight(const SceneView& S, const Mapper& M, const StatsView& st,
                                                         const FullPath& fp, int cur_s, bool use_stats) {
   PathTable T;
@@ -461,8 +558,8 @@ __device__ __forceinline__ double reciprocal_mis_weight(const SceneView& S, cons
 // connection_contribution (transport.cpp:187-196) incl. junction_kernels (:70-88).
 __device__ __forceinline__ V3 connection_contribution(const SceneView& S, const FullPath& fp) {
   if (fp.s < 1 || fp.t < 2) return v3(0.0);
-  const PV& y = fp.L[(fp.s - 1) * fp.ls];
-  const PV& z = fp.E[(fp.t - 1) * fp.es];
+  const PV& y = fp.vtx(fp.s - 1);
+  const PV& z = fp.vtx(fp.s);
   if (z.flag != kDiffuse) return v3(0.0);
   V3 d = z.p - y.p;
   double len = length(d);
@@ -492,12 +589,12 @@ __device__ __forceinline__ V3 weighted_bdpt_value(const SceneView& S, const Mapp
     if (z.emitter >= 0) {
       V3 le = z.thr * emitted(S, z.emitter, z.n, z.wi);
       if (!near_zero(le)) {
-        FullPath fp{light, ls, eye, es, 0, t};
+        FullPath fp = make_fp(light, ls, eye, es, 0, t);
         radiance += le * reciprocal_mis_weight(S, M, st, fp, 0, use_stats);
       }
     }
     for (int s = 1; s <= n_light && s + t <= S.max_depth + 1; ++s) {
-      FullPath fp{light, ls, eye, es, s, t};
+      FullPath fp = make_fp(light, ls, eye, es, s, t);
       V3 c = connection_contribution(S, fp);
       if (near_zero(c)) continue;
       radiance += c * reciprocal_mis_weight(S, M, st, fp, s, use_stats);

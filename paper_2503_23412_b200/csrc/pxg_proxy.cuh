@@ -512,7 +512,7 @@ __device__ __forceinline__ V3 proxy_connect(const SceneView& S, const Mapper& M,
   V3 fz = eval_bsdf(S.materials[z.mat], z.n, z.wi, normalize(lv[s - 1].p - z.p));
   if (near_zero(fz)) return v3(0.0);
   value = value * fz * z.thr;
-  FullPath fp{lv, 1, eye, es, s, t};
+  FullPath fp = make_fp(lv, 1, eye, es, s, t);
   const double w = reciprocal_mis_weight(S, M, st, fp, -1, true);
   if (!(w > 0.0)) return v3(0.0);
   return value * (h.inverse_p * w / (h.prefix_pdf * density));

@@ -372,6 +372,121 @@ __global__ void k_path_factors(SceneView S, const PV* eye, const int* n_eye, con
   C.ld[i] = area;
 }
 
+// Per pixel, one warp: stage the pixel's eye and light vertices in shared memory, compute
+// the per-sub-path step caches with the lanes, weight every contributing slot
+// (reciprocal_mis_weight, proxy.cpp:533-546) with the lanes, then lane 0 accumulates the
+// slots in the reference's (t, s) order (proxy.cpp:627-641) into bdpt[i].
+constexpr int kConnWarps = 4;
+constexpr int kMaxEye = 17;    // max_depth + 1
+constexpr int kMaxSlots = 136; // sum over t of (1 + min(n_light, max_depth + 1 - t)) at max_depth 16
+
+// Vertices are stored at a 144-byte stride (not 128): with 128 B every lane reading the
+// same field of a different vertex hits the same shared-memory bank.
+constexpr int kSmemVtx = 144;
+struct ConnSmem {
+  alignas(16) char eye[kMaxEye * kSmemVtx];
+  alignas(16) char light[kMaxLight * kSmemVtx];
+  double LF[kMaxPath], LR[kMaxPath], EF[kMaxPath], ER[kMaxPath];
+  double val[kMaxSlots * 3];
+  double ld;
+  int ld_ok;
+};
+
+__global__ void __launch_bounds__(32 * kConnWarps) k_conn_pixel(SceneView S, Mapper M, StatsView st, int use_stats,
+                                                                const PV* eye, const int* n_eye, const PV* light,
+                                                                const int* n_light, int n, ConnBuf C,
+                                                                double* bdpt) {
+  __shared__ ConnSmem sm_all[kConnWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * kConnWarps + wid;
+  if (i >= n) return;
+  ConnSmem& sm = sm_all[wid];
+  const size_t stv = static_cast<size_t>(n);
+  const int ne = n_eye[i], nl = n_light[i];
+  // stage vertices (16 B per lane per step, coalesced within a vertex)
+  for (int k = 0; k < ne; ++k) {
+    const double2* src = reinterpret_cast<const double2*>(eye + k * stv + i);
+    double2* dst = reinterpret_cast<double2*>(sm.eye + k * kSmemVtx);
+    if (lane < 8) dst[lane] = src[lane];
+  }
+  for (int k = 0; k < nl; ++k) {
+    const double2* src = reinterpret_cast<const double2*>(light + k * stv + i);
+    double2* dst = reinterpret_cast<double2*>(sm.light + k * kSmemVtx);
+    if (lane < 8) dst[lane] = src[lane];
+  }
+  __syncwarp();
+  // per-sub-path step densities (same values as PathCache / k_path_factors)
+  const int nLF = nl > 2 ? nl - 2 : 0, nLR = nl > 2 ? nl - 2 : 0;
+  const int nEF = ne > 2 ? ne - 2 : 0, nER = ne > 2 ? ne - 2 : 0;
+  auto EV = [&](int k) -> const PV& { return *reinterpret_cast<const PV*>(sm.eye + k * kSmemVtx); };
+  auto LV = [&](int k) -> const PV& { return *reinterpret_cast<const PV*>(sm.light + k * kSmemVtx); };
+  for (int q = lane; q < nLF + nLR + nEF + nER; q += 32) {
+    if (q < nLF) {
+      const int k = q + 2;
+      sm.LF[k] = bsdf_step_v(S, LV(k - 1), LV(k - 2), LV(k));
+    } else if (q < nLF + nLR) {
+      const int j = q - nLF;
+      sm.LR[j] = bsdf_step_v(S, LV(j + 1), LV(j + 2), LV(j));
+    } else if (q < nLF + nLR + nEF) {
+      const int m = q - nLF - nLR;
+      sm.EF[m] = bsdf_step_v(S, EV(m + 1), EV(m + 2), EV(m));
+    } else {
+      const int m = q - nLF - nLR - nEF + 2;
+      sm.ER[m] = bsdf_step_v(S, EV(m - 1), EV(m - 2), EV(m));
+    }
+  }
+  if (lane == 0) {
+    int ok = 0;
+    double area = 0.0;
+    if (nl >= 2) {
+      const PV& y0 = LV(0);
+      const PV& y1 = LV(1);
+      V3 d = y1.p - y0.p;
+      double len = length(d);
+      if (len > 0.0) {
+        double pdf_w = light_direction_pdf(y0.n, d / len);
+        if (pdf_w > 0.0) {
+          ok = 1;
+          area = to_area_density(pdf_w, y0.p, y1.p, y1.n);
+        }
+      }
+    }
+    sm.ld = area;
+    sm.ld_ok = ok;
+  }
+  __syncwarp();
+  const int a = C.offset[i], b = C.offset[i + 1];
+  for (int g = a + lane; g < b; g += 32) {
+    const int state = C.state[g];
+    double* out = &sm.val[3 * (g - a)];
+    if (state != 1) {
+      out[0] = out[1] = out[2] = 0.0;
+      continue;
+    }
+    const int ts = C.desc[g].y;
+    const int t = ts >> 8, s = ts & 255;
+    FullPath fp{sm.light, kSmemVtx, sm.eye, kSmemVtx, s, t};
+    PathTable T;
+    table_init_local(T, sm.LF, sm.LR, sm.EF, sm.ER, sm.ld, sm.ld_ok, s, t);
+    const double w = reciprocal_mis_weight_t(S, M, st, fp, T, s, use_stats != 0);
+    out[0] = C.value[3 * g] * w;
+    out[1] = C.value[3 * g + 1] * w;
+    out[2] = C.value[3 * g + 2] * w;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    V3 r = v3(0.0);
+    for (int g = a; g < b; ++g) {
+      if (C.state[g] != 1) continue;
+      const double* v = &sm.val[3 * (g - a)];
+      r += v3(v[0], v[1], v[2]);
+    }
+    bdpt[3 * i] = r.x;
+    bdpt[3 * i + 1] = r.y;
+    bdpt[3 * i + 2] = r.z;
+  }
+}
+
 // reciprocal_mis_weight of every live slot; value <- value * w.
 __global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
                            int n, ConnBuf C, PathCache PC) {
@@ -381,10 +496,11 @@ __global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, c
   const int2 dsc = C.desc[g];
   const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
   const size_t st_ = static_cast<size_t>(n);
-  FullPath fp{light + i, st_, eye + i, st_, s, t};
+  FullPath fp = make_fp(light + i, st_, eye + i, st_, s, t);
   PathTable T;
   table_init_cached(T, PC, i, s, t);
-  const double w = reciprocal_mis_weight_t(S, M, st, fp, T, s, use_stats != 0);
+  table_fill_junctions(S, fp, T);
+  const double w = mis_weight_full(S, M, st, fp, T, s, use_stats != 0);
   C.value[3 * g] = C.value[3 * g] * w;
   C.value[3 * g + 1] = C.value[3 * g + 1] * w;
   C.value[3 * g + 2] = C.value[3 * g + 2] * w;
