@@ -133,6 +133,9 @@ struct pxg_ctx {
   cudaEvent_t ev_call[3];
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
+  ProxWave pw{};
+  int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
+  int* d_trav_next = nullptr;  // [8] ray fetch counters (per stream use)
   // traversal roofline measurement (pxg_measure_traversal)
   bool measure = false;
   unsigned long long* d_tcnt = nullptr;  // closest {rays, nodes, prims}, any-hit {rays, nodes, prims}
@@ -241,15 +244,17 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
     k_light_start<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in);
   ++c->launches;
   for (int b = 0; b + 1 < P.max_vertices; ++b) {
+    int* fetch = c->d_trav_next + (st == c->stream1 ? 1 : 0);
+    CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
     if (c->measure) {
       pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 0};
       CK(cudaEventRecord(t.a, st));
-      k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
       CK(cudaEventRecord(t.b, st));
       k_closest_count<<<blocks(P.n, T), T, 0, st>>>(c->S, in, c->d_tcnt);
       c->tl.push_back(t);
     } else {
-      k_closest<<<blocks(P.n, T), T, 0, st>>>(c->S, in);
+      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
     }
     CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
     k_shade<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, out);
@@ -270,15 +275,17 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   CK(cudaMemsetAsync(C.n_live, 0, sizeof(int), st));
   const long long slots = static_cast<long long>(n) * c->max_slots;
   k_conn_eval<<<blocks(slots, T), T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
+  int* fetch = c->d_trav_next + 2;
+  CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
   if (c->measure) {
     pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 1};
     CK(cudaEventRecord(t.a, st));
-    k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+    k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
     CK(cudaEventRecord(t.b, st));
     k_anyhit_count<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS, c->d_tcnt + 3);
     c->tl.push_back(t);
   } else {
-    k_anyhit<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS);
+    k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
   }
   k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
   k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
@@ -500,9 +507,31 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
   P.seed = c->seed;
   P.record_prims = record_prims ? 1 : 0;
   if (c->proxy_on) {
-    k_proxy<<<blocks(c->n, T), T, 0, st>>>(P, pass, c->n_px_total, sl.inc, sl.prefix, sl.label_start, sl.label_list,
-                                           c->d_gamma, sl.ps, c->d_prox, c->d_scratch);
-    ++c->launches;
+    ProxCtx C{c->S, c->M, StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt}, c->d_eye, c->d_neye,
+              c->n, c->row0, c->width, c->max_depth, c->seed, sl.inc, sl.prefix, sl.label_start, sl.label_list,
+              c->d_gamma, sl.ps};
+    ProxWave& W = c->pw;
+    RayQueue in = c->qA, out = c->qB;
+    CK(cudaMemsetAsync(in.count, 0, sizeof(int), st));
+    k_pxw_select<<<blocks(c->n, T), T, 0, st>>>(C, W, pass, c->n_px_total, c->d_prox, in);
+    for (int step = 0; step < 4; ++step) {
+      int* fetch = c->d_trav_next + 3;
+      CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
+      CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
+      k_pxw_retrace<<<blocks(c->n, T), T, 0, st>>>(C, W, pass, c->n_px_total, in, out);
+      std::swap(in, out);
+    }
+    CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
+    k_pxw_value<<<blocks(c->n, T), T, 0, st>>>(C, W, c->qS);
+    {
+      int* fetch = c->d_trav_next + 4;
+      CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+      k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
+    }
+    k_pxw_occlusion<<<blocks(static_cast<long long>(c->n) * kMaxLight, T), T, 0, st>>>(W, c->qS);
+    k_pxw_mis<<<blocks(c->n, T), T, 0, st>>>(C, W, c->d_prox);
+    c->launches += 13;
   }
   CK(cudaEventRecord(c->ev[6], st));
   hp.mark("proxy");
@@ -753,6 +782,16 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_acc = c->zeros<double>(3 * n);
     c->d_prox = c->zeros<ProxRec>(n);
     c->d_scratch = c->alloc<PV>(n * kMaxLight);
+    c->pw.entry = c->zeros<int>(n);
+    c->pw.tp = c->zeros<int>(n);
+    c->pw.ctr = c->zeros<unsigned>(n);
+    c->pw.step = c->zeros<int>(n);
+    c->pw.state = c->zeros<int>(n);
+    c->pw.density = c->zeros<double>(n);
+    c->pw.pdf = c->zeros<double>(n);
+    c->pw.value = c->zeros<double>(3 * n);
+    c->pw.occl = c->zeros<int>(n);
+    c->pw.lv = c->d_scratch;
     c->d_ebeta = c->zeros<double>(3 * n);
     c->d_epdf = c->zeros<double>(n);
     c->d_lbeta = c->zeros<double>(3 * n);
@@ -894,6 +933,13 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_err = c->zeros<int>(1);
     c->d_kept_total = c->zeros<unsigned long long>(1);
     c->d_tcnt = c->zeros<unsigned long long>(6);
+    c->d_trav_next = c->zeros<int>(8);
+    {
+      int sms = 0, per_sm = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false>, 128, 0));
+      c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
+    }
     c->d_diag = c->zeros<long long>(kBuckets * 5);
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
     c->d_diag_accept = c->zeros<unsigned long long>(kBuckets);

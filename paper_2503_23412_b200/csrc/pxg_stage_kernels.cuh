@@ -35,7 +35,7 @@
 
 #include "pxg.h"
 #include "pxg_host.h"
-#include "pxg_wave.cuh"
+#include "pxg_proxy_wave.cuh"
 
 using namespace pxg;
 
@@ -45,21 +45,9 @@ constexpr int kBuckets = 4000;
 constexpr int kS = 100, kT = 32;
 thread_local std::string g_global_err;
 
-struct ProxRec {
-  double c[3];
-  double u_gate;
-  double q_sel;
-  int t_label, chosen, key, flags;  // flags bit0 tp>=2, bit1 attempted, bit2 z_norm>0
-};
 
 
 
-struct PassState {  // device-resident per-pass scalars
-  double kappa;
-  int n_kept;
-  int err;
-  long long pool_kept_total;
-};
 
 #define CK(x)                                                                           \
   do {                                                                                  \
@@ -548,82 +536,6 @@ __global__ void k_record_prims(const PV* eye, const int* n_eye, const PV* light,
   for (int k = 0; k < max_depth - 1; ++k)
     light_prims[static_cast<size_t>(i) * (max_depth - 1) + k] =
         k < nl ? light[static_cast<size_t>(k) * n + i].prim : -2;
-}
-
-__global__ void k_proxy(Stage2 P, int pass, int n_px_total, const IncHdr* inc, const PV* prefix,
-                        const int* label_start, const int* label_list, const double* gamma_rows,
-                        const PassState* ps, ProxRec* out, PV* scratch) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  ProxRec o;
-  o.c[0] = o.c[1] = o.c[2] = 0.0;
-  o.u_gate = 0.0;
-  o.q_sel = 0.0;
-  o.t_label = o.chosen = o.key = -1;
-  o.flags = 0;
-  if (ps->n_kept <= 0) {
-    out[i] = o;
-    return;
-  }
-  const PV* eye = P.eye + i;
-  const size_t es = static_cast<size_t>(P.n);
-  const int ne = P.n_eye[i];
-  int tp = 0;
-  for (int k = 1; k < ne; ++k) {
-    const int f = eye[k * es].flag;
-    if (f == kDiffuse) {
-      tp = k + 1;
-      break;
-    }
-    if (f != kSpecular) break;
-  }
-  if (tp < 2) {
-    out[i] = o;
-    return;
-  }
-  o.flags |= 1;
-  const int idx = P.row0 * P.width + i;
-  Rng prox = make_rng(P.seed, PXG_KIND_REF, 0,
-                      (uint64_t(2) << 32) + static_cast<uint64_t>(pass) * static_cast<uint64_t>(n_px_total) + idx);
-  o.u_gate = prox.next_double();
-  const PV& z = eye[(tp - 1) * es];
-  const int t_label = classify_eye(P.M, z.p, -z.wi);
-  const double* row = gamma_rows + t_label * kS;
-  double z_norm = 0.0;
-  for (int sl = 0; sl < kS; ++sl)
-    if (label_start[sl + 1] > label_start[sl]) z_norm += row[sl];
-  if (!(z_norm > 0.0)) {
-    out[i] = o;
-    return;
-  }
-  o.flags |= 4;
-  const double uu = prox.next_double() * z_norm;
-  int chosen = -1;
-  double cdf = 0.0;
-  for (int sl = 0; sl < kS; ++sl) {
-    if (label_start[sl + 1] == label_start[sl]) continue;
-    chosen = sl;
-    cdf += row[sl];
-    if (uu < cdf) break;
-  }
-  const double row_p = row[chosen] / z_norm;
-  const int bsize = label_start[chosen + 1] - label_start[chosen];
-  const int e = label_list[label_start[chosen] + static_cast<int>(prox.next_below(static_cast<uint32_t>(bsize)))];
-  const IncHdr& h = inc[e];
-  const int s_rep = h.n_prefix + h.u + 1;
-  o.t_label = t_label;
-  o.chosen = chosen;
-  o.key = h.key;
-  o.q_sel = row_p / static_cast<double>(bsize);
-  if (s_rep + tp <= P.max_depth + 1) {
-    o.flags |= 2;
-    V3 c = proxy_connect(P.S, P.M, P.st, eye, es, tp, h, prefix + static_cast<size_t>(e) * kMaxLight, prox,
-                         scratch + static_cast<size_t>(i) * kMaxLight);
-    o.c[0] = c.x;
-    o.c[1] = c.y;
-    o.c[2] = c.z;
-  }
-  out[i] = o;
 }
 
 // Per 10x10 cell in the reference's scan order (proxy.cpp:761-817).

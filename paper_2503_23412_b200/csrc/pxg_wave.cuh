@@ -195,6 +195,174 @@ __global__ void __launch_bounds__(128) k_anyhit(SceneView S, RayQueue Q) {
   Q.hit_prim[j] = trace_any(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), r1.z) ? 1 : 0;
 }
 
+// ---------------------------------------------------------------- persistent traversal
+// One BVH node step per loop iteration; a lane whose ray finishes takes the next ray of the
+// queue (warp-aggregated atomic fetch) instead of idling until the warp's longest ray is
+// done (ncu on the one-ray-per-thread kernel: 4.8-7.8 of 32 lanes active). The node step is
+// exactly the loop body of trace_closest_t / trace_any_t, so results are identical.
+struct TravState {
+  V3 o, d;
+  RayF rf;
+  double t_best;
+  int best, node, sp;
+  int stack[kStack];
+};
+
+__device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int j) {
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  ts.o = v3(r0.x, r0.y, r0.z);
+  ts.d = v3(r0.w, r1.x, r1.y);
+  ts.rf = make_rayf(ts.o, ts.d);
+  ts.t_best = r1.z;
+  ts.best = -1;
+  ts.node = 0;
+  ts.sp = 0;
+}
+
+// Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
+__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts) {
+  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
+  const int node = ts.node;
+  const float4 n0 = __ldg(nodes + 4 * node + 0);
+  const float4 n1 = __ldg(nodes + 4 * node + 1);
+  const float4 n2 = __ldg(nodes + 4 * node + 2);
+  const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+  const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
+  const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
+  const float tb = tbound_f(ts.t_best);
+  float tn0, tn1;
+  const bool h0 = box_f(lo0, hi0, ts.rf, tb, tn0);
+  const bool h1 = box_f(lo1, hi1, ts.rf, tb, tn1);
+  const int c0 = n3.x, c1 = n3.y;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool h = k == 0 ? h0 : h1;
+    const int c = k == 0 ? c0 : c1;
+    if (!h || c >= 0) continue;
+    const int code = ~c;
+    const int first = code >> 4, count = code & 15;
+    for (int i = 0; i < count; ++i) {
+      int id;
+      const double t = rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id);
+      if (t > 0.0 && (t < ts.t_best || id > ts.best)) {
+        ts.t_best = t;
+        ts.best = id;
+      }
+    }
+  }
+  const float tbn = tbound_f(ts.t_best);
+  const bool in0 = h0 && c0 >= 0 && tn0 <= tbn;
+  const bool in1 = h1 && c1 >= 0 && tn1 <= tbn;
+  int next;
+  if (in0 && in1) {
+    const bool first0 = tn0 <= tn1;
+    next = first0 ? c0 : c1;
+    if (ts.sp < kStack) ts.stack[ts.sp++] = first0 ? c1 : c0;
+  } else if (in0) {
+    next = c0;
+  } else if (in1) {
+    next = c1;
+  } else {
+    if (ts.sp == 0) return true;
+    next = ts.stack[--ts.sp];
+  }
+  ts.node = next;
+  return false;
+}
+
+// Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
+__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts) {
+  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
+  const int node = ts.node;
+  const float4 n0 = __ldg(nodes + 4 * node + 0);
+  const float4 n1 = __ldg(nodes + 4 * node + 1);
+  const float4 n2 = __ldg(nodes + 4 * node + 2);
+  const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
+  const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
+  const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
+  const float tb = tbound_f(ts.t_best);
+  float tn0, tn1;
+  const bool h0 = box_f(lo0, hi0, ts.rf, tb, tn0);
+  const bool h1 = box_f(lo1, hi1, ts.rf, tb, tn1);
+  const int c0 = n3.x, c1 = n3.y;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool h = k == 0 ? h0 : h1;
+    const int c = k == 0 ? c0 : c1;
+    if (!h || c >= 0) continue;
+    const int code = ~c;
+    const int first = code >> 4, count = code & 15;
+    for (int i = 0; i < count; ++i) {
+      int id;
+      if (rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
+    }
+  }
+  const bool in0 = h0 && c0 >= 0;
+  const bool in1 = h1 && c1 >= 0;
+  int next;
+  if (in0 && in1) {
+    const bool first0 = tn0 <= tn1;
+    next = first0 ? c0 : c1;
+    if (ts.sp < kStack) ts.stack[ts.sp++] = first0 ? c1 : c0;
+  } else if (in0) {
+    next = c0;
+  } else if (in1) {
+    next = c1;
+  } else {
+    if (ts.sp == 0) return 2;
+    next = ts.stack[--ts.sp];
+  }
+  ts.node = next;
+  return 0;
+}
+
+constexpr int kRefill = 4;  // refill a warp's idle lanes once at least this many are idle
+
+template <bool kAny>
+__global__ void __launch_bounds__(128) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int total = *Q.count;
+  int j = -1;
+  bool exhausted = false;
+  TravState ts;
+  for (;;) {
+    const bool idle = j < 0;
+    const unsigned m = __ballot_sync(FULL, idle);
+    if (!exhausted && m && (__popc(m) >= kRefill || m == FULL)) {
+      const int leader = __ffs(m) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(next_ray, __popc(m));
+      base = __shfl_sync(FULL, base, leader);
+      if (base + __popc(m) > total) exhausted = true;
+      if (idle) {
+        const int jj = base + __popc(m & ((1u << lane) - 1));
+        if (jj < total) {
+          j = jj;
+          trav_init(ts, Q, j);
+        }
+      }
+    }
+    if (__ballot_sync(FULL, j >= 0) == 0) {
+      if (exhausted || total == 0) break;
+      continue;
+    }
+    if (j >= 0) {
+      if (kAny) {
+        const int r = any_step(S, ts);
+        if (r) {
+          Q.hit_prim[j] = r == 1 ? 1 : 0;
+          j = -1;
+        }
+      } else if (closest_step(S, ts)) {
+        Q.hit_prim[j] = ts.best;
+        Q.hit_t[j] = ts.t_best;
+        j = -1;
+      }
+    }
+  }
+}
+
 // Instrumented copies of the traversal kernels for the roofline measurement: the same
 // traversal code on the same queue, counting node visits (64 B each) and primitive tests
 // (80 B each). Launched after the timed launch; results are identical and discarded.
