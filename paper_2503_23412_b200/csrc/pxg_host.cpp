@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <stdexcept>
@@ -108,9 +109,11 @@ struct Builder {
   }
 
   // Builds [first, first+count) and returns the child code referencing it.
+  int leaf_max = 1;  // measured best on C2 (fp64 primitive tests dominate); PXG_LEAF overrides
+
   int build(int first, int count, const Box& bounds, int depth) {
     max_depth_seen = std::max(max_depth_seen, depth);
-    if (count <= 4 || depth >= 56) {
+    if (count <= leaf_max || depth >= 56) {
       if (count <= 15) return leaf_code(first, count);
     }
     Box cb;
@@ -265,6 +268,7 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
   h.order.reserve(n);
   const double pad = 1e-5 * scale;
   Builder B{bp, h.nodes, h.order, pad};
+  if (const char* lm = std::getenv("PXG_LEAF")) B.leaf_max = std::max(1, std::min(15, std::atoi(lm)));
   Box all;
   for (auto& p : bp) all.grow(p.lo, p.hi);
   if (n <= 4) {

@@ -101,7 +101,8 @@ struct pxg_ctx {
   int* d_ract[2] = {nullptr, nullptr};
   int* d_rnact = nullptr;
   int recip_rounds = 0;
-  static constexpr int kBatchMax = 8;  // passes per Stage-1 batch
+  static constexpr int kBatchMax = 32;  // passes per Stage-1 batch (PXG_BATCH, default kBatchDefault)
+  static constexpr int kBatchDefault = 8;
   PoolSlot slot[2 * kBatchMax];        // ring: batch k uses half k & 1
   int batch = kBatchMax;               // passes per batch (<= kBatchMax)
   int next_batch = 0;                  // first pass without a launched Stage 1
@@ -910,7 +911,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     }
     {
       const char* eb = std::getenv("PXG_BATCH");
-      c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchMax));
+      c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchDefault));
     }
     const size_t NR = static_cast<size_t>(B) * R * c->batch;  // reciprocal runs of one Stage-1 batch
     c->d_run_est = c->zeros<double>(NR);
