@@ -209,20 +209,43 @@ def run_ours(args):
     sc, walks = make_scene(args.config)
     W, H = sc.camera.width, sc.camera.height
     params = ProxyParams(light_walks=walks)
-    seed = 0 + rank  # N > 1: independent replicas on disjoint Philox seeds (weak scaling)
 
     # ---- device-resident throughput: K passes after W warm-up passes (CUDA events)
+    # N > 1: sample sharding (paper_2503_23412_b200/distributed.py): every rank renders K
+    # passes of its own Philox key and the fp64 accumulators are summed with one NCCL
+    # all-reduce per pass; N = 1 is the plain single-GPU render.
+    from paper_2503_23412_b200.distributed import rank_seed
+    seed = rank_seed(0, rank)
     r = ProxyRenderer(sc, seed, params, device=local)
-    r.render_passes(max(args.warmup, 3))
+    acc = torch.zeros((H, W, 3), dtype=torch.float64, device="cuda")
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
+        r.render_passes(1)
+        if world > 1:
+            r.accum_to_device(acc.data_ptr())
+            dist.all_reduce(acc)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        r.render_passes(args.steps)
-        torch.cuda.synchronize()
+        if world == 1:
+            r.render_passes(args.steps)
+            torch.cuda.synchronize()
+        else:
+            ev0.record()
+            for _ in range(args.steps):
+                r.render_passes(1)
+                r.accum_to_device(acc.data_ptr())
+                dist.all_reduce(acc)
+            ev1.record()
+            torch.cuda.synchronize()
     stage_ms, counts = r.timing()
-    dev_ms = float(stage_ms[6])  # first pass start -> last pass end on the device, host gaps included
+    if world == 1:
+        dev_ms = float(stage_ms[6])  # first pass start -> last pass end on the device, host gaps included
+    else:
+        dev_ms = float(ev0.elapsed_time(ev1))
     t = torch.tensor([dev_ms], device="cuda")
     if world > 1:
         dist.barrier()
@@ -259,14 +282,15 @@ def run_ours(args):
 
     # ---- end to end through the public API: render_proxy_bdpt(scene arrays on the host, spp=K)
     # with the pass_done callback reading the running mean image back every pass
+    # (N > 1: render_proxy_bdpt_distributed, K passes per rank, NCCL all-reduce per round)
     e2e = None
-    if rank == 0 or world > 1:
-        reads = [0]
+    reads = [0]
 
-        def cb(done, img):
-            reads[0] += img.nbytes
-            return True
+    def cb(done, img):
+        reads[0] += img.nbytes
+        return True
 
+    if world == 1:
         render_proxy_bdpt(sc, 1, seed + 1000, params, pass_done=cb, device=local)  # warm the path
         torch.cuda.synchronize()
         reads[0] = 0
@@ -274,11 +298,24 @@ def run_ours(args):
         img = render_proxy_bdpt(sc, args.steps, seed + 2000, params, pass_done=cb, device=local)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        d2h = (reads[0] + img.nbytes) / args.steps
-        e2e = {"value": round(W * H * args.steps * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
-               "h2d_bytes_per_step": int(scene_bytes(sc) / args.steps), "d2h_bytes_per_step": int(d2h),
-               "includes": "pxg_create (scene upload from host arrays, finalize, BVH build, pretrace) + K passes + "
-                           "running-mean read-back every pass (the reference's pass_done callback) + final image"}
+    else:
+        from paper_2503_23412_b200.distributed import render_proxy_bdpt_distributed
+        render_proxy_bdpt_distributed(sc, world, 1000, params, pass_done=cb, local_rank=local)
+        torch.cuda.synchronize()
+        dist.barrier()
+        reads[0] = 0
+        t0 = time.perf_counter()
+        img = render_proxy_bdpt_distributed(sc, args.steps * world, 2000, params, pass_done=cb, local_rank=local)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    d2h = (reads[0] + img.nbytes) / args.steps
+    e2e = {"value": round(W * H * args.steps * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
+           "h2d_bytes_per_step": int(scene_bytes(sc) / args.steps), "d2h_bytes_per_step": int(d2h),
+           "includes": "pxg_create (scene upload from host arrays, finalize, BVH build, pretrace) + K passes + "
+                       "running-mean read-back every pass (the reference's pass_done callback) + final image"}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,6 +342,8 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded scene generator, paper_2503_23412_b200/scenes.py)",
+        "parallelism": ("single GPU" if world == 1 else
+                        f"sample-sharded x{world}: per-rank Philox keys, NCCL all-reduce of fp64 film every pass"),
         "config": config_json(args.config, sc, walks),
         "clocks": clk.summary(),
         "gpu_launches": int(counts[0]),

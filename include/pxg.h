@@ -122,6 +122,9 @@ int pxg_synchronize(pxg_ctx* ctx);
 int pxg_read_mean(pxg_ctx* ctx, double* rgb, int* passes_done);
 /* Unnormalised accumulator (sum of per-pass values), for shard reduction. */
 int pxg_read_accum(pxg_ctx* ctx, double* rgb, int* passes_done);
+/* Same, copied device-to-device into `dst` (a device buffer on the context's GPU, e.g. a
+ * torch tensor that is then NCCL-reduced across ranks). */
+int pxg_accum_to_device(pxg_ctx* ctx, double* dst, int* passes_done);
 
 /* ProxyDiagnostics: rows[4000*5] = {retrace_attempts, retrace_accepts, recip_runs,
  * recip_truncated, estimates_failed} per dense key ((u-1)*10+c)*100+s; touched[4000]

@@ -93,6 +93,7 @@ def lib():
     L.pxg_measure_traversal.argtypes = [C.c_void_p, C.c_int, _DP]
     L.pxg_read_mean.argtypes = [C.c_void_p, _DP, _IP]
     L.pxg_read_accum.argtypes = [C.c_void_p, _DP, _IP]
+    L.pxg_accum_to_device.argtypes = [C.c_void_p, C.c_void_p, _IP]
     L.pxg_read_diag.argtypes = [C.c_void_p, _LP, _IP, _LP]
     L.pxg_read_stats.argtypes = [C.c_void_p, _DP, _LP, _DP]
     L.pxg_dump_pass.argtypes = [C.c_void_p, _DP, _DP, _DP, _IP]
@@ -109,7 +110,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "pxg_default_params", "pxg_abi_version", "pxg_device_count", "pxg_create", "pxg_destroy", "pxg_last_error",
-    "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_read_diag",
+    "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_read_diag",
     "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_intersect", "pxg_occluded",
     "pxg_recip_twopoint", "pxg_rng_draws", "pxg_read_timing",
 ]

@@ -1031,6 +1031,14 @@ int pxg_read_accum(pxg_ctx* c, double* rgb, int* passes) {
   });
 }
 
+int pxg_accum_to_device(pxg_ctx* c, double* dst, int* passes) {
+  return guarded(c, [&]() {
+    CK(cudaMemcpyAsync(dst, c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (passes) *passes = c->passes_done;
+  });
+}
+
 int pxg_read_mean(pxg_ctx* c, double* rgb, int* passes) {
   return guarded(c, [&]() {
     CK(cudaMemcpyAsync(rgb, c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost, c->stream));

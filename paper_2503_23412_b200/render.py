@@ -197,6 +197,12 @@ class ProxyRenderer:
         self._check(self._L.pxg_read_accum(self._ctx, _dp(out), C.byref(done)))
         return out, done.value
 
+    def accum_to_device(self, ptr: int) -> int:
+        """Copy the fp64 accumulator (H_shard x W x 3) into device memory at `ptr`."""
+        done = C.c_int()
+        self._check(self._L.pxg_accum_to_device(self._ctx, C.c_void_p(ptr), C.byref(done)))
+        return done.value
+
     def timing(self):
         t = np.zeros(8)
         cnt = np.zeros(2, np.int64)
