@@ -109,6 +109,14 @@ int pxg_render_passes(pxg_ctx* ctx, int n);
 /* Total number of passes the caller intends to render (the spp of the render call): no
  * look-ahead Stage 1 is started for pass >= limit. -1 (default) = unbounded. */
 int pxg_set_pass_limit(pxg_ctx* ctx, int limit);
+/* Pipelined progressive rendering: enqueue passes without waiting for them, snapshot the
+ * running mean on the device after the enqueued passes (slot 0 or 1), and read a snapshot
+ * back later (waits for it). A caller can hand pass p's mean to its pass_done callback
+ * while pass p+1 already runs; stopping early returns the snapshot of pass p, which is
+ * bitwise the image a p-pass render returns. */
+int pxg_render_passes_async(pxg_ctx* ctx, int n);
+int pxg_snapshot_mean(pxg_ctx* ctx, int slot);
+int pxg_read_snapshot(pxg_ctx* ctx, int slot, double* rgb, int* passes_done);
 /* Renders `n` passes in measurement mode: every traversal launch (closest hit / any hit)
  * is bracketed by CUDA events on its stream and followed by an instrumented copy on the
  * same rays that counts BVH node visits (64 B each) and primitive tests (80 B each).

@@ -90,6 +90,9 @@ def lib():
     L.pxg_render_pass_traced.argtypes = [C.c_void_p]
     L.pxg_synchronize.argtypes = [C.c_void_p]
     L.pxg_set_pass_limit.argtypes = [C.c_void_p, C.c_int]
+    L.pxg_render_passes_async.argtypes = [C.c_void_p, C.c_int]
+    L.pxg_snapshot_mean.argtypes = [C.c_void_p, C.c_int]
+    L.pxg_read_snapshot.argtypes = [C.c_void_p, C.c_int, _DP, _IP]
     L.pxg_measure_traversal.argtypes = [C.c_void_p, C.c_int, _DP]
     L.pxg_read_mean.argtypes = [C.c_void_p, _DP, _IP]
     L.pxg_read_accum.argtypes = [C.c_void_p, _DP, _IP]
@@ -110,7 +113,8 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "pxg_default_params", "pxg_abi_version", "pxg_device_count", "pxg_create", "pxg_destroy", "pxg_last_error",
-    "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_read_diag",
+    "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_render_passes_async", "pxg_snapshot_mean", "pxg_read_snapshot",
+    "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_read_diag",
     "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_intersect", "pxg_occluded",
     "pxg_recip_twopoint", "pxg_rng_draws", "pxg_read_timing",
 ]

@@ -135,6 +135,10 @@ struct pxg_ctx {
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
   ProxWave pw{};
+  double* d_snap[2] = {nullptr, nullptr};  // running-mean snapshots for pipelined pass_done
+  cudaEvent_t snap_ev[2] = {nullptr, nullptr};
+  int snap_passes[2] = {0, 0};
+  double* h_pinned = nullptr;              // pinned staging for read-backs
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
   int* d_trav_next = nullptr;  // [8] ray fetch counters (per stream use)
   // traversal roofline measurement (pxg_measure_traversal)
@@ -158,32 +162,39 @@ struct pxg_ctx {
 
   template <typename T>
   T* alloc(size_t n_) {
-    T* p = dalloc<T>(n_);
+    // stream-ordered allocator on a process-wide pool that keeps freed memory (release
+    // threshold = max): creating and destroying contexts does not map/unmap GBs each time
+    T* p = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n_, 1) * sizeof(T), stream));
     allocs.push_back(p);
     return p;
   }
   template <typename T>
   T* upload(const std::vector<T>& v) {
     T* p = alloc<T>(v.size());
-    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));  // v may be a temporary
     return p;
   }
   template <typename T>
   T* zeros(size_t n_) {
     T* p = alloc<T>(n_);
-    CK(cudaMemset(p, 0, std::max<size_t>(n_, 1) * sizeof(T)));
+    CK(cudaMemsetAsync(p, 0, std::max<size_t>(n_, 1) * sizeof(T), stream));
     return p;
   }
   ~pxg_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     if (stream1) cudaStreamSynchronize(stream1);
-    for (void* p : allocs) cudaFree(p);
+    for (void* p : allocs) cudaFreeAsync(p, stream);
+    if (stream) cudaStreamSynchronize(stream);
     if (d_sort_tmp) cudaFree(d_sort_tmp);
     if (d_scan_tmp) cudaFree(d_scan_tmp);
     if (d_gsort_tmp) cudaFree(d_gsort_tmp);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& e : ev_call) if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool) cudaEventDestroy(e);
+    for (auto& e : snap_ev) if (e) cudaEventDestroy(e);
+    if (h_pinned) cudaFreeHost(h_pinned);
     for (auto& sl : slot)
       for (cudaEvent_t e : {sl.s1_done, sl.s2_done, sl.t0, sl.t1, sl.r0, sl.r1})
         if (e) cudaEventDestroy(e);
@@ -573,12 +584,10 @@ void read_stage2_timing(pxg_ctx* c) {
   c->stage_ms[5] += el(6, 7);
 }
 
-// Renders `npass` passes. Stage 1 of pass p+1 is issued on stream1 right after Stage 2
-// of pass p is enqueued on `stream`, so the two overlap on the device.
 // Renders `npass` passes. Stage 1 runs in batches of c->batch passes on stream1; while
 // the GPU renders Stage 2 of one batch (enqueued without host synchronisation), the host
 // drives Stage 1 of the next batch, so the two overlap.
-void render_passes_impl(pxg_ctx* c, int npass, bool record_last) {
+void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = true) {
   for (int k = 0; k < 8; ++k) c->stage_ms[k] = 0.0;
   c->launches = 0;
   CK(cudaEventRecord(c->ev_call[0], c->stream));
@@ -605,14 +614,19 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last) {
     static const bool overlap = std::getenv("PXG_NO_OVERLAP") == nullptr;
     if (!overlap) CK(cudaStreamSynchronize(c->stream));
     // look-ahead: Stage 1 of the next batch while Stage 2 of this one runs
-    if (c->proxy_on && c->passes_done == stop && (c->pass_limit < 0 || stop < c->pass_limit) &&
+    // (launched as soon as Stage 2 of the current batch has been enqueued, so a caller that
+    // renders one pass per call gets the same pipeline as a bulk call)
+    if (c->proxy_on && (c->pass_limit < 0 || stop < c->pass_limit) &&
         c->slot_of(stop).pass != stop) {
       for (int q = 0; q < c->batch; ++q) read_stage1_timing(c, c->slot_of(stop + q));
       run_stage1_batch(c, stop, batch_len(stop));
     }
-    CK(cudaEventSynchronize(c->ev[7]));
-    read_stage2_timing(c);
+    if (wait) {
+      CK(cudaEventSynchronize(c->ev[7]));
+      read_stage2_timing(c);
+    }
   }
+  if (!wait) return;  // asynchronous: the caller synchronises (snapshot / read)
   CK(cudaEventRecord(c->ev_call[2], c->stream1));
   CK(cudaStreamWaitEvent(c->stream, c->ev_call[2], 0));
   CK(cudaEventRecord(c->ev_call[1], c->stream));
@@ -694,6 +708,13 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       throw InvalidErr{"pxg: max_depth above 16 is not supported"};
     if (params) c->P = *params; else pxg_default_params(&c->P);
     c->seed = seed;
+    CK(cudaSetDevice(device));
+    {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     {
       // Stage 1 is a chain of small latency-bound launches (reciprocal rounds): give it the
@@ -793,6 +814,11 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->pw.value = c->zeros<double>(3 * n);
     c->pw.occl = c->zeros<int>(n);
     c->pw.lv = c->d_scratch;
+    for (int k = 0; k < 2; ++k) {
+      c->d_snap[k] = c->alloc<double>(3 * n);
+      CK(cudaEventCreateWithFlags(&c->snap_ev[k], cudaEventDisableTiming));
+    }
+    CK(cudaMallocHost(&c->h_pinned, sizeof(double) * 3 * n));
     c->d_ebeta = c->zeros<double>(3 * n);
     c->d_epdf = c->zeros<double>(n);
     c->d_lbeta = c->zeros<double>(3 * n);
@@ -1007,6 +1033,32 @@ int pxg_measure_traversal(pxg_ctx* c, int npass, double* out) {
       out[5 * k + 3] = static_cast<double>(h[3 * k + 1]);
       out[5 * k + 4] = static_cast<double>(h[3 * k + 2]);
     }
+  });
+}
+
+int pxg_render_passes_async(pxg_ctx* c, int npass) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
+  return guarded(c, [&]() { render_passes_impl(c, npass, false, false); });
+}
+
+int pxg_snapshot_mean(pxg_ctx* c, int slot) {
+  if (!c || slot < 0 || slot > 1) return fail(c, PXG_E_INVALID, "pxg_snapshot_mean: bad slot");
+  return guarded(c, [&]() {
+    CK(cudaMemcpyAsync(c->d_snap[slot], c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaEventRecord(c->snap_ev[slot], c->stream));
+    c->snap_passes[slot] = c->passes_done;
+  });
+}
+
+int pxg_read_snapshot(pxg_ctx* c, int slot, double* rgb, int* passes) {
+  if (!c || slot < 0 || slot > 1) return fail(c, PXG_E_INVALID, "pxg_read_snapshot: bad slot");
+  return guarded(c, [&]() {
+    CK(cudaEventSynchronize(c->snap_ev[slot]));
+    CK(cudaMemcpy(c->h_pinned, c->d_snap[slot], sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost));
+    const double inv = 1.0 / static_cast<double>(c->snap_passes[slot] > 0 ? c->snap_passes[slot] : 1);
+    for (size_t i = 0; i < 3 * static_cast<size_t>(c->n); ++i) rgb[i] = c->h_pinned[i] * inv;
+    if (passes) *passes = c->snap_passes[slot];
+    check_err(c, c->stream1);
   });
 }
 

@@ -169,6 +169,19 @@ class ProxyRenderer:
     def render_passes(self, n: int = 1):
         self._check(self._L.pxg_render_passes(self._ctx, n))
 
+    def render_passes_async(self, n: int = 1):
+        """Enqueue n passes without waiting for them (see snapshot / read_snapshot)."""
+        self._check(self._L.pxg_render_passes_async(self._ctx, n))
+
+    def snapshot(self, slot: int):
+        self._check(self._L.pxg_snapshot_mean(self._ctx, slot))
+
+    def read_snapshot(self, slot: int) -> np.ndarray:
+        out = np.zeros((self.row1 - self.row0, self.width, 3))
+        done = C.c_int()
+        self._check(self._L.pxg_read_snapshot(self._ctx, slot, _dp(out), C.byref(done)))
+        return out
+
     def set_pass_limit(self, limit: int):
         """No look-ahead Stage 1 for passes >= limit (the render's spp)."""
         self._check(self._L.pxg_set_pass_limit(self._ctx, int(limit)))
@@ -190,6 +203,12 @@ class ProxyRenderer:
         done = C.c_int()
         self._check(self._L.pxg_read_mean(self._ctx, _dp(out), C.byref(done)))
         return out
+
+    def passes_done(self) -> int:
+        done = C.c_int()
+        tmp = np.zeros((self.row1 - self.row0, self.width, 3))
+        self._check(self._L.pxg_read_accum(self._ctx, _dp(tmp), C.byref(done)))
+        return done.value
 
     def accum(self):
         out = np.zeros((self.row1 - self.row0, self.width, 3))
@@ -276,13 +295,29 @@ def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | N
         spp = scene.settings.spp
     with ProxyRenderer(scene, seed, params, device=device) as r:
         r.set_pass_limit(spp)
-        done = 0
-        for _ in range(spp):
-            r.render_passes(1)
-            done += 1
-            if pass_done is not None and not pass_done(done, r.mean()):
-                break
-        img = r.mean()
+        if pass_done is None:
+            r.render_passes(spp)
+            img = r.mean()
+        elif diagnostics is None:
+            # pipelined: pass k+1 is already running while pass_done sees the mean after k;
+            # an early stop returns that snapshot (bitwise the k-pass image)
+            r.render_passes_async(1)
+            r.snapshot(0)
+            img = None
+            for k in range(1, spp + 1):
+                if k < spp:
+                    r.render_passes_async(1)
+                    r.snapshot(k & 1)
+                img = r.read_snapshot((k - 1) & 1)
+                if not pass_done(k, img):
+                    break
+        else:
+            # diagnostics must not include a pass beyond an early stop: one pass at a time
+            for _ in range(spp):
+                r.render_passes(1)
+                if not pass_done(r.passes_done(), r.mean()):
+                    break
+            img = r.mean()
         if diagnostics is not None:
             d = r.diagnostics()
             diagnostics.rows = d.rows
