@@ -35,7 +35,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "Msamples/s (full proxy-BDPT px samples)"
-NODE_BYTES, PRIM_BYTES = 64, 80  # BvhNode, PrimRec (csrc/pxg_scene.cuh)
+NODE_BYTES, PRIM_BYTES = 128, 80  # BvhNode4, PrimRec (csrc/pxg_scene.cuh)
 
 
 def parse():

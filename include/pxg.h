@@ -119,7 +119,7 @@ int pxg_snapshot_mean(pxg_ctx* ctx, int slot);
 int pxg_read_snapshot(pxg_ctx* ctx, int slot, double* rgb, int* passes_done);
 /* Renders `n` passes in measurement mode: every traversal launch (closest hit / any hit)
  * is bracketed by CUDA events on its stream and followed by an instrumented copy on the
- * same rays that counts BVH node visits (64 B each) and primitive tests (80 B each).
+ * same rays that counts 4-wide BVH node visits (128 B each) and primitive tests (80 B each).
  * out[10] = {closest: ms, launches, rays, node visits, prim tests,
  *            any-hit: ms, launches, rays, node visits, prim tests}. */
 int pxg_measure_traversal(pxg_ctx* ctx, int n, double* out);

@@ -181,6 +181,72 @@ struct Builder {
   }
 };
 
+// Collapses the binary BVH into a 4-wide one: each wide node takes up to four descendants,
+// always opening the internal child with the largest box surface (the usual collapse
+// heuristic). Child boxes are copied from the binary nodes, so they stay conservative.
+struct Collapser {
+  const std::vector<HostNode>& bin;
+  std::vector<HostNode4>& out;
+
+  struct Child {
+    float lo[3], hi[3];
+    int code;
+  };
+
+  static float area(const Child& c) {
+    if (c.hi[0] < c.lo[0]) return -1.f;
+    const float ex = c.hi[0] - c.lo[0], ey = c.hi[1] - c.lo[1], ez = c.hi[2] - c.lo[2];
+    return ex * ey + ey * ez + ez * ex;
+  }
+
+  Child child_of(int node, int k) const {
+    const HostNode& n = bin[node];
+    Child c;
+    for (int a = 0; a < 3; ++a) {
+      c.lo[a] = k == 0 ? n.lo0[a] : n.lo1[a];
+      c.hi[a] = k == 0 ? n.hi0[a] : n.hi1[a];
+    }
+    c.code = k == 0 ? n.c0 : n.c1;
+    return c;
+  }
+
+  int build(int node) {
+    Child ch[4];
+    int m = 0;
+    ch[m++] = child_of(node, 0);
+    ch[m++] = child_of(node, 1);
+    while (m < 4) {
+      int best = -1;
+      float best_area = -1.f;
+      for (int k = 0; k < m; ++k)
+        if (ch[k].code >= 0 && area(ch[k]) > best_area) {
+          best = k;
+          best_area = area(ch[k]);
+        }
+      if (best < 0) break;
+      const int b = ch[best].code;
+      ch[best] = child_of(b, 0);
+      ch[m++] = child_of(b, 1);
+    }
+    const int idx = static_cast<int>(out.size());
+    out.push_back(HostNode4{});
+    int codes[4];
+    for (int k = 0; k < 4; ++k) {
+      if (k < m && ch[k].code >= 0) codes[k] = build(ch[k].code);
+      else codes[k] = k < m ? ch[k].code : ~0;
+    }
+    HostNode4& w = out[idx];
+    for (int k = 0; k < 4; ++k) {
+      for (int a = 0; a < 3; ++a) {
+        w.lo[a][k] = k < m ? ch[k].lo[a] : 1e30f;
+        w.hi[a][k] = k < m ? ch[k].hi[a] : -1e30f;
+      }
+      w.child[k] = codes[k];
+    }
+    return idx;
+  }
+};
+
 }  // namespace
 
 void finalize_scene(const SceneDesc& d, SceneHost& h) {
@@ -285,6 +351,9 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
     B.build(0, n, all, 0);  // nodes is empty, so the root lands in slot 0
     h.bvh_depth = B.max_depth_seen;
   }
+  h.nodes4.clear();
+  h.nodes4.reserve(h.nodes.size() / 2 + 2);
+  Collapser{h.nodes, h.nodes4}.build(0);
   // leaf-ordered exact records
   h.recs.resize(n);
   for (int k = 0; k < n; ++k) {

@@ -26,6 +26,16 @@ struct alignas(16) HostRec {
 };
 static_assert(sizeof(HostRec) == 80, "record size");
 
+// Layout-identical to pxg::BvhNode4 (pxg_scene.cuh), 128 B: four child boxes as SoA
+// float4s (lo x/y/z, hi x/y/z), four child codes (>= 0 node, < 0 leaf ~(first*16+count)).
+struct alignas(16) HostNode4 {
+  float lo[3][4];
+  float hi[3][4];
+  int child[4];
+  int pad[4];
+};
+static_assert(sizeof(HostNode4) == 128, "node4 size");
+
 struct SceneHost {
   std::vector<int> prim_mat, prim_shape, prim_emitter;
   std::vector<double> prim_geo;     // [n][3]
@@ -37,6 +47,7 @@ struct SceneHost {
   double cam[12];  // position, fwd, right, up
   double tan_half = 0.0, aspect = 1.0;
   std::vector<HostNode> nodes;
+  std::vector<HostNode4> nodes4;
   std::vector<int> order;
   std::vector<HostRec> recs;
   int bvh_depth = 0;

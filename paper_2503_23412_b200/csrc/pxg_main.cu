@@ -763,6 +763,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     // device scene
     SceneView& S = c->S;
     S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
+    S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
     S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
     S.prim_mat = c->upload(h.prim_mat);
     S.prim_emitter = c->upload(h.prim_emitter);

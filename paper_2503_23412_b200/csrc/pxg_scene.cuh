@@ -21,7 +21,7 @@
 namespace pxg {
 
 constexpr double kRayEps = 1e-7;  // scene.cpp:19
-constexpr int kStack = 64;
+constexpr int kStack = 96;  // 4-wide BVH: up to 3 pushes per level
 
 enum Shape { kSphere = 0, kTriangle = 1, kRectangle = 2 };
 
@@ -30,6 +30,15 @@ struct alignas(16) BvhNode {
   float lo1[3], hi1[3];
   int c0, c1;  // >= 0 internal node, < 0 leaf: ~c = first*16 + count
   int pad0, pad1;
+};
+
+// 4-wide node (128 B): child boxes as SoA float4 (lo x, lo y, lo z, hi x, hi y, hi z) so a
+// step is 7 independent 16-byte loads; child codes as in BvhNode.
+struct alignas(16) BvhNode4 {
+  float lo[3][4];
+  float hi[3][4];
+  int child[4];
+  int pad[4];
 };
 
 struct alignas(16) PrimRec {
@@ -42,6 +51,7 @@ struct alignas(16) PrimRec {
 
 struct SceneView {
   const BvhNode* nodes;
+  const BvhNode4* nodes4;
   const PrimRec* recs;
   const int* prim_mat;       // [n_prims]
   const int* prim_emitter;   // [n_prims] emitter index or -1
@@ -163,7 +173,75 @@ struct TravCount {
   unsigned long long nodes, prims;
 };
 
+// One 4-wide node: box tests of the four children (fp32, conservative).
+struct Node4Hits {
+  float tn[4];
+  int code[4];
+  unsigned hit;  // bit k: child k's box is hit
+};
+
+__device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, const RayF& rf, float tb) {
+  const float4* __restrict__ q = reinterpret_cast<const float4*>(S.nodes4 + node);
+  const float4 lx = __ldg(q + 0), ly = __ldg(q + 1), lz = __ldg(q + 2);
+  const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
+  const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
+  Node4Hits r;
+  r.hit = 0u;
+  const float lxs[4] = {lx.x, lx.y, lx.z, lx.w}, lys[4] = {ly.x, ly.y, ly.z, ly.w}, lzs[4] = {lz.x, lz.y, lz.z, lz.w};
+  const float hxs[4] = {hx.x, hx.y, hx.z, hx.w}, hys[4] = {hy.x, hy.y, hy.z, hy.w}, hzs[4] = {hz.x, hz.y, hz.z, hz.w};
+  r.code[0] = ch.x;
+  r.code[1] = ch.y;
+  r.code[2] = ch.z;
+  r.code[3] = ch.w;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float lo[3] = {lxs[k], lys[k], lzs[k]}, hi[3] = {hxs[k], hys[k], hzs[k]};
+    float tn;
+    if (box_f(lo, hi, rf, tb, tn)) r.hit |= 1u << k;
+    r.tn[k] = tn;
+  }
+  return r;
+}
+
+// Pushes the internal children of `h` that are hit within tb, nearest popped first;
+// returns the nearest one to visit next (or -1).
+__device__ __forceinline__ void cswap4(float& ta, int& ca, float& tb, int& cb) {
+  const bool sw = tb < ta;
+  const float t = sw ? tb : ta;
+  const int c = sw ? cb : ca;
+  tb = sw ? ta : tb;
+  cb = sw ? ca : cb;
+  ta = t;
+  ca = c;
+}
+
+constexpr int kNoChild = static_cast<int>(0x80000000u);  // never a node or leaf code
+
+// Orders the children of `h` (internal nodes and leaves) hit within tbn by tnear: the
+// nearest is returned (kNoChild if none), the rest are pushed so that nearer ones pop
+// first. Non-candidates get +inf keys; a 5-comparator network sorts in registers.
+__device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* stack, int& sp) {
+  float t[4];
+  int c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool ok = (h.hit >> k & 1u) && h.tn[k] <= tbn;
+    t[k] = ok ? h.tn[k] : __int_as_float(0x7f800000);
+    c[k] = ok ? h.code[k] : kNoChild;
+  }
+  cswap4(t[0], c[0], t[1], c[1]);
+  cswap4(t[2], c[2], t[3], c[3]);
+  cswap4(t[0], c[0], t[2], c[2]);
+  cswap4(t[1], c[1], t[3], c[3]);
+  cswap4(t[1], c[1], t[2], c[2]);
+#pragma unroll
+  for (int k = 3; k >= 1; --k)
+    if (c[k] != kNoChild && sp < kStack) stack[sp++] = c[k];
+  return c[0];
+}
+
 // Closest hit: returns the original primitive id or -1; t_best in/out (fp64).
+// A step visits either one 4-wide node (four box tests) or one leaf (its primitives).
 template <bool kCount = false>
 __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, const V3& d, double& t_best,
                                             TravCount* cnt = nullptr) {
@@ -171,63 +249,31 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
   int best = -1;
   int stack[kStack];
   int sp = 0;
-  int node = 0;
-  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
+  int code = 0;
   for (;;) {
-    // internal node: test both children
-    const float4 n0 = __ldg(nodes + 4 * node + 0);
-    const float4 n1 = __ldg(nodes + 4 * node + 1);
-    const float4 n2 = __ldg(nodes + 4 * node + 2);
-    const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
-    if (kCount) cnt->nodes += 1;
-    const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
-    const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
-    const float tb = tbound_f(t_best);
-    float tn0, tn1;
-    bool h0 = box_f(lo0, hi0, rf, tb, tn0);
-    bool h1 = box_f(lo1, hi1, rf, tb, tn1);
-    int c0 = n3.x, c1 = n3.y;
-    // leaves are processed immediately; internal children are pushed near-first
-    int next = -1;
-    #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool h = k == 0 ? h0 : h1;
-      const int c = k == 0 ? c0 : c1;
-      if (!h) continue;
-      if (c < 0) {
-        const int code = ~c;
-        const int first = code >> 4, count = code & 15;
-        if (kCount) cnt->prims += count;
-        for (int i = 0; i < count; ++i) {
-          int id;
-          double t = rec_hit(S.recs + first + i, o, d, t_best, id);
-          if (t > 0.0 && (t < t_best || id > best)) {
-            t_best = t;
-            best = id;
-          }
+    int next;
+    if (code >= 0) {
+      const Node4Hits h = node4_test(S, code, rf, tbound_f(t_best));
+      if (kCount) cnt->nodes += 1;
+      next = node4_order(h, tbound_f(t_best), stack, sp);
+    } else {
+      const int first = (~code) >> 4, count = (~code) & 15;
+      if (kCount) cnt->prims += count;
+      for (int i = 0; i < count; ++i) {
+        int id;
+        const double t = rec_hit(S.recs + first + i, o, d, t_best, id);
+        if (t > 0.0 && (t < t_best || id > best)) {
+          t_best = t;
+          best = id;
         }
       }
+      next = kNoChild;
     }
-    const float tbn = tbound_f(t_best);
-    const bool in0 = h0 && c0 >= 0 && tn0 <= tbn;
-    const bool in1 = h1 && c1 >= 0 && tn1 <= tbn;
-    if (in0 && in1) {
-      const bool first0 = tn0 <= tn1;
-      next = first0 ? c0 : c1;
-      if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
-    } else if (in0) {
-      next = c0;
-    } else if (in1) {
-      next = c1;
-    } else {
-      next = -1;
-    }
-    if (next < 0) {
-      // pop until a node still in range (stack entries are re-tested at the next visit)
+    if (next == kNoChild) {
       if (sp == 0) break;
       next = stack[--sp];
     }
-    node = next;
+    code = next;
   }
   return best;
 }
@@ -243,51 +289,28 @@ __device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const 
   const RayF rf = make_rayf(o, d);
   int stack[kStack];
   int sp = 0;
-  int node = 0;
+  int code = 0;
   const float tb = tbound_f(t_max);
-  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
   for (;;) {
-    const float4 n0 = __ldg(nodes + 4 * node + 0);
-    const float4 n1 = __ldg(nodes + 4 * node + 1);
-    const float4 n2 = __ldg(nodes + 4 * node + 2);
-    const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
-    if (kCount) cnt->nodes += 1;
-    const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
-    const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
-    float tn0, tn1;
-    bool h0 = box_f(lo0, hi0, rf, tb, tn0);
-    bool h1 = box_f(lo1, hi1, rf, tb, tn1);
-    int c0 = n3.x, c1 = n3.y;
-    #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool h = k == 0 ? h0 : h1;
-      const int c = k == 0 ? c0 : c1;
-      if (!h || c >= 0) continue;
-      const int code = ~c;
-      const int first = code >> 4, count = code & 15;
+    int next;
+    if (code >= 0) {
+      const Node4Hits h = node4_test(S, code, rf, tb);
+      if (kCount) cnt->nodes += 1;
+      next = node4_order(h, tb, stack, sp);
+    } else {
+      const int first = (~code) >> 4, count = (~code) & 15;
       for (int i = 0; i < count; ++i) {
         int id;
         if (kCount) cnt->prims += 1;
-        double t = rec_hit(S.recs + first + i, o, d, t_max, id);
-        if (t > 0.0) return true;
+        if (rec_hit(S.recs + first + i, o, d, t_max, id) > 0.0) return true;
       }
+      next = kNoChild;
     }
-    const bool in0 = h0 && c0 >= 0;
-    const bool in1 = h1 && c1 >= 0;
-    int next;
-    if (in0 && in1) {
-      const bool first0 = tn0 <= tn1;
-      next = first0 ? c0 : c1;
-      if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
-    } else if (in0) {
-      next = c0;
-    } else if (in1) {
-      next = c1;
-    } else {
+    if (next == kNoChild) {
       if (sp == 0) break;
       next = stack[--sp];
     }
-    node = next;
+    code = next;
   }
   return false;
 }

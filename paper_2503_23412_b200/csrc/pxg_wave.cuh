@@ -205,8 +205,7 @@ struct TravState {
   RayF rf;
   double t_best;
   int best, node, sp;
-  int stack[kStack];
-};
+};  // the traversal stack is a separate local array so these stay in registers
 
 __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int j) {
   const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
@@ -220,27 +219,15 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
 }
 
 // Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
-__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts) {
-  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
-  const int node = ts.node;
-  const float4 n0 = __ldg(nodes + 4 * node + 0);
-  const float4 n1 = __ldg(nodes + 4 * node + 1);
-  const float4 n2 = __ldg(nodes + 4 * node + 2);
-  const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
-  const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
-  const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
-  const float tb = tbound_f(ts.t_best);
-  float tn0, tn1;
-  const bool h0 = box_f(lo0, hi0, ts.rf, tb, tn0);
-  const bool h1 = box_f(lo1, hi1, ts.rf, tb, tn1);
-  const int c0 = n3.x, c1 = n3.y;
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool h = k == 0 ? h0 : h1;
-    const int c = k == 0 ? c0 : c1;
-    if (!h || c >= 0) continue;
-    const int code = ~c;
-    const int first = code >> 4, count = code & 15;
+// ts.node holds a child code: >= 0 a 4-wide node, < 0 a leaf.
+__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack) {
+  int next;
+  if (ts.node >= 0) {
+    const float tb = tbound_f(ts.t_best);
+    const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
+    next = node4_order(h, tb, stack, ts.sp);
+  } else {
+    const int first = (~ts.node) >> 4, count = (~ts.node) & 15;
     for (int i = 0; i < count; ++i) {
       int id;
       const double t = rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id);
@@ -249,68 +236,34 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts) 
         ts.best = id;
       }
     }
+    next = kNoChild;
   }
-  const float tbn = tbound_f(ts.t_best);
-  const bool in0 = h0 && c0 >= 0 && tn0 <= tbn;
-  const bool in1 = h1 && c1 >= 0 && tn1 <= tbn;
-  int next;
-  if (in0 && in1) {
-    const bool first0 = tn0 <= tn1;
-    next = first0 ? c0 : c1;
-    if (ts.sp < kStack) ts.stack[ts.sp++] = first0 ? c1 : c0;
-  } else if (in0) {
-    next = c0;
-  } else if (in1) {
-    next = c1;
-  } else {
+  if (next == kNoChild) {
     if (ts.sp == 0) return true;
-    next = ts.stack[--ts.sp];
+    next = stack[--ts.sp];
   }
   ts.node = next;
   return false;
 }
 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
-__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts) {
-  const float4* __restrict__ nodes = reinterpret_cast<const float4*>(S.nodes);
-  const int node = ts.node;
-  const float4 n0 = __ldg(nodes + 4 * node + 0);
-  const float4 n1 = __ldg(nodes + 4 * node + 1);
-  const float4 n2 = __ldg(nodes + 4 * node + 2);
-  const int4 n3 = __ldg(reinterpret_cast<const int4*>(nodes + 4 * node + 3));
-  const float lo0[3] = {n0.x, n0.y, n0.z}, hi0[3] = {n0.w, n1.x, n1.y};
-  const float lo1[3] = {n1.z, n1.w, n2.x}, hi1[3] = {n2.y, n2.z, n2.w};
-  const float tb = tbound_f(ts.t_best);
-  float tn0, tn1;
-  const bool h0 = box_f(lo0, hi0, ts.rf, tb, tn0);
-  const bool h1 = box_f(lo1, hi1, ts.rf, tb, tn1);
-  const int c0 = n3.x, c1 = n3.y;
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool h = k == 0 ? h0 : h1;
-    const int c = k == 0 ? c0 : c1;
-    if (!h || c >= 0) continue;
-    const int code = ~c;
-    const int first = code >> 4, count = code & 15;
+__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack) {
+  int next;
+  if (ts.node >= 0) {
+    const float tb = tbound_f(ts.t_best);
+    const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
+    next = node4_order(h, tb, stack, ts.sp);
+  } else {
+    const int first = (~ts.node) >> 4, count = (~ts.node) & 15;
     for (int i = 0; i < count; ++i) {
       int id;
       if (rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
+    next = kNoChild;
   }
-  const bool in0 = h0 && c0 >= 0;
-  const bool in1 = h1 && c1 >= 0;
-  int next;
-  if (in0 && in1) {
-    const bool first0 = tn0 <= tn1;
-    next = first0 ? c0 : c1;
-    if (ts.sp < kStack) ts.stack[ts.sp++] = first0 ? c1 : c0;
-  } else if (in0) {
-    next = c0;
-  } else if (in1) {
-    next = c1;
-  } else {
+  if (next == kNoChild) {
     if (ts.sp == 0) return 2;
-    next = ts.stack[--ts.sp];
+    next = stack[--ts.sp];
   }
   ts.node = next;
   return 0;
@@ -326,6 +279,7 @@ __global__ void __launch_bounds__(128) k_trav_persistent(SceneView S, RayQueue Q
   int j = -1;
   bool exhausted = false;
   TravState ts;
+  int stack[kStack];
   for (;;) {
     const bool idle = j < 0;
     const unsigned m = __ballot_sync(FULL, idle);
@@ -349,12 +303,12 @@ __global__ void __launch_bounds__(128) k_trav_persistent(SceneView S, RayQueue Q
     }
     if (j >= 0) {
       if (kAny) {
-        const int r = any_step(S, ts);
+        const int r = any_step(S, ts, stack);
         if (r) {
           Q.hit_prim[j] = r == 1 ? 1 : 0;
           j = -1;
         }
-      } else if (closest_step(S, ts)) {
+      } else if (closest_step(S, ts, stack)) {
         Q.hit_prim[j] = ts.best;
         Q.hit_t[j] = ts.t_best;
         j = -1;
@@ -364,7 +318,7 @@ __global__ void __launch_bounds__(128) k_trav_persistent(SceneView S, RayQueue Q
 }
 
 // Instrumented copies of the traversal kernels for the roofline measurement: the same
-// traversal code on the same queue, counting node visits (64 B each) and primitive tests
+// traversal code on the same queue, counting node visits (128 B 4-wide nodes) and primitive tests
 // (80 B each). Launched after the timed launch; results are identical and discarded.
 __global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, unsigned long long* acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
