@@ -440,13 +440,24 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
       k_recip_eval<<<blocks(static_cast<long long>(count) * chunk, 64), 64, 0, st>>>(
           c->S, c->seed, R, stride, cap, c->d_bp, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
           c->d_rn, c->d_re);
-      k_recip_dfs<<<blocks(count, 64), 64, 0, st>>>(R, stride, cap, c->d_bp, 0.0, c->d_ract[cur], c->d_rnact + cur,
-                                                    chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
+      k_recip_dfs_warp<128><<<blocks(count, 4), 128, 0, st>>>(R, stride, cap, c->d_bp, 0.0, c->d_ract[cur],
+                                                    c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
                                                     c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
                                                     c->d_rnact + (1 - cur), c->d_err);
       c->launches += 2;
     });
     c->launches += 1;
+    if (std::getenv("PXG_PROFILE")) {  // run-cost distribution of this batch
+      std::vector<long long> cost(runs);
+      CK(cudaMemcpyAsync(cost.data(), c->d_run_cost, sizeof(long long) * runs, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::sort(cost.begin(), cost.end());
+      long long sum = 0, live = 0;
+      for (long long v : cost) sum += v, live += v > 0;
+      auto q = [&](double f) { return cost[std::min<size_t>(runs - 1, static_cast<size_t>(f * runs))]; };
+      std::fprintf(stderr, "[pxg] recip batch: runs %d live %lld nodes %lld p50 %lld p90 %lld p99 %lld p999 %lld max %lld\n",
+                   runs, live, sum, q(0.5), q(0.9), q(0.99), q(0.999), cost[runs - 1]);
+    }
   }
   CK(cudaEventRecord(s0.r1, st));
   hp.mark("recip");
@@ -601,6 +612,9 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   while (left > 0) {
     const int p = c->passes_done;
     if (c->proxy_on && c->slot_of(p).pass != p) run_stage1_batch(c, p, batch_len(p));
+    // measurement mode: the streams are serialised so every timed traversal launch has the
+    // GPU to itself (its duration is the kernel's, not a share of the Stage-1 overlap)
+    if (c->measure) CK(cudaStreamSynchronize(c->stream1));
     // Stage 2 of the passes of this batch, enqueued without host synchronisation
     const int stop = c->proxy_on ? c->slot_of(p).batch_end : p + left;
     const int m = std::min(left, stop - p);
@@ -612,7 +626,7 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
     }
     left -= m;
     static const bool overlap = std::getenv("PXG_NO_OVERLAP") == nullptr;
-    if (!overlap) CK(cudaStreamSynchronize(c->stream));
+    if (!overlap || c->measure) CK(cudaStreamSynchronize(c->stream));
     // look-ahead: Stage 1 of the next batch while Stage 2 of this one runs
     // (launched as soon as Stage 2 of the current batch has been enqueued, so a caller that
     // renders one pass per call gets the same pipeline as a bulk call)
@@ -1295,8 +1309,9 @@ int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double
       recip_rounds(st, nact, [&](int cur, int count, int chunk) {
         k_twopoint_eval<<<blocks(static_cast<long long>(count) * chunk, 128), 128>>>(seed, bound, cap, act[cur],
                                                                                      nact + cur, chunk, rs, g, ns, ne);
-        k_recip_dfs<<<blocks(count, 128), 128>>>(1, 1, cap, nullptr, bound, act[cur], nact + cur, chunk, rs, g, ns, ne,
-                                                 fr, de, dc, dt, act[1 - cur], nact + (1 - cur), derr);
+        // a small frame window so the spill / reload paths are exercised by the fixture
+        k_recip_dfs_warp<4><<<blocks(count, 4), 128>>>(1, 1, cap, nullptr, bound, act[cur], nact + cur, chunk, rs, g,
+                                                       ns, ne, fr, de, dc, dt, act[1 - cur], nact + (1 - cur), derr);
       });
       CK(cudaGetLastError());
       CK(cudaMemcpy(est, de, sizeof(double) * n, cudaMemcpyDeviceToHost));

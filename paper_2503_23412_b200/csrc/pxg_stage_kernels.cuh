@@ -355,6 +355,151 @@ __global__ void k_recip_dfs(int repeats, int stride, long long cap, const BatchP
   trunc[j] = s.truncated;
 }
 
+// Phase B, warp-cooperative: one warp per active run. The DFS state machine of dfs_resume
+// runs redundantly (warp-uniform) in every lane; node values are fetched 32 at a time with
+// one coalesced load per lane and broadcast by shuffle, and the frame stack's top W frames
+// live in shared memory (frames below are spilled to the run's global frame array and
+// reloaded in blocks). A long run then costs a few shared-memory round trips per node
+// instead of dependent global loads (the single-thread kernel's long-run tail). Same
+// arithmetic in the same order as dfs_resume, so estimates are bit-identical.
+template <int W>
+__global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride, long long cap, const BatchPass* bp,
+                                                        double fixed_bound, const int* active, const int* n_active,
+                                                        int chunk, RunState* st, const double* g,
+                                                        const long long* nsplit, const int* nerr, RecipFrame* frames,
+                                                        double* est, long long* cost, int* trunc, int* next,
+                                                        int* n_next, int* err) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double s_ans[4][W];
+  __shared__ long long s_rem[4][W];
+  __shared__ signed char s_sgn[4][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long a = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (a >= *n_active) return;  // warp-uniform
+  const int j = active[a];
+  RunState s = st[j];
+  s.avail = min(cap, s.avail + chunk);
+  const double B = bp ? bp[j / stride].bound[(j % stride) / repeats] : fixed_bound;
+  const size_t o = static_cast<size_t>(j) * cap;
+  const double* G = g + o;
+  const long long* N = nsplit + o;
+  const int* E = nerr + o;
+  RecipFrame* F = frames + o;
+  double* sa = s_ans[warp];
+  long long* sr = s_rem[warp];
+  signed char* sg = s_sgn[warp];
+  long long lo = s.depth;  // frames [lo, depth) are in shared memory, [0, lo) in F
+  long long base = -1;     // node window: lane i holds node base + i
+  double wg = 0.0;
+  long long wn = 0;
+  int we = 0;
+  bool done;
+  for (;;) {
+    if (s.entering) {
+      if (s.depth >= cap || s.cost >= cap) {
+        s.entering = 0;
+        s.truncated = 1;
+        s.ret = 0.0;
+      } else {
+        const long long k = s.cost;
+        if (k >= s.avail) {
+          done = false;
+          break;
+        }
+        if (base < 0 || k >= base + 32) {
+          base = k;
+          const long long kk = k + lane;
+          if (kk < s.avail) {
+            wg = G[kk];
+            wn = N[kk];
+            we = E[kk];
+          }
+        }
+        const int src = static_cast<int>(k - base);
+        const int ek = __shfl_sync(FULL, we, src);
+        s.entering = 0;
+        if (ek) {
+          s.err = ek;
+          s.done = 1;
+          done = true;
+          break;
+        }
+        const double gk = __shfl_sync(FULL, wg, src);
+        const long long nk = __shfl_sync(FULL, wn, src);
+        ++s.cost;
+        const double ans = gk / B;
+        if (nk > 0) {
+          const long long d = s.depth;
+          if (d - lo == W) {  // window full: spill its bottom frame
+            const int ls = static_cast<int>(lo % W);
+            if (lane == 0) F[lo] = RecipFrame{sa[ls], static_cast<double>(sg[ls]), sr[ls]};
+            ++lo;
+          }
+          const int slot = static_cast<int>(d % W);
+          sa[slot] = ans;
+          sg[slot] = static_cast<signed char>((gk > 0.0) - (gk < 0.0));
+          sr[slot] = nk - 1;
+          ++s.depth;
+          s.entering = 1;
+          continue;
+        }
+        s.ret = ans;
+      }
+    }
+    if (s.depth == 0) {
+      s.done = 1;
+      s.ret = 1.0 / B + s.ret;
+      done = true;
+      break;
+    }
+    --s.depth;
+    if (s.depth < lo) {  // reload frames [new_lo, depth] spilled earlier
+      const long long nl = s.depth - W + 1 > 0 ? s.depth - W + 1 : 0;
+      __syncwarp();
+      for (long long i = nl + lane; i <= s.depth; i += 32) {
+        const RecipFrame fr = F[i];
+        const int sl = static_cast<int>(i % W);
+        sa[sl] = fr.ans;
+        sg[sl] = static_cast<signed char>(fr.sgn);
+        sr[sl] = fr.rem;
+      }
+      __syncwarp();
+      lo = nl;
+    }
+    const int slot = static_cast<int>(s.depth % W);
+    const double pa = sa[slot] + static_cast<double>(sg[slot]) * s.ret;
+    const long long rem = sr[slot];
+    sa[slot] = pa;
+    if (rem > 0) {
+      sr[slot] = rem - 1;
+      ++s.depth;
+      s.entering = 1;
+      continue;
+    }
+    s.ret = pa;
+  }
+  if (!done) {  // flush the window; the next round resumes from global frames
+    __syncwarp();
+    for (long long i = lo + lane; i < s.depth; i += 32) {
+      const int sl = static_cast<int>(i % W);
+      F[i] = RecipFrame{sa[sl], static_cast<double>(sg[sl]), sr[sl]};
+    }
+  }
+  if (lane != 0) return;
+  st[j] = s;
+  if (!done) {
+    next[atomicAdd(n_next, 1)] = j;
+    return;
+  }
+  if (s.err) {
+    set_err(err, s.err);
+    return;
+  }
+  est[j] = s.ret;
+  cost[j] = s.cost;
+  trunc[j] = s.truncated;
+}
+
 // Per entry: mean and second moment of its runs, validity (proxy.cpp:409-427); per bucket
 // the estimate sums in pool order; the kept list and the per-label lists in pool order
 // (proxy.cpp:729-735); then the stats snapshot Stage 2 of this pass reads. One block.
