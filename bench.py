@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="tuning sweeps: skip roofline, e2e and cpu_baseline")
     return ap.parse_args()
 
 
@@ -263,11 +264,11 @@ def run_ours(args):
 
     # ---- roofline: every traversal launch of 2 more passes timed + work-counted
     r.set_pass_limit(-1)
-    tr = r.measure_traversal(2)
+    tr = r.measure_traversal(2) if not args.quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
     r.close()
     peak, peak_src = measured_peak_gbs()
     roof = {}
-    for kind, kname in (("closest", "k_closest"), ("anyhit", "k_anyhit")):
+    for kind, kname in (("closest", "k_trav_persistent<0>"), ("anyhit", "k_trav_persistent<1>")):
         m = tr[kind]
         if m["launches"] <= 0 or m["ms"] <= 0:
             continue
@@ -299,7 +300,9 @@ def run_ours(args):
         reads[0] += img.nbytes
         return True
 
-    if world == 1:
+    if args.quick:
+        pass
+    elif world == 1:
         render_proxy_bdpt(sc, 1, seed + 1000, params, pass_done=cb, device=local)  # warm the path
         torch.cuda.synchronize()
         reads[0] = 0
@@ -320,14 +323,15 @@ def run_ours(args):
         tt = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    d2h = (reads[0] + img.nbytes) / args.steps
-    e2e = {"value": round(W * H * args.steps * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
-           "h2d_bytes_per_step": int(scene_bytes(sc) / args.steps), "d2h_bytes_per_step": int(d2h),
-           "includes": "pxg_create (scene upload from host arrays, finalize, BVH build, pretrace) + K passes + "
-                       "running-mean read-back every pass (the reference's pass_done callback) + final image"}
+    if not args.quick:
+        d2h = (reads[0] + img.nbytes) / args.steps
+        e2e = {"value": round(W * H * args.steps * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(scene_bytes(sc) / args.steps), "d2h_bytes_per_step": int(d2h),
+               "includes": "pxg_create (scene upload from host arrays, finalize, BVH build, pretrace) + K passes + "
+                           "running-mean read-back every pass (the reference's pass_done callback) + final image"}
 
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
             cores = host_cores()
             v, dt = reference_sample(sc, walks, cores, seed=0)

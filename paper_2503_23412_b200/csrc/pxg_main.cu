@@ -6,6 +6,9 @@
 // -> gamma) on `stream`. Stage 1 of pass p+1 reads and writes only the subspace statistics
 // and its own pool slot, never the film, the grid shares or gamma, so overlapping it with
 // Stage 2 of pass p leaves every result identical to the sequential order.
+#include <mutex>
+#include <utility>
+
 #include "pxg_stage_kernels.cuh"
 
 // ------------------------------------------------------------------ context
@@ -31,10 +34,40 @@ struct PoolSlot {
   long long* snap_rcnt = nullptr;
   int pass = -1;
   int batch_end = 0;  // first pass after the Stage-1 batch this slot belongs to
-  int n_ent = 0;
-  long long raw = 0;
   bool timing_pending = false;
 };
+
+// Process-wide cache of pinned host staging buffers: page-locking and unlocking host memory
+// (cudaMallocHost / cudaFreeHost) costs up to hundreds of ms and would otherwise be paid by
+// every context create / destroy (the per-call render_proxy_bdpt path).
+namespace {
+std::mutex g_pinned_mu;
+std::vector<std::pair<size_t, void*>> g_pinned_free;
+
+void* pinned_acquire(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    for (size_t i = 0; i < g_pinned_free.size(); ++i)
+      if (g_pinned_free[i].first == bytes) {
+        void* p = g_pinned_free[i].second;
+        g_pinned_free.erase(g_pinned_free.begin() + static_cast<long>(i));
+        return p;
+      }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) throw CudaErr{"cudaMallocHost failed"};
+  return p;
+}
+
+void pinned_release(void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  if (g_pinned_free.size() >= 8) {  // bounded: free the oldest
+    cudaFreeHost(g_pinned_free.front().second);
+    g_pinned_free.erase(g_pinned_free.begin());
+  }
+  g_pinned_free.emplace_back(bytes, p);
+}
+}  // namespace
 
 struct pxg_ctx {
   std::string err;
@@ -81,11 +114,9 @@ struct pxg_ctx {
   double* d_gamma_accum = nullptr;
   // pool (Stage 1 working buffers)
   int cand_cap = 0;
-  unsigned long long *d_ckey = nullptr, *d_ckey_alt = nullptr;
-  unsigned *d_cval = nullptr, *d_cval_alt = nullptr;
+  unsigned long long* d_ckey = nullptr;
+  unsigned* d_cval = nullptr;
   int* d_ccount = nullptr;
-  void* d_sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
   unsigned* d_sel = nullptr;
   double* d_probe = nullptr;
   int* d_probe_ok = nullptr;
@@ -101,12 +132,11 @@ struct pxg_ctx {
   int* d_ract[2] = {nullptr, nullptr};
   int* d_rnact = nullptr;
   int recip_rounds = 0;
-  static constexpr int kBatchMax = 32;  // passes per Stage-1 batch (PXG_BATCH, default kBatchDefault)
+  static constexpr int kBatchMax = kBatchSetMax;  // passes per Stage-1 batch (PXG_BATCH, default kBatchDefault)
   static constexpr int kBatchDefault = 8;
   PoolSlot slot[2 * kBatchMax];        // ring: batch k uses half k & 1
   int batch = kBatchMax;               // passes per batch (<= kBatchMax)
   int next_batch = 0;                  // first pass without a launched Stage 1
-  BatchPass* d_bp = nullptr;           // [kBatchMax]
   PoolSlot& slot_of(int pass) { return slot[pass % (2 * batch)]; }
   int* d_err = nullptr;
   // diagnostics
@@ -114,7 +144,6 @@ struct pxg_ctx {
   unsigned long long *d_diag_attempt = nullptr, *d_diag_accept = nullptr;
   unsigned long long* d_kept_total = nullptr;
   int* d_diag_touched = nullptr;
-  long long pool_raw_total = 0;
   // wavefront queues and buffers
   RayQueue qA{}, qB{}, qS{};  // qA/qB: Stage 2 bounces; qS: shadow rays
   RayQueue wA{}, wB{};        // Stage-1 pool-walk bounces (own queues: runs concurrently)
@@ -138,8 +167,14 @@ struct pxg_ctx {
   double* d_snap[2] = {nullptr, nullptr};  // running-mean snapshots for pipelined pass_done
   cudaEvent_t snap_ev[2] = {nullptr, nullptr};
   int snap_passes[2] = {0, 0};
-  double* h_pinned = nullptr;              // pinned staging for read-backs
+  double* h_pinned = nullptr;              // pinned staging for read-backs (process-wide cache)
+  size_t pinned_bytes = 0;
+  int* h_err = nullptr;                    // [2] pinned error flags of the two snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
+  int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
+  int dfs_blocks = 0;         // grid-stride warp-DFS grid
+  int sel_cap = 0;            // shared-memory capacity (entries) of the pool selection
+  size_t sel_smem = 0;
   int* d_trav_next = nullptr;  // [8] ray fetch counters (per stream use)
   // traversal roofline measurement (pxg_measure_traversal)
   bool measure = false;
@@ -187,14 +222,12 @@ struct pxg_ctx {
     if (stream1) cudaStreamSynchronize(stream1);
     for (void* p : allocs) cudaFreeAsync(p, stream);
     if (stream) cudaStreamSynchronize(stream);
-    if (d_sort_tmp) cudaFree(d_sort_tmp);
-    if (d_scan_tmp) cudaFree(d_scan_tmp);
-    if (d_gsort_tmp) cudaFree(d_gsort_tmp);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& e : ev_call) if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& e : snap_ev) if (e) cudaEventDestroy(e);
-    if (h_pinned) cudaFreeHost(h_pinned);
+    if (h_pinned) pinned_release(h_pinned, pinned_bytes);
+    if (h_err) pinned_release(h_err, 2 * sizeof(int));
     for (auto& sl : slot)
       for (cudaEvent_t e : {sl.s1_done, sl.s2_done, sl.t0, sl.t1, sl.r0, sl.r1})
         if (e) cudaEventDestroy(e);
@@ -205,17 +238,21 @@ struct pxg_ctx {
 
 namespace {
 
+void raise_err(int e) {
+  if (!e) return;
+  const char* what = e == kErrIntegrand ? "reciprocal: integrand must be finite and non-negative"
+                     : e == kErrSupport ? "reciprocal: support pdf must be finite and positive"
+                     : e == kErrSplit   ? "stochastic_split: bad ratio"
+                     : e == kErrPool    ? "pool: candidate selection failed (buffer overflow or key ties)"
+                                        : "update_ratio: ratio must be finite and non-negative";
+  throw RuntimeErr{what};
+}
+
 void check_err(pxg_ctx* c, cudaStream_t st) {
   int e = 0;
   CK(cudaMemcpyAsync(&e, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (e) {
-    const char* what = e == kErrIntegrand ? "reciprocal: integrand must be finite and non-negative"
-                       : e == kErrSupport ? "reciprocal: support pdf must be finite and positive"
-                       : e == kErrSplit   ? "stochastic_split: bad ratio"
-                                          : "update_ratio: ratio must be finite and non-negative";
-    throw RuntimeErr{what};
-  }
+  raise_err(e);
 }
 
 // PXG_PROFILE=1: synchronise and print host-side stage timestamps (debugging aid).
@@ -308,32 +345,42 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   c->launches += 10;
 }
 
-// The reciprocal runs of one pass: rounds of (parallel node evaluation, DFS resume) with
-// the evaluated prefix doubling per round, until every run has finished.
+// The reciprocal runs of a batch: rounds of (parallel node evaluation, DFS resume); round r
+// evaluates the next chunk_r = min(first * grow^r, 16384) nodes of every active run. The
+// round count is fixed on the host (the smallest R with chunk_0 + ... + chunk_{R-1} >= cap,
+// after which every run has finished), and the kernels read the active count on the device,
+// so no round waits for the host; a round with no active run costs two empty launches.
 template <typename Eval>
-int recip_rounds(cudaStream_t stream, int* nact, Eval&& eval_and_dfs) {
-  static const int first = std::getenv("PXG_RECIP_CHUNK") ? std::atoi(std::getenv("PXG_RECIP_CHUNK")) : 32;
-  static const int grow = std::getenv("PXG_RECIP_GROW") ? std::atoi(std::getenv("PXG_RECIP_GROW")) : 4;
+int recip_rounds(cudaStream_t stream, long long cap, int* nact, Eval&& eval_and_dfs) {
+  static const int first = std::getenv("PXG_RECIP_CHUNK") ? std::atoi(std::getenv("PXG_RECIP_CHUNK")) : 16;
+  static const int grow = std::getenv("PXG_RECIP_GROW") ? std::atoi(std::getenv("PXG_RECIP_GROW")) : 2;
   static const bool verbose = std::getenv("PXG_PROFILE") != nullptr;
-  int cur = 0, chunk = first, rounds = 0;
-  for (;;) {
-    int count = 0;
-    CK(cudaMemcpyAsync(&count, nact + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    if (verbose) std::fprintf(stderr, "[pxg]   round %d: %d runs x %d nodes\n", rounds, count, chunk);
-    if (count == 0) break;
+  int cur = 0, chunk = std::max(first, 1), rounds = 0;
+  long long covered = 0;
+  do {
+    if (verbose) {
+      int count = 0;
+      CK(cudaMemcpyAsync(&count, nact + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      std::fprintf(stderr, "[pxg]   round %d: %d runs x %d nodes\n", rounds, count, chunk);
+    }
     CK(cudaMemsetAsync(nact + (1 - cur), 0, sizeof(int), stream));
-    eval_and_dfs(cur, count, chunk);
+    eval_and_dfs(cur, chunk);
     cur = 1 - cur;
-    chunk = std::min(chunk * grow, 16384);
+    covered += chunk;
+    chunk = static_cast<int>(std::min<long long>(static_cast<long long>(chunk) * std::max(grow, 1), 16384));
     ++rounds;
-  }
+  } while (covered < cap);
   return rounds;
 }
 
 void read_stage1_timing(pxg_ctx* c, PoolSlot& sl) {
   if (!sl.timing_pending) return;
-  cudaEventSynchronize(sl.t1);
+  sl.timing_pending = false;
+  if (cudaEventQuery(sl.t1) != cudaSuccess) {  // never block the host for diagnostics
+    cudaGetLastError();
+    return;
+  }
   float a = 0.f, b = 0.f;
   if (cudaEventElapsedTime(&a, sl.t0, sl.t1) != cudaSuccess) a = 0.f;
   if (cudaEventElapsedTime(&b, sl.r0, sl.r1) != cudaSuccess) b = 0.f;
@@ -369,42 +416,22 @@ void stage1_front(pxg_ctx* c, int pass, PoolSlot& sl) {
     ++c->launches;
     hp.mark("walks");
   }
-  int raw = 0;
-  CK(cudaMemcpyAsync(&raw, c->d_ccount, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (raw > c->cand_cap) throw RuntimeErr{"pool candidate buffer overflow"};
+  // priority selection, entry count, raw count and kappa on the device (no host round trip)
   const int budget = c->P.pool_budget;
-  const int n_ent = std::min(raw, std::max(budget, 0));
-  std::vector<unsigned> sel(n_ent);
-  if (n_ent > 0) {
-    const unsigned* src = c->d_cval;
-    if (raw > budget) {
-      CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, c->sort_tmp_bytes, c->d_ckey, c->d_ckey_alt, c->d_cval,
-                                         c->d_cval_alt, raw, 0, 64, st));
-      ++c->launches;
-      src = c->d_cval_alt;
-    }
-    CK(cudaMemcpyAsync(sel.data(), src, sizeof(unsigned) * n_ent, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    // keys tie only with probability ~2^-64; ties are broken by (walk, end) like the oracle
-    std::sort(sel.begin(), sel.end());  // (walk << 5 | end) order == (walk, end) order
-    CK(cudaMemcpyAsync(c->d_sel, sel.data(), sizeof(unsigned) * n_ent, cudaMemcpyHostToDevice, st));
-  }
-  hp.mark("select");
-  sl.raw = raw;
-  sl.n_ent = n_ent;
+  k_pool_select<<<1, 1024, c->sel_smem, st>>>(c->d_ckey, c->d_cval, c->d_ccount, c->cand_cap, budget, c->sel_cap,
+                                              c->d_sel, sl.ps, c->d_err);
+  ++c->launches;
   sl.pass = pass;
-  const double kappa = raw > 0 ? std::min(1.0, static_cast<double>(budget) / static_cast<double>(raw)) : 1.0;
-  CK(cudaMemcpyAsync(&sl.ps->kappa, &kappa, sizeof(double), cudaMemcpyHostToDevice, st));
-  if (n_ent > 0) {
+  hp.mark("select");
+  if (budget > 0) {
     const int R = c->P.recip_repeats;
-    k_pool_entries<<<blocks(n_ent, 64), 64, 0, st>>>(c->M, n_ent, c->d_sel, c->d_wpool, walks, c->shard.walk_begin,
-                                                     sl.inc, sl.prefix);
-    k_pool_probes<<<blocks(4 * n_ent, 64), 64, 0, st>>>(c->S, c->seed, pass, n_ent, sl.inc, sl.prefix, c->d_probe,
-                                                        c->d_probe_ok, R);
-    k_pool_bounds<<<1, 512, 2 * sizeof(double) * n_ent, st>>>(n_ent, sl.inc, c->d_probe, c->d_probe_ok,
-                                                              c->d_max_ratio, c->d_ratio_cnt, c->d_touched,
-                                                              sl.bound, c->d_err);
+    k_pool_entries<<<blocks(budget, 64), 64, 0, st>>>(c->M, sl.ps, c->d_sel, c->d_wpool, walks, c->shard.walk_begin,
+                                                      sl.inc, sl.prefix);
+    k_pool_probes<<<blocks(4 * budget, 64), 64, 0, st>>>(c->S, c->seed, pass, sl.ps, sl.inc, sl.prefix, c->d_probe,
+                                                         c->d_probe_ok, R);
+    k_pool_bounds<<<1, 512, 2 * sizeof(double) * budget, st>>>(sl.ps, sl.inc, c->d_probe, c->d_probe_ok,
+                                                               c->d_max_ratio, c->d_ratio_cnt, c->d_touched,
+                                                               sl.bound, c->d_err);
     c->launches += 3;
     hp.mark("entries+bounds");
   }
@@ -419,28 +446,28 @@ void stage1_front(pxg_ctx* c, int pass, PoolSlot& sl) {
 void run_stage1_batch(pxg_ctx* c, int p0, int L) {
   cudaStream_t st = c->stream1;
   HostProbe hp(st);
-  std::vector<BatchPass> bp(L);
+  BatchSet bs{};
+  bs.n = L;
   for (int b = 0; b < L; ++b) {
     PoolSlot& sl = c->slot_of(p0 + b);
     stage1_front(c, p0 + b, sl);
-    bp[b] = BatchPass{sl.inc, sl.prefix, sl.bound, p0 + b, sl.n_ent};
+    bs.p[b] = BatchPass{sl.inc, sl.prefix, sl.bound, sl.ps, p0 + b};
   }
   const int R = c->P.recip_repeats;
   const int stride = std::max(c->P.pool_budget, 1) * std::max(R, 1);
   PoolSlot& s0 = c->slot_of(p0);
   CK(cudaEventRecord(s0.r0, st));
   if (R >= 1) {
-    CK(cudaMemcpyAsync(c->d_bp, bp.data(), sizeof(BatchPass) * L, cudaMemcpyHostToDevice, st));
     const int runs = L * stride;
     const long long cap = c->P.recursion_cap;
     CK(cudaMemsetAsync(c->d_rnact, 0, 2 * sizeof(int), st));
-    k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, c->d_bp, c->d_rstate, c->d_ract[0], c->d_rnact,
+    k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, bs, c->d_rstate, c->d_ract[0], c->d_rnact,
                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc);
-    c->recip_rounds = recip_rounds(st, c->d_rnact, [&](int cur, int count, int chunk) {
-      k_recip_eval<<<blocks(static_cast<long long>(count) * chunk, 64), 64, 0, st>>>(
-          c->S, c->seed, R, stride, cap, c->d_bp, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
+    c->recip_rounds = recip_rounds(st, cap, c->d_rnact, [&](int cur, int chunk) {
+      k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
+          c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
           c->d_rn, c->d_re);
-      k_recip_dfs_warp<128><<<blocks(count, 4), 128, 0, st>>>(R, stride, cap, c->d_bp, 0.0, c->d_ract[cur],
+      k_recip_dfs_warp<128><<<c->dfs_blocks, 128, 0, st>>>(R, stride, cap, bs, 0.0, c->d_ract[cur],
                                                     c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
                                                     c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
                                                     c->d_rnact + (1 - cur), c->d_err);
@@ -464,8 +491,8 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
   for (int b = 0; b < L; ++b) {
     PoolSlot& sl = c->slot_of(p0 + b);
     const size_t o = static_cast<size_t>(b) * stride;
-    k_pool_finish<<<1, 512, sizeof(int) * (sl.n_ent + kS), st>>>(
-        sl.n_ent, R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq,
+    k_pool_finish<<<1, 512, sizeof(int) * (std::max(c->P.pool_budget, 0) + kS), st>>>(
+        R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq,
         c->d_est_cnt, c->d_touched, sl.diag, sl.diag_touched, sl.kept, sl.label_start, sl.label_list, sl.ps,
         sl.snap_sum, sl.snap_sq, sl.snap_cnt, c->d_max_ratio, c->d_ratio_cnt, sl.snap_max, sl.snap_rcnt);
     ++c->launches;
@@ -489,7 +516,6 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
     k_fold_diag<<<blocks(kBuckets, 128), 128, 0, st>>>(sl.diag, sl.diag_touched, sl.ps, c->d_diag,
                                                        c->d_diag_touched, c->d_kept_total);
     ++c->launches;
-    c->pool_raw_total += sl.raw;
   }
   CK(cudaEventRecord(c->ev[1], st));
   {
@@ -603,8 +629,12 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   c->launches = 0;
   CK(cudaEventRecord(c->ev_call[0], c->stream));
   CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
+  // The first batch of a context is one pass: nothing can overlap it, so a short first
+  // batch lets Stage 2 start after one pass of Stage 1 (the pipeline fill of the per-call
+  // render_proxy_bdpt path). Batch composition does not change any result.
+  static const int first_batch = std::getenv("PXG_FIRST_BATCH") ? std::atoi(std::getenv("PXG_FIRST_BATCH")) : 1;
   auto batch_len = [&](int p0) {
-    int L = c->batch;
+    int L = p0 == 0 ? std::max(1, std::min(c->batch, first_batch)) : c->batch;
     if (c->pass_limit >= 0) L = std::min(L, std::max(1, c->pass_limit - p0));
     return L;
   };
@@ -833,7 +863,10 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       c->d_snap[k] = c->alloc<double>(3 * n);
       CK(cudaEventCreateWithFlags(&c->snap_ev[k], cudaEventDisableTiming));
     }
-    CK(cudaMallocHost(&c->h_pinned, sizeof(double) * 3 * n));
+    c->pinned_bytes = sizeof(double) * 3 * n;
+    c->h_pinned = static_cast<double*>(pinned_acquire(c->pinned_bytes));
+    c->h_err = static_cast<int*>(pinned_acquire(2 * sizeof(int)));
+    c->h_err[0] = c->h_err[1] = 0;
     c->d_ebeta = c->zeros<double>(3 * n);
     c->d_epdf = c->zeros<double>(n);
     c->d_lbeta = c->zeros<double>(3 * n);
@@ -869,7 +902,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     {
       size_t need = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, need, c->conn.count, c->conn.offset, static_cast<int>(n + 1), c->stream);
-      CK(cudaMalloc(&c->d_scan_tmp, need));
+      c->d_scan_tmp = c->alloc<char>(need);
       c->scan_tmp_bytes = need;
     }
     if (c->proxy_on && c->n_walks > 0) {
@@ -895,7 +928,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       size_t need = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_gbin, c->d_gbin_sorted, c->d_gval, c->d_gval_sorted,
                                       static_cast<int>(n), 0, 12, c->stream);
-      CK(cudaMalloc(&c->d_gsort_tmp, need));
+      c->d_gsort_tmp = c->alloc<char>(need);
       c->gsort_bytes = need;
     }
     c->d_pflags = c->zeros<int>(n);
@@ -916,17 +949,17 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     const int walks = c->shard.walk_end - c->shard.walk_begin;
     c->cand_cap = std::max(1, walks) * std::max(1, c->max_depth - 2);
     c->d_ckey = c->alloc<unsigned long long>(c->cand_cap);
-    c->d_ckey_alt = c->alloc<unsigned long long>(c->cand_cap);
     c->d_cval = c->alloc<unsigned>(c->cand_cap);
-    c->d_cval_alt = c->alloc<unsigned>(c->cand_cap);
     c->d_ccount = c->zeros<int>(1);
+    if (c->P.pool_budget > 4096) throw InvalidErr{"pxg: pool_budget above 4096 is not supported"};
     {
-      // sort scratch sized once for the largest possible candidate count (no per-pass realloc)
-      size_t need = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_ckey, c->d_ckey_alt, c->d_cval, c->d_cval_alt,
-                                      c->cand_cap, 0, 64, c->stream);
-      CK(cudaMalloc(&c->d_sort_tmp, need));
-      c->sort_tmp_bytes = need;
+      // device priority selection: 2 x budget expected keys below the first threshold
+      int cap = 1024;
+      while (cap < 4 * c->P.pool_budget) cap <<= 1;
+      c->sel_cap = cap;
+      c->sel_smem = static_cast<size_t>(cap) * (sizeof(unsigned long long) + sizeof(unsigned));
+      CK(cudaFuncSetAttribute(k_pool_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(c->sel_smem)));
     }
     const int B = std::max(c->P.pool_budget, 1);
     const int R = std::max(c->P.recip_repeats, 1);
@@ -958,7 +991,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_run_est = c->zeros<double>(NR);
     c->d_run_cost = c->zeros<long long>(NR);
     c->d_run_trunc = c->zeros<int>(NR);
-    c->d_bp = c->zeros<BatchPass>(pxg_ctx::kBatchMax);
     if (c->P.recursion_cap > (1 << 20) || c->P.recip_repeats > 255)
       throw InvalidErr{"pxg: recursion_cap above 2^20 or recip_repeats above 255 is not supported"};
     if (c->proxy_on && c->P.recursion_cap > 0) {
@@ -973,7 +1005,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_ract[1] = c->alloc<int>(NR);
     c->d_rnact = c->zeros<int>(2);
     c->d_err = c->zeros<int>(1);
-    c->d_kept_total = c->zeros<unsigned long long>(1);
+    c->d_kept_total = c->zeros<unsigned long long>(2);  // kept, raw
     c->d_tcnt = c->zeros<unsigned long long>(6);
     c->d_trav_next = c->zeros<int>(8);
     {
@@ -981,6 +1013,11 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
+      int pe = 0, pd = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe, k_recip_eval, 64, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, k_recip_dfs_warp<128>, 128, 0));
+      c->eval_blocks = std::max(1, sms * std::max(pe, 1));
+      c->dfs_blocks = std::max(1, sms * std::max(pd, 1));
     }
     c->d_diag = c->zeros<long long>(kBuckets * 5);
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
@@ -1060,6 +1097,9 @@ int pxg_snapshot_mean(pxg_ctx* c, int slot) {
   if (!c || slot < 0 || slot > 1) return fail(c, PXG_E_INVALID, "pxg_snapshot_mean: bad slot");
   return guarded(c, [&]() {
     CK(cudaMemcpyAsync(c->d_snap[slot], c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    // the error flag as of these passes (Stage-1 errors of a pass are visible once its
+    // Stage 2, which waits for them, has run), read without waiting for the look-ahead
+    CK(cudaMemcpyAsync(c->h_err + slot, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaEventRecord(c->snap_ev[slot], c->stream));
     c->snap_passes[slot] = c->passes_done;
   });
@@ -1073,7 +1113,7 @@ int pxg_read_snapshot(pxg_ctx* c, int slot, double* rgb, int* passes) {
     const double inv = 1.0 / static_cast<double>(c->snap_passes[slot] > 0 ? c->snap_passes[slot] : 1);
     for (size_t i = 0; i < 3 * static_cast<size_t>(c->n); ++i) rgb[i] = c->h_pinned[i] * inv;
     if (passes) *passes = c->snap_passes[slot];
-    check_err(c, c->stream1);
+    raise_err(c->h_err[slot]);
   });
 }
 
@@ -1122,12 +1162,12 @@ int pxg_read_diag(pxg_ctx* c, long long* rows, int* touched, long long* pool) {
     std::vector<long long> d(kBuckets * 5);
     std::vector<unsigned long long> at(kBuckets), ac(kBuckets);
     std::vector<int> tc(kBuckets);
-    unsigned long long kept = 0;
+    unsigned long long kept[2] = {0, 0};
     CK(cudaMemcpy(d.data(), c->d_diag, sizeof(long long) * kBuckets * 5, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(at.data(), c->d_diag_attempt, sizeof(unsigned long long) * kBuckets, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(ac.data(), c->d_diag_accept, sizeof(unsigned long long) * kBuckets, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(tc.data(), c->d_diag_touched, sizeof(int) * kBuckets, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&kept, c->d_kept_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(kept, c->d_kept_total, sizeof(kept), cudaMemcpyDeviceToHost));
     for (int k = 0; k < kBuckets; ++k) {
       d[k * 5 + 0] = static_cast<long long>(at[k]);
       d[k * 5 + 1] = static_cast<long long>(ac[k]);
@@ -1135,8 +1175,8 @@ int pxg_read_diag(pxg_ctx* c, long long* rows, int* touched, long long* pool) {
     if (rows) std::memcpy(rows, d.data(), sizeof(long long) * kBuckets * 5);
     if (touched) std::memcpy(touched, tc.data(), sizeof(int) * kBuckets);
     if (pool) {
-      pool[0] = c->pool_raw_total;
-      pool[1] = static_cast<long long>(kept);
+      pool[0] = static_cast<long long>(kept[1]);
+      pool[1] = static_cast<long long>(kept[0]);
     }
   });
 }
@@ -1218,7 +1258,7 @@ int pxg_dump_pool(pxg_ctx* c, int cap, int* n_out, long long* raw, int* walk, in
     const PoolSlot& sl = c->slot_of(c->passes_done - 1);
     PassState ps;
     CK(cudaMemcpy(&ps, sl.ps, sizeof(PassState), cudaMemcpyDeviceToHost));
-    const int n_ent = sl.n_ent;
+    const int n_ent = ps.n_ent;
     std::vector<IncHdr> inc(n_ent);
     std::vector<int> kept(std::max(ps.n_kept, 0));
     std::vector<double> bd(n_ent);
@@ -1238,7 +1278,7 @@ int pxg_dump_pool(pxg_ctx* c, int cap, int* n_out, long long* raw, int* walk, in
       if (bound) bound[i] = bd[kept[i]];
     }
     if (n_out) *n_out = ps.n_kept;
-    if (raw) *raw = sl.raw;
+    if (raw) *raw = ps.raw;
   });
 }
 
@@ -1305,12 +1345,13 @@ int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double
       auto* derr = static_cast<int*>(A(sizeof(int)));
       CK(cudaMemset(nact, 0, 2 * sizeof(int)));
       CK(cudaMemset(derr, 0, sizeof(int)));
-      k_recip_init<<<blocks(n, 128), 128>>>(n, 1, 1, nullptr, rs, act[0], nact, de, dc, dt);
-      recip_rounds(st, nact, [&](int cur, int count, int chunk) {
-        k_twopoint_eval<<<blocks(static_cast<long long>(count) * chunk, 128), 128>>>(seed, bound, cap, act[cur],
+      const BatchSet none{};  // n == 0: every run live, fixed bound
+      k_recip_init<<<blocks(n, 128), 128>>>(n, 1, 1, none, rs, act[0], nact, de, dc, dt);
+      recip_rounds(st, cap, nact, [&](int cur, int chunk) {
+        k_twopoint_eval<<<4 * 148, 128>>>(seed, bound, cap, act[cur],
                                                                                      nact + cur, chunk, rs, g, ns, ne);
         // a small frame window so the spill / reload paths are exercised by the fixture
-        k_recip_dfs_warp<4><<<blocks(count, 4), 128>>>(1, 1, cap, nullptr, bound, act[cur], nact + cur, chunk, rs, g,
+        k_recip_dfs_warp<4><<<8 * 148, 128>>>(1, 1, cap, none, bound, act[cur], nact + cur, chunk, rs, g,
                                                        ns, ne, fr, de, dc, dt, act[1 - cur], nact + (1 - cur), derr);
       });
       CK(cudaGetLastError());

@@ -28,7 +28,7 @@ struct IncView {
 };
 
 // Errors raised by the estimator (the reference throws std::runtime_error).
-enum { kErrNone = 0, kErrIntegrand = 1, kErrSupport = 2, kErrSplit = 3, kErrRatio = 4 };
+enum { kErrNone = 0, kErrIntegrand = 1, kErrSupport = 2, kErrSplit = 3, kErrRatio = 4, kErrPool = 5 };
 
 struct RecipFrame {
   double ans;

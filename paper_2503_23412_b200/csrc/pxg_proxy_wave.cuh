@@ -29,6 +29,9 @@ struct PassState {  // device-resident per-pass scalars of a pool slot
   int n_kept;
   int err;
   long long pool_kept_total;
+  int n_ent;      // entries selected by the priority reservoir (min(raw, budget))
+  int pad_;
+  long long raw;  // eligible candidates of the pass (ProxyDiagnostics::pool_raw)
 };
 
 enum { kPxNone = 0, kPxRetrace = 1, kPxRetraced = 2, kPxShadow = 3 };

@@ -123,11 +123,113 @@ __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, uint64
   }
 }
 
+// Sorts n (a power of two) (key, value) pairs ascending, lexicographically; all threads.
+__device__ void bitonic_sort_pairs(unsigned long long* k, unsigned* v, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj <= i) continue;
+        const bool up = (i & size) == 0;
+        const unsigned long long ka = k[i], kb = k[ixj];
+        const unsigned va = v[i], vb = v[ixj];
+        const bool gt = ka > kb || (ka == kb && va > vb);
+        if (gt == up) {
+          k[i] = kb;
+          k[ixj] = ka;
+          v[i] = vb;
+          v[ixj] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Priority selection of the pool (deviation 2 for Algorithm R, proxy.cpp:696-711) on the
+// device, so Stage 1 never waits for the host: the `budget` smallest keys (ties by
+// (walk, end)) in (walk, end) order. One block. A key threshold T is bisected until the
+// keys below it number between need = min(raw, budget) and the shared-memory capacity `cap`
+// (keys are i.i.d. uniform, so the first guess, 2 x budget / raw of the key range, almost
+// always lands); those keys are compacted and bitonic-sorted by (key, value), and the
+// values of the first `need` are sorted again. Writes n_ent, raw and kappa of the pass.
+__global__ void __launch_bounds__(1024) k_pool_select(const unsigned long long* keys, const unsigned* vals,
+                                                      const int* count, int cand_cap, int budget, int cap,
+                                                      unsigned* sel, PassState* ps, int* err) {
+  extern __shared__ unsigned long long sk[];  // [cap] keys, then [cap] values
+  unsigned* sv = reinterpret_cast<unsigned*>(sk + cap);
+  __shared__ int s_cnt;
+  const int raw = *count;
+  const int need = min(raw, max(budget, 0));
+  if (threadIdx.x == 0) {
+    ps->raw = raw;
+    ps->n_ent = raw > cand_cap ? 0 : need;
+    const double r = static_cast<double>(budget) / static_cast<double>(raw);
+    ps->kappa = raw > 0 ? (r < 1.0 ? r : 1.0) : 1.0;  // std::min(1.0, budget / raw)
+    if (raw > cand_cap) set_err(err, kErrPool);
+  }
+  if (raw > cand_cap || need == 0) return;
+  const bool all = raw <= budget;
+  unsigned long long lo = 0, hi = ~0ull, T = ~0ull;
+  if (!all) {
+    const double f = 2.0 * static_cast<double>(budget) / static_cast<double>(raw);
+    T = f >= 1.0 ? ~0ull : static_cast<unsigned long long>(f * 18446744073709551616.0);
+  }
+  for (int it = 0;; ++it) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < raw; i += blockDim.x) {
+      const unsigned long long key = keys[i];
+      if (all || key < T) {
+        const int slot = atomicAdd(&s_cnt, 1);
+        if (slot < cap) {
+          sk[slot] = key;
+          sv[slot] = vals[i];
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (all || (cnt >= need && cnt <= cap)) break;
+    if (cnt < need) lo = T; else hi = T;
+    const unsigned long long nT = lo + (hi - lo) / 2;
+    if (nT == T || it > 130) {  // only possible with > cap equal keys
+      if (threadIdx.x == 0) {
+        set_err(err, kErrPool);
+        ps->n_ent = 0;
+      }
+      return;
+    }
+    T = nT;
+    __syncthreads();
+  }
+  const int cnt = min(s_cnt, cap);
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  for (int i = cnt + threadIdx.x; i < n2; i += blockDim.x) {
+    sk[i] = ~0ull;
+    sv[i] = ~0u;
+  }
+  __syncthreads();
+  if (!all) bitonic_sort_pairs(sk, sv, n2);
+  // the first `need` values, sorted: (walk << 5 | end) order == (walk, end) order
+  int m2 = 1;
+  while (m2 < need) m2 <<= 1;
+  for (int i = threadIdx.x; i < m2; i += blockDim.x) {  // each index read and written by one thread
+    const unsigned long long x = i < need ? static_cast<unsigned long long>(sv[i]) : ~0ull;
+    sk[i] = x;
+    sv[i] = 0u;
+  }
+  __syncthreads();
+  bitonic_sort_pairs(sk, sv, m2);
+  for (int i = threadIdx.x; i < need; i += blockDim.x) sel[i] = static_cast<unsigned>(sk[i]);
+}
+
 // Materialise the kept entries (dropout on the stored walk prefix, proxy.cpp:59-94).
-__global__ void k_pool_entries(Mapper M, int n_ent, const unsigned* sel, const PV* wpool, int n_walks, int walk_begin,
-                               IncHdr* inc, PV* prefix) {
+__global__ void k_pool_entries(Mapper M, const PassState* ps, const unsigned* sel, const PV* wpool, int n_walks,
+                               int walk_begin, IncHdr* inc, PV* prefix) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_ent) return;
+  if (k >= ps->n_ent) return;
   const int w = static_cast<int>(sel[k] >> 5), end = static_cast<int>(sel[k] & 31u);
   PV v[kMaxLight];
   for (int q = 0; q < end; ++q) v[q] = wpool[static_cast<size_t>(q) * n_walks + (w - walk_begin)];
@@ -141,10 +243,10 @@ __global__ void k_pool_entries(Mapper M, int n_ent, const unsigned* sel, const P
 
 // The four f/q probes of every entry (estimate_inverse_p, proxy.cpp:389-394), one thread
 // per probe on its own stream (PROBE, end | i << 8).
-__global__ void k_pool_probes(SceneView S, uint64_t seed, int pass, int n_ent, const IncHdr* inc, const PV* prefix,
-                              double* probe, int* probe_ok, int repeats) {
+__global__ void k_pool_probes(SceneView S, uint64_t seed, int pass, const PassState* ps, const IncHdr* inc,
+                              const PV* prefix, double* probe, int* probe_ok, int repeats) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 4 * n_ent) return;
+  if (t >= 4 * ps->n_ent) return;
   const int k = t >> 2, i = t & 3;
   probe_ok[t] = 0;
   const IncHdr& h = inc[k];
@@ -195,9 +297,10 @@ __global__ void k_pretrace(SceneView S, Mapper M, uint64_t seed, int n_paths, do
 // of the same bucket (the sequential update_ratio/b_bound order of proxy.cpp:389-395).
 // Maxima are order-independent, so every entry computes its own prefix maximum; the last
 // entry of each bucket then commits the bucket state. One block.
-__global__ void k_pool_bounds(int n_ent, const IncHdr* inc, const double* probe, const int* probe_ok,
+__global__ void k_pool_bounds(const PassState* ps, const IncHdr* inc, const double* probe, const int* probe_ok,
                               double* max_ratio, long long* ratio_cnt, int* touched, double* bound, int* err) {
   extern __shared__ double sm[];  // [n_ent] max, then [n_ent] touched flags (as double)
+  const int n_ent = ps->n_ent;
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     const int key = inc[k].key;
     double m = max_ratio[key];
@@ -243,8 +346,17 @@ struct BatchPass {
   const IncHdr* inc;
   const PV* prefix;
   const double* bound;
+  const PassState* ps;  // n_ent is device-resident (selected on the device)
   int pass;
-  int n_ent;
+};
+
+// The passes of one Stage-1 batch, passed BY VALUE as a __grid_constant__ kernel parameter
+// (no host-to-device copy, so enqueueing a batch never waits for the host). n == 0: the
+// two-point fixture (every run live, fixed bound).
+constexpr int kBatchSetMax = 32;
+struct BatchSet {
+  BatchPass p[kBatchSetMax];
+  int n;
 };
 
 // Phase A of the reciprocal runs: evaluate nodes [avail, avail + chunk) of every active
@@ -252,15 +364,16 @@ struct BatchPass {
 // decision from (RECIP_SPLIT, k) (include/pxg_philox.h), so its value does not depend on
 // the tree shape; draw_g (recip.hpp:69-77) and stochastic_split (recip.hpp:49-56).
 __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride, long long cap,
-                             const BatchPass* bp, const int* active, const int* n_active, int chunk,
-                             const RunState* st, double* g, long long* nsplit, int* nerr) {
-  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+                             const __grid_constant__ BatchSet bs, const int* active, const int* n_active,
+                             int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
+  const long long total = static_cast<long long>(*n_active) * chunk;
+  for (long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; tid < total;
+       tid += static_cast<long long>(gridDim.x) * blockDim.x) {
   const long long a = tid / chunk;
-  if (a >= *n_active) return;
   const int j = active[a];
   const long long k = st[j].avail + tid % chunk;
-  if (k >= cap) return;
-  const BatchPass& P = bp[j / stride];
+  if (k >= cap) continue;
+  const BatchPass& P = bs.p[j / stride];
   const int w = j % stride;
   const int e = w / repeats, r = w % repeats;
   const IncHdr& h = P.inc[e];
@@ -279,17 +392,19 @@ __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride
   g[o] = gv;
   nsplit[o] = n;
   nerr[o] = err;
+  }
 }
 
 // The two-point fixture f = {1, 3}, q = 1/2 (proj/tests/test_recip.cpp:16-23) as Phase A.
 __global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, const int* active, const int* n_active,
                                 int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
-  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long total = static_cast<long long>(*n_active) * chunk;
+  for (long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; tid < total;
+       tid += static_cast<long long>(gridDim.x) * blockDim.x) {
   const long long a = tid / chunk;
-  if (a >= *n_active) return;
   const int j = active[a];
   const long long k = st[j].avail + tid % chunk;
-  if (k >= cap) return;
+  if (k >= cap) continue;
   Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
   const int x = nr.next_double() < 0.5 ? 0 : 1;
   const double fx = x == 0 ? 1.0 : 3.0;
@@ -301,10 +416,12 @@ __global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, cons
   g[o] = gv;
   nsplit[o] = n;
   nerr[o] = err;
+  }
 }
 
 // bp == nullptr: every run is live (the two-point fixture).
-__global__ void k_recip_init(int runs, int repeats, int stride, const BatchPass* bp, RunState* st, int* active,
+__global__ void k_recip_init(int runs, int repeats, int stride, const __grid_constant__ BatchSet bs, RunState* st,
+                             int* active,
                              int* n_active, double* est, long long* cost, int* trunc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= runs) return;
@@ -315,10 +432,10 @@ __global__ void k_recip_init(int runs, int repeats, int stride, const BatchPass*
   s.truncated = 0;
   s.err = 0;
   bool live = true;
-  if (bp) {
-    const BatchPass& P = bp[j / stride];
+  if (bs.n) {
+    const BatchPass& P = bs.p[j / stride];
     const int e = (j % stride) / repeats;
-    live = e < P.n_ent && P.inc[e].valid && P.bound[e] > 0.0;
+    live = e < P.ps->n_ent && P.inc[e].valid && P.bound[e] > 0.0;
   }
   s.done = live ? 0 : 1;
   st[j] = s;
@@ -326,33 +443,6 @@ __global__ void k_recip_init(int runs, int repeats, int stride, const BatchPass*
   cost[j] = 0;
   trunc[j] = 0;
   if (live) active[atomicAdd(n_active, 1)] = j;
-}
-
-// Phase B: resume the DFS of every active run over its newly evaluated nodes.
-__global__ void k_recip_dfs(int repeats, int stride, long long cap, const BatchPass* bp, double fixed_bound,
-                            const int* active, const int* n_active, int chunk, RunState* st, const double* g,
-                            const long long* nsplit, const int* nerr, RecipFrame* frames, double* est,
-                            long long* cost, int* trunc, int* next, int* n_next, int* err) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= *n_active) return;
-  const int j = active[a];
-  RunState s = st[j];
-  s.avail = min(cap, s.avail + chunk);
-  const double B = bp ? bp[j / stride].bound[(j % stride) / repeats] : fixed_bound;
-  const size_t o = static_cast<size_t>(j) * cap;
-  const bool done = dfs_resume(s, g + o, nsplit + o, nerr + o, frames + o, B, cap);
-  st[j] = s;
-  if (!done) {
-    next[atomicAdd(n_next, 1)] = j;
-    return;
-  }
-  if (s.err) {
-    set_err(err, s.err);
-    return;
-  }
-  est[j] = s.ret;
-  cost[j] = s.cost;
-  trunc[j] = s.truncated;
 }
 
 // Phase B, warp-cooperative: one warp per active run. The DFS state machine of dfs_resume
@@ -363,8 +453,8 @@ __global__ void k_recip_dfs(int repeats, int stride, long long cap, const BatchP
 // instead of dependent global loads (the single-thread kernel's long-run tail). Same
 // arithmetic in the same order as dfs_resume, so estimates are bit-identical.
 template <int W>
-__global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride, long long cap, const BatchPass* bp,
-                                                        double fixed_bound, const int* active, const int* n_active,
+__global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride, long long cap,
+                                                        const __grid_constant__ BatchSet bs, double fixed_bound, const int* active, const int* n_active,
                                                         int chunk, RunState* st, const double* g,
                                                         const long long* nsplit, const int* nerr, RecipFrame* frames,
                                                         double* est, long long* cost, int* trunc, int* next,
@@ -374,12 +464,13 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
   __shared__ long long s_rem[4][W];
   __shared__ signed char s_sgn[4][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long a = static_cast<long long>(blockIdx.x) * 4 + warp;
-  if (a >= *n_active) return;  // warp-uniform
+  const int n_act = *n_active;
+  for (long long a = static_cast<long long>(blockIdx.x) * 4 + warp; a < n_act;
+       a += static_cast<long long>(gridDim.x) * 4) {  // warp-uniform
   const int j = active[a];
   RunState s = st[j];
   s.avail = min(cap, s.avail + chunk);
-  const double B = bp ? bp[j / stride].bound[(j % stride) / repeats] : fixed_bound;
+  const double B = bs.n ? bs.p[j / stride].bound[(j % stride) / repeats] : fixed_bound;
   const size_t o = static_cast<size_t>(j) * cap;
   const double* G = g + o;
   const long long* N = nsplit + o;
@@ -485,30 +576,32 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
       F[i] = RecipFrame{sa[sl], static_cast<double>(sg[sl]), sr[sl]};
     }
   }
-  if (lane != 0) return;
-  st[j] = s;
-  if (!done) {
-    next[atomicAdd(n_next, 1)] = j;
-    return;
+  if (lane == 0) {
+    st[j] = s;
+    if (!done) {
+      next[atomicAdd(n_next, 1)] = j;
+    } else if (s.err) {
+      set_err(err, s.err);
+    } else {
+      est[j] = s.ret;
+      cost[j] = s.cost;
+      trunc[j] = s.truncated;
+    }
   }
-  if (s.err) {
-    set_err(err, s.err);
-    return;
+  __syncwarp();
   }
-  est[j] = s.ret;
-  cost[j] = s.cost;
-  trunc[j] = s.truncated;
 }
 
 // Per entry: mean and second moment of its runs, validity (proxy.cpp:409-427); per bucket
 // the estimate sums in pool order; the kept list and the per-label lists in pool order
 // (proxy.cpp:729-735); then the stats snapshot Stage 2 of this pass reads. One block.
-__global__ void k_pool_finish(int n_ent, int repeats, IncHdr* inc, const double* bound, const double* est,
+__global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, const double* est,
                               const int* trunc, double* sum_est, double* sum_sq, long long* est_cnt, int* touched,
                               long long* diag, int* diag_touched, int* kept, int* label_start, int* label_list,
                               PassState* ps, double* snap_sum, double* snap_sq, long long* snap_cnt,
                               const double* max_ratio, const long long* ratio_cnt, double* snap_max,
                               long long* snap_rcnt) {
+  const int n_ent = ps->n_ent;
   extern __shared__ int smi[];  // [n_ent] valid flags, [kS] label counts
   int* ok = smi;
   int* lcount = smi + n_ent;
@@ -609,7 +702,10 @@ __global__ void k_pool_finish(int n_ent, int repeats, IncHdr* inc, const double*
 __global__ void k_fold_diag(const long long* sdiag, const int* stouched, const PassState* ps, long long* diag,
                             int* touched, unsigned long long* kept_total) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b == 0) atomicAdd(kept_total, static_cast<unsigned long long>(ps->n_kept));
+  if (b == 0) {
+    atomicAdd(kept_total, static_cast<unsigned long long>(ps->n_kept));
+    atomicAdd(kept_total + 1, static_cast<unsigned long long>(ps->raw));
+  }
   if (b >= kBuckets) return;
   for (int k = 2; k < 5; ++k) diag[b * 5 + k] += sdiag[b * 5 + k];
   if (stouched[b]) touched[b] = 1;

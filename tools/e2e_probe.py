@@ -20,3 +20,10 @@ for trial in range(3):
     r.close()
     t3 = time.perf_counter()
     print(f"trial {trial}: create {1e3*(t1-t0):.1f} ms, passes {1e3*tr:.1f} ms, mean readback {1e3*tm:.1f} ms, destroy {1e3*(t3-t2):.1f} ms")
+
+# the public API path bench.py times (pipelined pass_done callback)
+from paper_2503_23412_b200.render import render_proxy_bdpt
+for trial in range(3):
+    t0 = time.perf_counter()
+    img = render_proxy_bdpt(sc, 16, 2000 + trial, p, pass_done=lambda d, im: True)
+    print(f"render_proxy_bdpt trial {trial}: {1e3 * (time.perf_counter() - t0):.1f} ms")
