@@ -74,6 +74,16 @@ struct pxg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;   // Stage 2 (and everything else)
   cudaStream_t stream1 = nullptr;  // Stage 1 of the next pass
+  cudaStream_t stream_t = nullptr;  // Stage 2a: eye + light sub-path traces, one pass ahead
+  // sub-path vertex pools, double-buffered by pass parity so the traces of pass p+1 run
+  // while the connections / proxy connection of pass p read pass p's pools
+  PV* eye_buf[2] = {nullptr, nullptr};
+  PV* light_buf[2] = {nullptr, nullptr};
+  int* neye_buf[2] = {nullptr, nullptr};
+  int* nlight_buf[2] = {nullptr, nullptr};
+  cudaEvent_t trace_done[2] = {nullptr, nullptr};  // Stage 2a of the buffer's pass finished
+  cudaEvent_t paths_free[2] = {nullptr, nullptr};  // Stage 2b finished reading the buffer
+  RayQueue qP, qQ;  // proxy-wavefront queues (qA / qB belong to the traces)
   SceneHost host;
   pxg_params P{};
   pxg_shard shard{};
@@ -220,6 +230,7 @@ struct pxg_ctx {
   ~pxg_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     if (stream1) cudaStreamSynchronize(stream1);
+    if (stream_t) cudaStreamSynchronize(stream_t);
     for (void* p : allocs) cudaFreeAsync(p, stream);
     if (stream) cudaStreamSynchronize(stream);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
@@ -233,6 +244,9 @@ struct pxg_ctx {
         if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (stream1) cudaStreamDestroy(stream1);
+    if (stream_t) cudaStreamDestroy(stream_t);
+    for (cudaEvent_t e : {trace_done[0], trace_done[1], paths_free[0], paths_free[1]})
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -506,10 +520,41 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
 }
 
 // Stage 2 of `pass` on `stream` (proxy.cpp:738-827), reading pool slot `sl`.
+// Stage 2 of `pass`, split in two stream-ordered halves (proj/src/proxy.cpp:738-827):
+//   2a on stream_t: eye then light sub-paths of every pixel (the pixel's Rng stream continues
+//      from pass to pass, so traces run in pass order on their own stream; they never read
+//      Stage 1), into the vertex pools of buffer pass & 1;
+//   2b on stream:   connections + MIS, proxy connection, gate + film, gamma, in pass order.
+// 2a(p+1) overlaps 2b(p); 2a(p+2) waits until 2b(p) has released the buffer.
 void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
-  cudaStream_t st = c->stream;
+  cudaStream_t st = c->stream, tt = c->stream_t;
   const int T = 128;
+  const int b = pass & 1;
+  c->d_eye = c->eye_buf[b];
+  c->d_light = c->light_buf[b];
+  c->d_neye = c->neye_buf[b];
+  c->d_nlight = c->nlight_buf[b];
   HostProbe hp(st);
+  // ---- 2a
+  if (c->measure) CK(cudaStreamSynchronize(st));  // measurement: no 2a / 2b overlap
+  CK(cudaStreamWaitEvent(tt, c->paths_free[b], 0));
+  CK(cudaEventRecord(c->ev[1], tt));
+  {
+    PathSet E{c->d_eye, c->d_neye, c->d_ctr, c->d_ebeta, c->d_epdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth + 1, 1};
+    trace_paths(c, E, c->qA, c->qB, tt);
+    PathSet L{c->d_light, c->d_nlight, c->d_ctr, c->d_lbeta, c->d_lpdf, c->seed,
+              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth - 1, 0};
+    trace_paths(c, L, c->qA, c->qB, tt);
+    if (record_prims) {
+      k_record_prims<<<blocks(c->n, T), T, 0, tt>>>(c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
+                                                   c->max_depth, c->d_eye_prims, c->d_light_prims);
+      ++c->launches;
+    }
+  }
+  CK(cudaEventRecord(c->ev[4], tt));
+  CK(cudaEventRecord(c->trace_done[b], tt));
+  // ---- 2b
   CK(cudaEventRecord(c->ev[0], st));
   if (c->proxy_on) {
     CK(cudaStreamWaitEvent(st, sl.s1_done, 0));
@@ -517,50 +562,17 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
                                                        c->d_diag_touched, c->d_kept_total);
     ++c->launches;
   }
-  CK(cudaEventRecord(c->ev[1], st));
-  {
-    PathSet E{c->d_eye, c->d_neye, c->d_ctr, c->d_ebeta, c->d_epdf, c->seed,
-              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth + 1, 1};
-    trace_paths(c, E, c->qA, c->qB, st);
-    PathSet L{c->d_light, c->d_nlight, c->d_ctr, c->d_lbeta, c->d_lpdf, c->seed,
-              static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth - 1, 0};
-    trace_paths(c, L, c->qA, c->qB, st);
-    if (record_prims) {
-      k_record_prims<<<blocks(c->n, T), T, 0, st>>>(c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
-                                                   c->max_depth, c->d_eye_prims, c->d_light_prims);
-      ++c->launches;
-    }
-  }
-  CK(cudaEventRecord(c->ev[4], st));
+  CK(cudaStreamWaitEvent(st, c->trace_done[b], 0));
   hp.mark("trace");
   connections(c, c->proxy_on, sl);
   CK(cudaEventRecord(c->ev[5], st));
   hp.mark("connect");
-  Stage2 P;
-  P.S = c->S;
-  P.M = c->M;
-  P.st = StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt};
-  P.eye = c->d_eye;
-  P.light = c->d_light;
-  P.n_eye = c->d_neye;
-  P.n_light = c->d_nlight;
-  P.ctr = c->d_ctr;
-  P.bdpt = c->d_bdpt;
-  P.eye_prims = c->d_eye_prims;
-  P.light_prims = c->d_light_prims;
-  P.n = c->n;
-  P.row0 = c->row0;
-  P.width = c->width;
-  P.height = c->height;
-  P.max_depth = c->max_depth;
-  P.seed = c->seed;
-  P.record_prims = record_prims ? 1 : 0;
   if (c->proxy_on) {
     ProxCtx C{c->S, c->M, StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt}, c->d_eye, c->d_neye,
               c->n, c->row0, c->width, c->max_depth, c->seed, sl.inc, sl.prefix, sl.label_start, sl.label_list,
               c->d_gamma, sl.ps};
     ProxWave& W = c->pw;
-    RayQueue in = c->qA, out = c->qB;
+    RayQueue in = c->qP, out = c->qQ;
     CK(cudaMemsetAsync(in.count, 0, sizeof(int), st));
     k_pxw_select<<<blocks(c->n, T), T, 0, st>>>(C, W, pass, c->n_px_total, c->d_prox, in);
     for (int step = 0; step < 4; ++step) {
@@ -582,6 +594,7 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
     k_pxw_mis<<<blocks(c->n, T), T, 0, st>>>(C, W, c->d_prox);
     c->launches += 13;
   }
+  CK(cudaEventRecord(c->paths_free[b], st));  // last reader of this pass's vertex pools
   CK(cudaEventRecord(c->ev[6], st));
   hp.mark("proxy");
   k_gate<<<blocks(c->n_cells, 64), 64, 0, st>>>(
@@ -629,6 +642,7 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   c->launches = 0;
   CK(cudaEventRecord(c->ev_call[0], c->stream));
   CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
+  CK(cudaStreamWaitEvent(c->stream_t, c->ev_call[0], 0));
   // The first batch of a context is one pass: nothing can overlap it, so a short first
   // batch lets Stage 2 start after one pass of Stage 1 (the pipeline fill of the per-call
   // render_proxy_bdpt path). Batch composition does not change any result.
@@ -766,6 +780,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       int lo = 0, hi = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CK(cudaStreamCreateWithPriority(&c->stream1, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithFlags(&c->stream_t, cudaStreamNonBlocking));
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
@@ -839,10 +854,18 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->M.bmax = S.bbox_max;
     // stage-2 buffers
     const size_t n = c->n;
-    c->d_eye = c->alloc<PV>(n * (c->max_depth + 1));
-    c->d_light = c->alloc<PV>(n * std::max(c->max_depth - 1, 1));
-    c->d_neye = c->zeros<int>(n);
-    c->d_nlight = c->zeros<int>(n);
+    for (int k = 0; k < 2; ++k) {
+      c->eye_buf[k] = c->alloc<PV>(n * (c->max_depth + 1));
+      c->light_buf[k] = c->alloc<PV>(n * std::max(c->max_depth - 1, 1));
+      c->neye_buf[k] = c->zeros<int>(n);
+      c->nlight_buf[k] = c->zeros<int>(n);
+      CK(cudaEventCreateWithFlags(&c->trace_done[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->paths_free[k], cudaEventDisableTiming));
+    }
+    c->d_eye = c->eye_buf[0];
+    c->d_light = c->light_buf[0];
+    c->d_neye = c->neye_buf[0];
+    c->d_nlight = c->nlight_buf[0];
     c->d_ctr = c->zeros<unsigned>(n);
     c->d_bdpt = c->zeros<double>(3 * n);
     c->d_val = c->zeros<double>(3 * n);
@@ -899,6 +922,8 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->n_walks = c->shard.walk_end - c->shard.walk_begin;
     c->qA = make_queue(c, n);
     c->qB = make_queue(c, n);
+    c->qP = make_queue(c, n);
+    c->qQ = make_queue(c, n);
     {
       size_t need = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, need, c->conn.count, c->conn.offset, static_cast<int>(n + 1), c->stream);

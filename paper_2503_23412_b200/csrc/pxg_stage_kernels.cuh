@@ -750,23 +750,6 @@ __global__ void k_gamma_rows(const double* accum, double* rows) {
 }
 
 // ------------------------------------------------------------------ Stage 2 kernels
-struct Stage2 {
-  SceneView S;
-  Mapper M;
-  StatsView st;
-  PV* eye;
-  PV* light;
-  int* n_eye;
-  int* n_light;
-  unsigned* ctr;
-  double* bdpt;  // [n*3]
-  int* eye_prims;
-  int* light_prims;
-  int n, row0, width, height, max_depth;
-  uint64_t seed;
-  int record_prims;
-};
-
 __global__ void k_record_prims(const PV* eye, const int* n_eye, const PV* light, const int* n_light, int n,
                                int max_depth, int* eye_prims, int* light_prims) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

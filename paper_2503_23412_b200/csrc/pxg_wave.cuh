@@ -130,7 +130,7 @@ __global__ void k_light_start(SceneView S, PathSet P, RayQueue Q) {
 }
 
 // One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
-__global__ void k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
+__global__ void __launch_bounds__(128, 4) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *in.count) return;
   const int i = in.path[j];
@@ -272,7 +272,7 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* 
 constexpr int kRefill = 4;  // refill a warp's idle lanes once at least this many are idle
 
 template <bool kAny>
-__global__ void __launch_bounds__(128) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
+__global__ void __launch_bounds__(128, 8) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int total = *Q.count;
