@@ -13,7 +13,6 @@ cap() {  # name regex skip
   if [ "$1" = trav ]; then cp /tmp/$1.ncu-rep gpurun_out/prof/; fi
 }
 cap trav k_trav_persistent 40
-cap dfs k_recip_dfs_warp 9
 cap eval k_recip_eval 2
 cap shade k_shade 40
 # gpurun copies back at most 64 MiB
