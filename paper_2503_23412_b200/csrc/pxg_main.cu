@@ -84,6 +84,10 @@ struct pxg_ctx {
   cudaEvent_t trace_done[2] = {nullptr, nullptr};  // Stage 2a of the buffer's pass finished
   cudaEvent_t paths_free[2] = {nullptr, nullptr};  // Stage 2b finished reading the buffer
   RayQueue qP, qQ;  // proxy-wavefront queues (qA / qB belong to the traces)
+  RayQueue qPS;     // proxy-connection shadow rays (qS belongs to the connections)
+  PathCache pcache_buf[2];  // per-sub-path MIS step caches, double-buffered like the pools
+  cudaStream_t stream_p = nullptr;  // Stage 2b': proxy connection, forked from the pass
+  cudaEvent_t proxy_done = nullptr, gamma_done = nullptr;
   SceneHost host;
   pxg_params P{};
   pxg_shard shard{};
@@ -231,6 +235,7 @@ struct pxg_ctx {
     if (stream) cudaStreamSynchronize(stream);
     if (stream1) cudaStreamSynchronize(stream1);
     if (stream_t) cudaStreamSynchronize(stream_t);
+    if (stream_p) cudaStreamSynchronize(stream_p);
     for (void* p : allocs) cudaFreeAsync(p, stream);
     if (stream) cudaStreamSynchronize(stream);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
@@ -245,6 +250,9 @@ struct pxg_ctx {
     if (stream) cudaStreamDestroy(stream);
     if (stream1) cudaStreamDestroy(stream1);
     if (stream_t) cudaStreamDestroy(stream_t);
+    if (stream_p) cudaStreamDestroy(stream_p);
+    for (cudaEvent_t e : {proxy_done, gamma_done})
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {trace_done[0], trace_done[1], paths_free[0], paths_free[1]})
       if (e) cudaEventDestroy(e);
   }
@@ -351,7 +359,6 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
     k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
   }
   k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
-  k_path_factors<<<blocks(n, T), T, 0, st>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, n, c->pcache);
   k_conn_mis<<<blocks(slots, T), T, 0, st>>>(c->S, c->M,
                                              StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
                                              use_stats ? 1 : 0, c->d_eye, c->d_light, n, C, c->pcache);
@@ -534,6 +541,7 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
   c->d_light = c->light_buf[b];
   c->d_neye = c->neye_buf[b];
   c->d_nlight = c->nlight_buf[b];
+  c->pcache = c->pcache_buf[b];
   HostProbe hp(st);
   // ---- 2a
   if (c->measure) CK(cudaStreamSynchronize(st));  // measurement: no 2a / 2b overlap
@@ -551,6 +559,10 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
                                                    c->max_depth, c->d_eye_prims, c->d_light_prims);
       ++c->launches;
     }
+    // sub-path-only MIS step densities (used by the connections of this pass)
+    k_path_factors<<<blocks(c->n, T), T, 0, tt>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
+                                                  c->pcache);
+    ++c->launches;
   }
   CK(cudaEventRecord(c->ev[4], tt));
   CK(cudaEventRecord(c->trace_done[b], tt));
@@ -564,38 +576,50 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
   }
   CK(cudaStreamWaitEvent(st, c->trace_done[b], 0));
   hp.mark("trace");
+  // ---- 2b': the proxy connection forks here (it reads the eye sub-paths, the pool slot and
+  // gamma, never the connections) and joins before the gate
+  cudaStream_t sp = c->stream_p;
+  if (c->proxy_on) {
+    CK(cudaEventRecord(c->proxy_done, st));  // fork point: s1_done and trace_done already waited
+    CK(cudaStreamWaitEvent(sp, c->proxy_done, 0));
+    CK(cudaStreamWaitEvent(sp, c->gamma_done, 0));  // gamma of the previous pass
+  }
   connections(c, c->proxy_on, sl);
   CK(cudaEventRecord(c->ev[5], st));
   hp.mark("connect");
   if (c->proxy_on) {
+    if (c->measure) CK(cudaStreamWaitEvent(sp, c->ev[5], 0));  // measurement: no overlap with timed launches
     ProxCtx C{c->S, c->M, StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt}, c->d_eye, c->d_neye,
               c->n, c->row0, c->width, c->max_depth, c->seed, sl.inc, sl.prefix, sl.label_start, sl.label_list,
               c->d_gamma, sl.ps};
     ProxWave& W = c->pw;
     RayQueue in = c->qP, out = c->qQ;
-    CK(cudaMemsetAsync(in.count, 0, sizeof(int), st));
-    k_pxw_select<<<blocks(c->n, T), T, 0, st>>>(C, W, pass, c->n_px_total, c->d_prox, in);
+    CK(cudaMemsetAsync(in.count, 0, sizeof(int), sp));
+    k_pxw_select<<<blocks(c->n, T), T, 0, sp>>>(C, W, pass, c->n_px_total, c->d_prox, in);
     for (int step = 0; step < 4; ++step) {
       int* fetch = c->d_trav_next + 3;
-      CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
-      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
-      CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
-      k_pxw_retrace<<<blocks(c->n, T), T, 0, st>>>(C, W, pass, c->n_px_total, in, out);
+      CK(cudaMemsetAsync(fetch, 0, sizeof(int), sp));
+      k_trav_persistent<false><<<c->trav_blocks, 128, 0, sp>>>(c->S, in, fetch);
+      CK(cudaMemsetAsync(out.count, 0, sizeof(int), sp));
+      k_pxw_retrace<<<blocks(c->n, T), T, 0, sp>>>(C, W, pass, c->n_px_total, in, out);
       std::swap(in, out);
     }
-    CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
-    k_pxw_value<<<blocks(c->n, T), T, 0, st>>>(C, W, c->qS);
+    CK(cudaMemsetAsync(c->qPS.count, 0, sizeof(int), sp));
+    k_pxw_value<<<blocks(c->n, T), T, 0, sp>>>(C, W, c->qPS);
     {
       int* fetch = c->d_trav_next + 4;
-      CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
-      k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
+      CK(cudaMemsetAsync(fetch, 0, sizeof(int), sp));
+      k_trav_persistent<true><<<c->trav_blocks, 128, 0, sp>>>(c->S, c->qPS, fetch);
     }
-    k_pxw_occlusion<<<blocks(static_cast<long long>(c->n) * kMaxLight, T), T, 0, st>>>(W, c->qS);
-    k_pxw_mis<<<blocks(c->n, T), T, 0, st>>>(C, W, c->d_prox);
+    k_pxw_occlusion<<<blocks(static_cast<long long>(c->n) * kMaxLight, T), T, 0, sp>>>(W, c->qPS);
+    k_pxw_mis<<<blocks(c->n, T), T, 0, sp>>>(C, W, c->d_prox);
     c->launches += 13;
+    CK(cudaEventRecord(c->ev[6], sp));
+    CK(cudaEventRecord(c->proxy_done, sp));
+    CK(cudaStreamWaitEvent(st, c->proxy_done, 0));  // join
   }
   CK(cudaEventRecord(c->paths_free[b], st));  // last reader of this pass's vertex pools
-  CK(cudaEventRecord(c->ev[6], st));
+  if (!c->proxy_on) CK(cudaEventRecord(c->ev[6], st));
   hp.mark("proxy");
   k_gate<<<blocks(c->n_cells, 64), 64, 0, st>>>(
       c->n_cells, c->grid_w, c->row0, c->rows, c->width, pass, c->P.gate_high, c->P.gate_low, c->P.gate_threshold,
@@ -614,6 +638,7 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
     ++c->gamma_iter;
     if (c->gamma_iter >= c->P.freeze_iteration) c->gamma_learning = false;
   }
+  CK(cudaEventRecord(c->gamma_done, st));
   CK(cudaEventRecord(c->ev[7], st));
   CK(cudaEventRecord(sl.s2_done, st));
   hp.mark("gate+gamma");
@@ -781,6 +806,9 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CK(cudaStreamCreateWithPriority(&c->stream1, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithFlags(&c->stream_t, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->stream_p, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->proxy_done, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->gamma_done, cudaEventDisableTiming));
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
@@ -910,13 +938,16 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->conn.n_live = c->zeros<int>(1);
     {
       const size_t L = static_cast<size_t>(kMaxPath);
-      c->pcache.LF = c->zeros<double>(L * n);
-      c->pcache.LR = c->zeros<double>(L * n);
-      c->pcache.EF = c->zeros<double>(L * n);
-      c->pcache.ER = c->zeros<double>(L * n);
-      c->pcache.ld = c->zeros<double>(n);
-      c->pcache.ld_ok = c->zeros<int>(n);
-      c->pcache.n = static_cast<int>(n);
+      for (PathCache& pc : c->pcache_buf) {
+        pc.LF = c->zeros<double>(L * n);
+        pc.LR = c->zeros<double>(L * n);
+        pc.EF = c->zeros<double>(L * n);
+        pc.ER = c->zeros<double>(L * n);
+        pc.ld = c->zeros<double>(n);
+        pc.ld_ok = c->zeros<int>(n);
+        pc.n = static_cast<int>(n);
+      }
+      c->pcache = c->pcache_buf[0];
     }
     c->qS = make_queue(c, slots);
     c->n_walks = c->shard.walk_end - c->shard.walk_begin;
@@ -924,6 +955,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->qB = make_queue(c, n);
     c->qP = make_queue(c, n);
     c->qQ = make_queue(c, n);
+    c->qPS = make_queue(c, n * kMaxLight);
     {
       size_t need = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, need, c->conn.count, c->conn.offset, static_cast<int>(n + 1), c->stream);

@@ -131,6 +131,7 @@ __device__ __forceinline__ double rec_hit(const PrimRec* __restrict__ rp, const 
 
 struct RayF {
   float ox, oy, oz, ix, iy, iz;
+  float nx, ny, nz;  // -o * inv(d) per axis: slab distance = fma(plane, inv, n)
 };
 
 __device__ __forceinline__ RayF make_rayf(const V3& o, const V3& d) {
@@ -147,15 +148,21 @@ __device__ __forceinline__ RayF make_rayf(const V3& o, const V3& d) {
   r.ix = 1.0f / dx;
   r.iy = 1.0f / dy;
   r.iz = 1.0f / dz;
+  r.nx = -r.ox * r.ix;
+  r.ny = -r.oy * r.iy;
+  r.nz = -r.oz * r.iz;
   return r;
 }
 
 // Slab test in fp32 (boxes padded outward on the host, directions never exactly zero).
 __device__ __forceinline__ bool box_f(const float* lo, const float* hi, const RayF& r, float tmax,
                                       float& tnear) {
-  float tx0 = (lo[0] - r.ox) * r.ix, tx1 = (hi[0] - r.ox) * r.ix;
-  float ty0 = (lo[1] - r.oy) * r.iy, ty1 = (hi[1] - r.oy) * r.iy;
-  float tz0 = (lo[2] - r.oz) * r.iz, tz1 = (hi[2] - r.oz) * r.iz;
+  // one FFMA per slab plane (explicit: the file is built with --fmad=false for the fp64
+  // path math). The cancellation error of lo*inv - o*inv is ~|o| * 2^-24 along the ray,
+  // far inside the boxes' 1e-5 x scene-scale padding, so the test stays conservative.
+  float tx0 = __fmaf_rn(lo[0], r.ix, r.nx), tx1 = __fmaf_rn(hi[0], r.ix, r.nx);
+  float ty0 = __fmaf_rn(lo[1], r.iy, r.ny), ty1 = __fmaf_rn(hi[1], r.iy, r.ny);
+  float tz0 = __fmaf_rn(lo[2], r.iz, r.nz), tz1 = __fmaf_rn(hi[2], r.iz, r.nz);
   float t0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
   float t1 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
   tnear = t0;
