@@ -172,8 +172,9 @@ int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, i
 /* Device timeline of the last pxg_render_passes call (ms, CUDA events on the context's
  * stream): t[0] stage 1 (pool walks, selection, probes, reciprocal runs, incl. the host
  * round trip of the selection), t[1] reciprocal runs alone, t[2] sub-path trace,
- * t[3] connections + MIS, t[4] proxy connection, t[5] gate + film, t[6] the whole call
- * (first pass start to last pass end, including host gaps), t[7] reserved.
+ * t[3] connections + MIS, t[4] proxy connection, t[5] gate + film (t[2..5]: the last pass
+ * of the call; the streams overlap, so these are spans, not exclusive times), t[6] the
+ * whole call (first pass start to the end of all work it enqueued), t[7] reserved.
  * counts[0] = kernel launches, counts[1] reserved. t holds 8 doubles. */
 int pxg_read_timing(pxg_ctx* ctx, double* t, long long* counts);
 

@@ -450,7 +450,7 @@ void stage1_front(pxg_ctx* c, int pass, PoolSlot& sl) {
                                                       sl.inc, sl.prefix);
     k_pool_probes<<<blocks(4 * budget, 64), 64, 0, st>>>(c->S, c->seed, pass, sl.ps, sl.inc, sl.prefix, c->d_probe,
                                                          c->d_probe_ok, R);
-    k_pool_bounds<<<1, 512, 2 * sizeof(double) * budget, st>>>(sl.ps, sl.inc, c->d_probe, c->d_probe_ok,
+    k_pool_bounds<<<1, 512, (6 * sizeof(double) + 5 * sizeof(int)) * budget, st>>>(sl.ps, sl.inc, c->d_probe, c->d_probe_ok,
                                                                c->d_max_ratio, c->d_ratio_cnt, c->d_touched,
                                                                sl.bound, c->d_err);
     c->launches += 3;
@@ -512,7 +512,8 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
   for (int b = 0; b < L; ++b) {
     PoolSlot& sl = c->slot_of(p0 + b);
     const size_t o = static_cast<size_t>(b) * stride;
-    k_pool_finish<<<1, 512, sizeof(int) * (std::max(c->P.pool_budget, 0) + kS), st>>>(
+    k_pool_finish<<<1, 512, (sizeof(double) + 3 * sizeof(int)) * std::max(c->P.pool_budget, 0) + sizeof(int) * kS,
+                    st>>>(
         R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq,
         c->d_est_cnt, c->d_touched, sl.diag, sl.diag_touched, sl.kept, sl.label_start, sl.label_list, sl.ps,
         sl.snap_sum, sl.snap_sq, sl.snap_cnt, c->d_max_ratio, c->d_ratio_cnt, sl.snap_max, sl.snap_rcnt);
@@ -668,46 +669,55 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   CK(cudaEventRecord(c->ev_call[0], c->stream));
   CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
   CK(cudaStreamWaitEvent(c->stream_t, c->ev_call[0], 0));
-  // The first batch of a context is one pass: nothing can overlap it, so a short first
-  // batch lets Stage 2 start after one pass of Stage 1 (the pipeline fill of the per-call
-  // render_proxy_bdpt path). Batch composition does not change any result.
-  static const int first_batch = std::getenv("PXG_FIRST_BATCH") ? std::atoi(std::getenv("PXG_FIRST_BATCH")) : 1;
+  // Pipeline fill: the first batches of a context grow geometrically (passes [0,1), [1,3),
+  // [3,7), [7,15), then c->batch at a time), so Stage 2 starts after one pass of Stage 1
+  // instead of a whole batch (the per-call render_proxy_bdpt path). Batch composition does
+  // not change any result.
   auto batch_len = [&](int p0) {
-    int L = p0 == 0 ? std::max(1, std::min(c->batch, first_batch)) : c->batch;
+    int L = p0 < c->batch ? std::min(c->batch, p0 + 1) : c->batch;
     if (c->pass_limit >= 0) L = std::min(L, std::max(1, c->pass_limit - p0));
     return L;
   };
-  int left = npass;
-  while (left > 0) {
+  // Look-ahead: after every Stage-2 enqueue, Stage 1 is launched for every batch starting
+  // before passes_done + batch (within the pass limit), so each batch has about a batch of
+  // Stage-2 time to finish. Launched batches never reach passes_done + 2 * batch - 1: the
+  // slot ring keeps the last rendered pass's slot for the dump / diagnostics readers.
+  auto launch_ahead = [&]() {
+    if (!c->proxy_on) return;
+    for (;;) {
+      const int q = c->passes_done, nb = c->next_batch;
+      if (nb >= q + c->batch) break;
+      if (c->pass_limit >= 0 && nb >= c->pass_limit) break;
+      const int L = std::min(batch_len(nb), q + 2 * c->batch - 1 - nb);
+      if (L <= 0) break;
+      for (int i = 0; i < L; ++i) read_stage1_timing(c, c->slot_of(nb + i));
+      run_stage1_batch(c, nb, L);
+    }
+  };
+  static const bool overlap = std::getenv("PXG_NO_OVERLAP") == nullptr;
+  for (int k = 0; k < npass; ++k) {
     const int p = c->passes_done;
-    if (c->proxy_on && c->slot_of(p).pass != p) run_stage1_batch(c, p, batch_len(p));
+    if (c->proxy_on && c->slot_of(p).pass != p) {  // first call, or the look-ahead stopped at the limit
+      c->next_batch = p;
+      run_stage1_batch(c, p, batch_len(p));
+    }
+    if (overlap && !c->measure) launch_ahead();
     // measurement mode: the streams are serialised so every timed traversal launch has the
     // GPU to itself (its duration is the kernel's, not a share of the Stage-1 overlap)
     if (c->measure) CK(cudaStreamSynchronize(c->stream1));
-    // Stage 2 of the passes of this batch, enqueued without host synchronisation
-    const int stop = c->proxy_on ? c->slot_of(p).batch_end : p + left;
-    const int m = std::min(left, stop - p);
-    for (int k = 0; k < m; ++k) {
-      const int pp = c->passes_done;
-      enqueue_stage2(c, pp, c->slot_of(pp), record_last && left - k == 1);
-      CK(cudaGetLastError());
-      ++c->passes_done;
+    enqueue_stage2(c, p, c->slot_of(p), record_last && k == npass - 1);
+    CK(cudaGetLastError());
+    ++c->passes_done;
+    if (!overlap || c->measure) {
+      CK(cudaStreamSynchronize(c->stream));
+      launch_ahead();
+    } else {
+      launch_ahead();
     }
-    left -= m;
-    static const bool overlap = std::getenv("PXG_NO_OVERLAP") == nullptr;
-    if (!overlap || c->measure) CK(cudaStreamSynchronize(c->stream));
-    // look-ahead: Stage 1 of the next batch while Stage 2 of this one runs
-    // (launched as soon as Stage 2 of the current batch has been enqueued, so a caller that
-    // renders one pass per call gets the same pipeline as a bulk call)
-    if (c->proxy_on && (c->pass_limit < 0 || stop < c->pass_limit) &&
-        c->slot_of(stop).pass != stop) {
-      for (int q = 0; q < c->batch; ++q) read_stage1_timing(c, c->slot_of(stop + q));
-      run_stage1_batch(c, stop, batch_len(stop));
-    }
-    if (wait) {
-      CK(cudaEventSynchronize(c->ev[7]));
-      read_stage2_timing(c);
-    }
+  }
+  if (wait) {
+    CK(cudaEventSynchronize(c->ev[7]));
+    read_stage2_timing(c);  // the last pass of the call
   }
   if (!wait) return;  // asynchronous: the caller synchronises (snapshot / read)
   CK(cudaEventRecord(c->ev_call[2], c->stream1));
@@ -1008,7 +1018,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_ckey = c->alloc<unsigned long long>(c->cand_cap);
     c->d_cval = c->alloc<unsigned>(c->cand_cap);
     c->d_ccount = c->zeros<int>(1);
-    if (c->P.pool_budget > 4096) throw InvalidErr{"pxg: pool_budget above 4096 is not supported"};
+    if (c->P.pool_budget > 3072) throw InvalidErr{"pxg: pool_budget above 3072 is not supported"};
     {
       // device priority selection: 2 x budget expected keys below the first threshold
       int cap = 1024;
@@ -1017,6 +1027,11 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       c->sel_smem = static_cast<size_t>(cap) * (sizeof(unsigned long long) + sizeof(unsigned));
       CK(cudaFuncSetAttribute(k_pool_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(c->sel_smem)));
+      const int b = std::max(c->P.pool_budget, 0);
+      CK(cudaFuncSetAttribute(k_pool_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>((6 * sizeof(double) + 5 * sizeof(int)) * b)));
+      CK(cudaFuncSetAttribute(k_pool_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>((sizeof(double) + 3 * sizeof(int)) * b + sizeof(int) * kS)));
     }
     const int B = std::max(c->P.pool_budget, 1);
     const int R = std::max(c->P.recip_repeats, 1);

@@ -299,17 +299,28 @@ __global__ void k_pretrace(SceneView S, Mapper M, uint64_t seed, int n_paths, do
 // entry of each bucket then commits the bucket state. One block.
 __global__ void k_pool_bounds(const PassState* ps, const IncHdr* inc, const double* probe, const int* probe_ok,
                               double* max_ratio, long long* ratio_cnt, int* touched, double* bound, int* err) {
-  extern __shared__ double sm[];  // [n_ent] max, then [n_ent] touched flags (as double)
+  // shared: [n_ent] prefix max, [n_ent] touched flags, [4 n_ent] probes (doubles), then
+  // [n_ent] keys (-1 = invalid entry), [4 n_ent] probe flags (ints)
+  extern __shared__ double sm[];
   const int n_ent = ps->n_ent;
+  double* s_pr = sm + 2 * n_ent;
+  int* s_key = reinterpret_cast<int*>(s_pr + 4 * n_ent);
+  int* s_ok = s_key + n_ent;
+  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) s_key[k] = inc[k].valid ? inc[k].key : -1;
+  for (int t = threadIdx.x; t < 4 * n_ent; t += blockDim.x) {
+    s_ok[t] = probe_ok[t];
+    s_pr[t] = s_ok[t] ? probe[t] : 0.0;
+  }
+  __syncthreads();
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     const int key = inc[k].key;
     double m = max_ratio[key];
     int tch = touched[key];
     for (int k2 = 0; k2 <= k; ++k2) {
-      if (!inc[k2].valid || inc[k2].key != key) continue;
+      if (s_key[k2] != key) continue;
       for (int i = 0; i < 4; ++i) {
-        if (!probe_ok[k2 * 4 + i]) continue;
-        const double r = probe[k2 * 4 + i];
+        if (!s_ok[k2 * 4 + i]) continue;
+        const double r = s_pr[k2 * 4 + i];
         if (!isfinite(r) || r < 0.0) {
           set_err(err, kErrRatio);
           continue;
@@ -318,20 +329,20 @@ __global__ void k_pool_bounds(const PassState* ps, const IncHdr* inc, const doub
         tch = 1;
       }
     }
-    bound[k] = (inc[k].valid && tch) ? 2.0 * m : 0.0;
+    bound[k] = (s_key[k] >= 0 && tch) ? 2.0 * m : 0.0;
     sm[k] = m;
     sm[n_ent + k] = tch;
   }
   __syncthreads();
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
-    if (!inc[k].valid) continue;
-    const int key = inc[k].key;
+    const int key = s_key[k];
+    if (key < 0) continue;
     bool last = true;
     long long cnt = 0;
     for (int k2 = 0; k2 < n_ent; ++k2) {
-      if (!inc[k2].valid || inc[k2].key != key) continue;
+      if (s_key[k2] != key) continue;
       if (k2 > k) last = false;
-      for (int i = 0; i < 4; ++i) cnt += probe_ok[k2 * 4 + i];
+      for (int i = 0; i < 4; ++i) cnt += s_ok[k2 * 4 + i];
     }
     if (!last) continue;
     max_ratio[key] = sm[k];
@@ -602,13 +613,19 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
                               const double* max_ratio, const long long* ratio_cnt, double* snap_max,
                               long long* snap_rcnt) {
   const int n_ent = ps->n_ent;
-  extern __shared__ int smi[];  // [n_ent] valid flags, [kS] label counts
-  int* ok = smi;
-  int* lcount = smi + n_ent;
+  // shared: [n_ent] inverse_p (double), then [n_ent] valid flags, keys, labels, [kS] label counts
+  extern __shared__ double smd[];
+  double* s_inv = smd;
+  int* ok = reinterpret_cast<int*>(smd + n_ent);
+  int* s_key = ok + n_ent;
+  int* s_lab = s_key + n_ent;
+  int* lcount = s_lab + n_ent;
   for (int s = threadIdx.x; s < kS; s += blockDim.x) lcount[s] = 0;
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     IncHdr& h = inc[k];
     ok[k] = 0;
+    s_key[k] = h.key;
+    s_lab[k] = h.s_label;
     if (!h.valid) continue;
     const int key = h.key;
     diag_touched[key] = 1;
@@ -629,6 +646,7 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
         valid = true;
         h.inverse_p = mean;
         h.inverse_p_m2 = m2;
+        s_inv[k] = mean;
       }
     }
     atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 2]), static_cast<unsigned long long>(repeats));
@@ -639,10 +657,10 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
   // bucket sums in pool order (SubspaceStats::update_estimate, subspace.cpp:64-70)
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     if (!ok[k]) continue;
-    const int key = inc[k].key;
+    const int key = s_key[k];
     bool last = true;
     for (int k2 = k + 1; k2 < n_ent; ++k2)
-      if (ok[k2] && inc[k2].key == key) {
+      if (ok[k2] && s_key[k2] == key) {
         last = false;
         break;
       }
@@ -650,8 +668,8 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
     double se = sum_est[key], sq = sum_sq[key];
     long long cnt = est_cnt[key];
     for (int k2 = 0; k2 <= k; ++k2) {
-      if (!ok[k2] || inc[k2].key != key) continue;
-      const double m = inc[k2].inverse_p;
+      if (!ok[k2] || s_key[k2] != key) continue;
+      const double m = s_inv[k2];
       se += m;
       sq += m * m;
       ++cnt;
@@ -667,7 +685,7 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
     int pos = 0;
     for (int k2 = 0; k2 < k; ++k2) pos += ok[k2];
     kept[pos] = k;
-    atomicAdd(&lcount[inc[k].s_label], 1);
+    atomicAdd(&lcount[s_lab[k]], 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -683,10 +701,10 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
   __syncthreads();
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     if (!ok[k]) continue;
-    const int sl = inc[k].s_label;
+    const int sl = s_lab[k];
     int pos = label_start[sl];
     for (int k2 = 0; k2 < k; ++k2)
-      if (ok[k2] && inc[k2].s_label == sl) ++pos;
+      if (ok[k2] && s_lab[k2] == sl) ++pos;
     label_list[pos] = k;
   }
   __syncthreads();

@@ -141,6 +141,12 @@ PROXY_SCENES = {
     "glass_slab": (lambda: scenes.glass_slab(20), {"pretrace_paths": 4000, "light_walks": 4000}),
     "c1_small": (lambda: scenes.cornell_c1(40, max_depth=8), {"pretrace_paths": 4000, "light_walks": 8000}),
     "c2_small": (lambda: scenes.cornell_c2(40, max_depth=10), {"pretrace_paths": 4000, "light_walks": 8000}),
+    # device priority selection: raw >> budget (threshold bisection + bitonic sort path) ...
+    "c2_budget7": (lambda: scenes.cornell_c2(30, max_depth=10),
+                   {"pretrace_paths": 4000, "light_walks": 8000, "pool_budget": 7}),
+    # ... and budget > raw (every candidate kept; only the (walk, end) sort)
+    "c1_budget3000": (lambda: scenes.cornell_c1(30, max_depth=8),
+                      {"pretrace_paths": 4000, "light_walks": 6000, "pool_budget": 3000}),
 }
 
 
@@ -152,7 +158,7 @@ def test_proxy_render_matches_oracle(pxg, oracle, name):
     sc = make()
     o = oracle.OracleScene(sc.to_json())
     spp = 3
-    img_o, run = o.render(spp, 9, params=pd, threads=8, trace=True)
+    img_o, run = o.render(spp, 9, params=pd, threads=8, trace=True, pool_cap=max(400, pd.get("pool_budget", 400)))
     params = ProxyParams(**pd)
     with ProxyRenderer(sc, 9, params) as r:
         for p in range(spp):
@@ -186,6 +192,25 @@ def test_proxy_render_matches_oracle(pxg, oracle, name):
     assert np.allclose(g, run.gamma_rows, rtol=1e-6, atol=1e-12)
     assert np.allclose(img, img_o, rtol=1e-4, atol=1e-10) or \
         np.count_nonzero(~np.isclose(img, img_o, rtol=1e-4, atol=1e-10)) <= 3 * max(2, sc.n_px // 500)
+
+
+def test_pool_budget_edges(pxg, oracle):
+    """pool_budget 0 keeps nothing (the pass is plain BDPT with the gate's proxy share 0);
+    budgets above the device selection's capacity are rejected like a bad scene."""
+    from paper_2503_23412_b200._lib import PxgValidationError
+    sc = scenes.caustic_box(12)
+    pd = {"pretrace_paths": 2000, "light_walks": 2000, "pool_budget": 0}
+    o = oracle.OracleScene(sc.to_json())
+    img_o, run = o.render(2, 5, params=pd, threads=4, trace=True)
+    with ProxyRenderer(sc, 5, ProxyParams(**pd)) as r:
+        for p in range(2):
+            r.render_passes(1)
+            pool = r.dump_pool()
+            assert pool["n"] == 0 and pool["raw"] == run.pool_raw[p]
+        img = r.mean()
+    assert np.allclose(img, img_o, rtol=1e-9, atol=1e-12)
+    with pytest.raises(PxgValidationError):
+        ProxyRenderer(sc, 5, ProxyParams(pool_budget=3073))
 
 
 def test_pretrace_matches_oracle(pxg, oracle):

@@ -15,5 +15,5 @@ r.set_pass_limit(32)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 r.render_passes(n)
 t, cnt = r.timing()
-print("stage1 %.2f recip %.2f | per sampled pass: trace %.3f conn %.3f proxy %.3f gate %.3f | call %.2f ms (%.3f ms/pass) launches %d"
-      % (t[0], t[1], t[2] / 2, t[3] / 2, t[4] / 2, t[5] / 2, t[6], t[6] / n, cnt[0]))
+print("stage1 %.2f recip %.2f | last pass: trace %.3f conn %.3f proxy %.3f gate %.3f | call %.2f ms (%.3f ms/pass) launches %d"
+      % (t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[6] / n, cnt[0]))
