@@ -41,7 +41,8 @@ NODE_BYTES, PRIM_BYTES = 128, 80  # BvhNode4, PrimRec (csrc/pxg_scene.cuh)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=16)
+    # default: the timed passes 8..63 of C2's 64-spp render (BASELINE configs[1])
+    ap.add_argument("--steps", type=int, default=56)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -67,6 +68,8 @@ def config_json(cfg, sc, walks):
     return {"workload": f"{cfg}: BASELINE.json configs[{1 if cfg == 'C2' else 0}], {sc.camera.width}x{sc.camera.height}, "
                         f"max_depth {sc.settings.max_depth}, {walks} pool walks/pass, {sc.n_prims} prims, proxy on",
             "step": "1 progressive pass (1 sample per pixel)",
+            "spp": sc.settings.spp,
+            "window": "default: warm-up passes 0..7, timed passes 8..63 of the config's 64-spp render",
             "l2": "inputs larger than L2: per-pass vertex pools/queues ~1 GB >> 126 MB L2 (scene itself L2-resident)"}
 
 
@@ -295,6 +298,7 @@ def run_ours(args):
     # (N > 1: render_proxy_bdpt_distributed, K passes per rank, NCCL all-reduce per round)
     e2e = None
     reads = [0]
+    spp_e2e = sc.settings.spp  # one full render call of the config (C2: 64 spp)
 
     def cb(done, img):
         reads[0] += img.nbytes
@@ -307,7 +311,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         reads[0] = 0
         t0 = time.perf_counter()
-        img = render_proxy_bdpt(sc, args.steps, seed + 2000, params, pass_done=cb, device=local)
+        img = render_proxy_bdpt(sc, spp_e2e, seed + 2000, params, pass_done=cb, device=local)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
     else:
@@ -317,18 +321,20 @@ def run_ours(args):
         dist.barrier()
         reads[0] = 0
         t0 = time.perf_counter()
-        img = render_proxy_bdpt_distributed(sc, args.steps * world, 2000, params, pass_done=cb, local_rank=local)
+        img = render_proxy_bdpt_distributed(sc, spp_e2e * world, 2000, params, pass_done=cb, local_rank=local)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         tt = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     if not args.quick:
-        d2h = (reads[0] + img.nbytes) / args.steps
-        e2e = {"value": round(W * H * args.steps * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
-               "h2d_bytes_per_step": int(scene_bytes(sc) / args.steps), "d2h_bytes_per_step": int(d2h),
-               "includes": "pxg_create (scene upload from host arrays, finalize, BVH build, pretrace) + K passes + "
-                           "running-mean read-back every pass (the reference's pass_done callback) + final image"}
+        d2h = (reads[0] + img.nbytes) / spp_e2e
+        e2e = {"value": round(W * H * spp_e2e * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(scene_bytes(sc) / spp_e2e), "d2h_bytes_per_step": int(d2h),
+               "spp": spp_e2e,
+               "includes": f"one full render call render_proxy_bdpt(scene, spp={spp_e2e}) per rank from host arrays: "
+                           "pxg_create (scene upload, finalize, BVH build, pretrace) + every pass + the running-mean "
+                           "read-back after every pass (the reference's pass_done callback) + the final image"}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:

@@ -110,10 +110,11 @@ int pxg_render_passes(pxg_ctx* ctx, int n);
  * look-ahead Stage 1 is started for pass >= limit. -1 (default) = unbounded. */
 int pxg_set_pass_limit(pxg_ctx* ctx, int limit);
 /* Pipelined progressive rendering: enqueue passes without waiting for them, snapshot the
- * running mean on the device after the enqueued passes (slot 0 or 1), and read a snapshot
- * back later (waits for it). A caller can hand pass p's mean to its pass_done callback
- * while pass p+1 already runs; stopping early returns the snapshot of pass p, which is
- * bitwise the image a p-pass render returns. */
+ * running mean on the device after the enqueued passes (slot 0 .. PXG_SNAPSHOT_SLOTS-1),
+ * and read a snapshot back later (waits for it). A caller can hand pass p's mean to its
+ * pass_done callback while passes p+1.. already run; stopping early returns the snapshot
+ * of pass p, which is bitwise the image a p-pass render returns. */
+#define PXG_SNAPSHOT_SLOTS 4
 int pxg_render_passes_async(pxg_ctx* ctx, int n);
 int pxg_snapshot_mean(pxg_ctx* ctx, int slot);
 int pxg_read_snapshot(pxg_ctx* ctx, int slot, double* rgb, int* passes_done);

@@ -178,12 +178,13 @@ struct pxg_ctx {
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
   ProxWave pw{};
-  double* d_snap[2] = {nullptr, nullptr};  // running-mean snapshots for pipelined pass_done
-  cudaEvent_t snap_ev[2] = {nullptr, nullptr};
-  int snap_passes[2] = {0, 0};
+  static constexpr int kSnap = PXG_SNAPSHOT_SLOTS;
+  double* d_snap[kSnap] = {};  // running-mean snapshots for the pipelined pass_done loop
+  cudaEvent_t snap_ev[kSnap] = {};
+  int snap_passes[kSnap] = {};
   double* h_pinned = nullptr;              // pinned staging for read-backs (process-wide cache)
   size_t pinned_bytes = 0;
-  int* h_err = nullptr;                    // [2] pinned error flags of the two snapshots
+  int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int dfs_blocks = 0;         // grid-stride warp-DFS grid
@@ -243,7 +244,7 @@ struct pxg_ctx {
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& e : snap_ev) if (e) cudaEventDestroy(e);
     if (h_pinned) pinned_release(h_pinned, pinned_bytes);
-    if (h_err) pinned_release(h_err, 2 * sizeof(int));
+    if (h_err) pinned_release(h_err, kSnap * sizeof(int));
     for (auto& sl : slot)
       for (cudaEvent_t e : {sl.s1_done, sl.s2_done, sl.t0, sl.t1, sl.r0, sl.r1})
         if (e) cudaEventDestroy(e);
@@ -667,8 +668,10 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   for (int k = 0; k < 8; ++k) c->stage_ms[k] = 0.0;
   c->launches = 0;
   CK(cudaEventRecord(c->ev_call[0], c->stream));
-  CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
-  CK(cudaStreamWaitEvent(c->stream_t, c->ev_call[0], 0));
+  if (wait) {  // a timed call: its work starts after the call's start event on every stream
+    CK(cudaStreamWaitEvent(c->stream1, c->ev_call[0], 0));
+    CK(cudaStreamWaitEvent(c->stream_t, c->ev_call[0], 0));
+  }  // (asynchronous calls must not serialise the streams: one call per pass in the pipeline)
   // Pipeline fill: the first batches of a context grow geometrically (passes [0,1), [1,3),
   // [3,7), [7,15), then c->batch at a time), so Stage 2 starts after one pass of Stage 1
   // instead of a whole batch (the per-call render_proxy_bdpt path). Batch composition does
@@ -920,14 +923,14 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->pw.value = c->zeros<double>(3 * n);
     c->pw.occl = c->zeros<int>(n);
     c->pw.lv = c->d_scratch;
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < pxg_ctx::kSnap; ++k) {
       c->d_snap[k] = c->alloc<double>(3 * n);
       CK(cudaEventCreateWithFlags(&c->snap_ev[k], cudaEventDisableTiming));
     }
     c->pinned_bytes = sizeof(double) * 3 * n;
     c->h_pinned = static_cast<double*>(pinned_acquire(c->pinned_bytes));
-    c->h_err = static_cast<int*>(pinned_acquire(2 * sizeof(int)));
-    c->h_err[0] = c->h_err[1] = 0;
+    c->h_err = static_cast<int*>(pinned_acquire(pxg_ctx::kSnap * sizeof(int)));
+    for (int k = 0; k < pxg_ctx::kSnap; ++k) c->h_err[k] = 0;
     c->d_ebeta = c->zeros<double>(3 * n);
     c->d_epdf = c->zeros<double>(n);
     c->d_lbeta = c->zeros<double>(3 * n);
@@ -1166,7 +1169,7 @@ int pxg_render_passes_async(pxg_ctx* c, int npass) {
 }
 
 int pxg_snapshot_mean(pxg_ctx* c, int slot) {
-  if (!c || slot < 0 || slot > 1) return fail(c, PXG_E_INVALID, "pxg_snapshot_mean: bad slot");
+  if (!c || slot < 0 || slot >= pxg_ctx::kSnap) return fail(c, PXG_E_INVALID, "pxg_snapshot_mean: bad slot");
   return guarded(c, [&]() {
     CK(cudaMemcpyAsync(c->d_snap[slot], c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
     // the error flag as of these passes (Stage-1 errors of a pass are visible once its
@@ -1178,7 +1181,7 @@ int pxg_snapshot_mean(pxg_ctx* c, int slot) {
 }
 
 int pxg_read_snapshot(pxg_ctx* c, int slot, double* rgb, int* passes) {
-  if (!c || slot < 0 || slot > 1) return fail(c, PXG_E_INVALID, "pxg_read_snapshot: bad slot");
+  if (!c || slot < 0 || slot >= pxg_ctx::kSnap) return fail(c, PXG_E_INVALID, "pxg_read_snapshot: bad slot");
   return guarded(c, [&]() {
     CK(cudaEventSynchronize(c->snap_ev[slot]));
     CK(cudaMemcpy(c->h_pinned, c->d_snap[slot], sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost));

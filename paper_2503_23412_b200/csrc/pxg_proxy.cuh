@@ -36,131 +36,16 @@ struct RecipFrame {
   long long rem;
 };
 
-// recip::estimate_reciprocal (recip.hpp:131-138) with main_tree (:89-97) unrolled onto an
-// explicit frame stack, so the DFS visits nodes, draws numbers and nests the partial sums
-// exactly like the recursion: frame d holds ans = g/B (+ sgn * child values so far) and
-// the number of children still to expand.
-template <typename DrawG>
-PXD double reciprocal_run(DrawG&& draw, double bound, long long cap, Rng& rng,
-                                                 RecipFrame* frames, long long& cost, bool& truncated, int& err) {
-  cost = 0;
-  truncated = false;
-  long long depth = 0;
-  double ret = 0.0;
-  bool entering = true;
-  for (;;) {
-    if (entering) {
-      entering = false;
-      if (depth >= cap || cost >= cap) {
-        truncated = true;
-        ret = 0.0;
-      } else {
-        double g = draw(rng);
-        ++cost;
-        if (err) return 0.0;
-        RecipFrame fr;
-        fr.ans = g / bound;
-        fr.sgn = static_cast<double>((g > 0.0) - (g < 0.0));
-        const double r = fabs(g);
-        if (!(r >= 0.0) || !isfinite(r)) {
-          err = kErrSplit;
-          return 0.0;
-        }
-        const double fl = floor(r);
-        const double frac = r - fl;
-        long long n = static_cast<long long>(fl);
-        if (frac > 0.0 && rng.bernoulli(frac)) ++n;
-        fr.rem = n;
-        frames[depth] = fr;
-        // fall through to "next child" at this depth
-        if (fr.rem > 0) {
-          frames[depth].rem = fr.rem - 1;
-          ++depth;
-          entering = true;
-          continue;
-        }
-        ret = fr.ans;
-      }
-    }
-    // return `ret` from node at `depth` to its parent
-    if (depth == 0) break;
-    --depth;
-    RecipFrame& pf = frames[depth];
-    pf.ans += pf.sgn * ret;
-    if (pf.rem > 0) {
-      pf.rem -= 1;
-      ++depth;
-      entering = true;
-      continue;
-    }
-    ret = pf.ans;
-  }
-  return 1.0 / bound + ret;
-}
-
 // Resumable state of one reciprocal run (recip::estimate_reciprocal, recip.hpp:131-138).
+// The DFS itself is k_recip_dfs_warp (pxg_stage_kernels.cuh): main_tree (recip.hpp:89-97)
+// unrolled onto an explicit frame stack over precomputed nodes, nesting the partial sums
+// exactly like the recursion (frame d holds ans = g/B + sgn * child values so far and the
+// number of children still to expand), so the estimate is bit-identical.
 struct RunState {
   long long depth, cost, avail;  // avail: nodes 0..avail-1 have precomputed (g, n)
   double ret;
   int entering, truncated, done, err;
 };
-
-// main_tree (recip.hpp:89-97) as an explicit-stack DFS over precomputed node values:
-// node k (the k-th draw_g call in pre-order) has g[k], split count n[k] and error code
-// e[k]. Returns false when it needs node `avail` (not yet evaluated); the state resumes.
-// The frame stack nests the partial sums exactly like the recursion, so the estimate is
-// bit-identical to the reference's.
-PXD bool dfs_resume(RunState& st, const double* g, const long long* nsplit, const int* e, RecipFrame* frames,
-                    double bound, long long cap) {
-  for (;;) {
-    if (st.entering) {
-      if (st.depth >= cap || st.cost >= cap) {
-        st.entering = 0;
-        st.truncated = 1;
-        st.ret = 0.0;
-      } else {
-        const long long k = st.cost;
-        if (k >= st.avail) return false;
-        st.entering = 0;
-        if (e[k]) {
-          st.err = e[k];
-          st.done = 1;
-          return true;
-        }
-        const double gk = g[k];
-        ++st.cost;
-        RecipFrame fr;
-        fr.ans = gk / bound;
-        fr.sgn = static_cast<double>((gk > 0.0) - (gk < 0.0));
-        fr.rem = nsplit[k];
-        if (fr.rem > 0) {
-          fr.rem -= 1;
-          frames[st.depth] = fr;
-          ++st.depth;
-          st.entering = 1;
-          continue;
-        }
-        frames[st.depth] = fr;
-        st.ret = fr.ans;
-      }
-    }
-    if (st.depth == 0) {
-      st.done = 1;
-      st.ret = 1.0 / bound + st.ret;
-      return true;
-    }
-    --st.depth;
-    RecipFrame& pf = frames[st.depth];
-    pf.ans += pf.sgn * st.ret;
-    if (pf.rem > 0) {
-      pf.rem -= 1;
-      ++st.depth;
-      st.entering = 1;
-      continue;
-    }
-    st.ret = pf.ans;
-  }
-}
 
 // stochastic_split (recip.hpp:49-56) of node k on its own split stream.
 PXD long long split_count(double g, Rng& split_rng, int& err) {

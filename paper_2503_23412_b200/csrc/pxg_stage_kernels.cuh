@@ -370,6 +370,16 @@ struct BatchSet {
   int n;
 };
 
+// A node as the DFS consumes it: its frame value g / B (the division is done here, in
+// parallel, instead of on the DFS's serial chain; same fp64 operation, same result), its
+// split count, and its error code with the sign of g in bits 8 (> 0) and 9 (< 0).
+__device__ __forceinline__ void store_node(double* g, long long* nsplit, int* nerr, double gv, double B, long long n,
+                                           int err) {
+  *g = gv / B;
+  *nsplit = n;
+  *nerr = err | ((gv > 0.0) ? 0x100 : 0) | ((gv < 0.0) ? 0x200 : 0);
+}
+
 // Phase A of the reciprocal runs: evaluate nodes [avail, avail + chunk) of every active
 // run in parallel. Node k draws its support sample from (RECIP_NODE, k) and its split
 // decision from (RECIP_SPLIT, k) (include/pxg_philox.h), so its value does not depend on
@@ -400,9 +410,7 @@ __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride
     n = split_count(gv, sr, err);
   }
   const size_t o = static_cast<size_t>(j) * cap + k;
-  g[o] = gv;
-  nsplit[o] = n;
-  nerr[o] = err;
+  store_node(g + o, nsplit + o, nerr + o, gv, B, n, err);
   }
 }
 
@@ -424,9 +432,7 @@ __global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, cons
   Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), static_cast<uint64_t>(j));
   const long long n = split_count(gv, sr, err);
   const size_t o = static_cast<size_t>(j) * cap + k;
-  g[o] = gv;
-  nsplit[o] = n;
-  nerr[o] = err;
+  store_node(g + o, nsplit + o, nerr + o, gv, bound, n, err);
   }
 }
 
@@ -456,13 +462,13 @@ __global__ void k_recip_init(int runs, int repeats, int stride, const __grid_con
   if (live) active[atomicAdd(n_active, 1)] = j;
 }
 
-// Phase B, warp-cooperative: one warp per active run. The DFS state machine of dfs_resume
-// runs redundantly (warp-uniform) in every lane; node values are fetched 32 at a time with
+// Phase B, warp-cooperative: one warp per active run. The DFS state machine (main_tree,
+// recip.hpp:89-97, on an explicit frame stack) runs redundantly (warp-uniform) in every lane; node values are fetched 32 at a time with
 // one coalesced load per lane and broadcast by shuffle, and the frame stack's top W frames
 // live in shared memory (frames below are spilled to the run's global frame array and
 // reloaded in blocks). A long run then costs a few shared-memory round trips per node
 // instead of dependent global loads (the single-thread kernel's long-run tail). Same
-// arithmetic in the same order as dfs_resume, so estimates are bit-identical.
+// arithmetic in the same order as the reference's recursion, so estimates are bit-identical.
 template <int W>
 __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride, long long cap,
                                                         const __grid_constant__ BatchSet bs, double fixed_bound, const int* active, const int* n_active,
@@ -518,7 +524,8 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
           }
         }
         const int src = static_cast<int>(k - base);
-        const int ek = __shfl_sync(FULL, we, src);
+        const int ew = __shfl_sync(FULL, we, src);
+        const int ek = ew & 0xff;
         s.entering = 0;
         if (ek) {
           s.err = ek;
@@ -526,10 +533,9 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
           done = true;
           break;
         }
-        const double gk = __shfl_sync(FULL, wg, src);
+        const double ans = __shfl_sync(FULL, wg, src);  // g / B, divided in phase A
         const long long nk = __shfl_sync(FULL, wn, src);
         ++s.cost;
-        const double ans = gk / B;
         if (nk > 0) {
           const long long d = s.depth;
           if (d - lo == W) {  // window full: spill its bottom frame
@@ -539,7 +545,7 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
           }
           const int slot = static_cast<int>(d % W);
           sa[slot] = ans;
-          sg[slot] = static_cast<signed char>((gk > 0.0) - (gk < 0.0));
+          sg[slot] = static_cast<signed char>(((ew >> 8) & 1) - ((ew >> 9) & 1));
           sr[slot] = nk - 1;
           ++s.depth;
           s.entering = 1;

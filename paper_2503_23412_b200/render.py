@@ -288,6 +288,10 @@ class ProxyRenderer:
         return occ.astype(bool)
 
 
+SNAPSHOT_SLOTS = 4   # PXG_SNAPSHOT_SLOTS (include/pxg.h)
+PIPELINE_AHEAD = 3   # passes in flight in the pipelined pass_done loop (< SNAPSHOT_SLOTS)
+
+
 def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | None = None,
                       diagnostics: ProxyDiagnostics | None = None, pass_done=None, device: int = 0) -> np.ndarray:
     """proxima::render_proxy_bdpt on the GPU (proj/src/proxy.cpp:647-834)."""
@@ -299,16 +303,21 @@ def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | N
             r.render_passes(spp)
             img = r.mean()
         elif diagnostics is None:
-            # pipelined: pass k+1 is already running while pass_done sees the mean after k;
-            # an early stop returns that snapshot (bitwise the k-pass image)
-            r.render_passes_async(1)
-            r.snapshot(0)
+            # pipelined: passes k+1 .. k+AHEAD-1 are already enqueued while pass_done sees the
+            # mean after k, so the GPU never drains while the host reads back and runs the
+            # callback; an early stop returns that snapshot (bitwise the k-pass image) and
+            # discards the passes rendered beyond it
+            ahead = min(PIPELINE_AHEAD, spp)
+            for j in range(ahead):
+                r.render_passes_async(1)
+                r.snapshot(j % SNAPSHOT_SLOTS)
             img = None
             for k in range(1, spp + 1):
-                if k < spp:
+                j = k + ahead - 1  # next pass index to enqueue (0-based)
+                if j < spp:
                     r.render_passes_async(1)
-                    r.snapshot(k & 1)
-                img = r.read_snapshot((k - 1) & 1)
+                    r.snapshot(j % SNAPSHOT_SLOTS)
+                img = r.read_snapshot((k - 1) % SNAPSHOT_SLOTS)
                 if not pass_done(k, img):
                     break
         else:

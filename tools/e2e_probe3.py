@@ -8,17 +8,18 @@ from paper_2503_23412_b200.render import ProxyParams, ProxyRenderer, render_prox
 
 sc = scenes.cornell_c2(512)
 p = ProxyParams(light_walks=262144)
+NP = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 render_proxy_bdpt(sc, 2, 1000, p, pass_done=lambda d, im: True)
 for trial in range(2):
     t0 = time.perf_counter()
     q = ProxyRenderer(sc, 2000 + trial, p)
     t1 = time.perf_counter()
-    q.set_pass_limit(32)
+    q.set_pass_limit(NP)
     q.render_passes_async(1)
     q.snapshot(0)
     marks = []
-    for k in range(1, 33):
-        if k < 32:
+    for k in range(1, NP + 1):
+        if k < NP:
             q.render_passes_async(1)
             q.snapshot(k & 1)
         a = time.perf_counter()
