@@ -6,7 +6,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpxg.so")
+# PXG_LIBRARY: an alternative build of the same library (A/B tuning experiments only)
+LIB_PATH = os.environ.get("PXG_LIBRARY") or os.path.join(HERE, "libpxg.so")
 
 
 class PxgError(RuntimeError):
