@@ -221,13 +221,18 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
 // Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
 // ts.node holds a child code: >= 0 a 4-wide node, < 0 a leaf.
 __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack) {
-  int next;
-  if (ts.node >= 0) {
-    const float tb = tbound_f(ts.t_best);
-    const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
-    next = node4_order(h, tb, stack, ts.sp);
-  } else {
-    const int first = (~ts.node) >> 4, count = (~ts.node) & 15;
+  // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
+  // inner children are ordered nearest-first (the next node, then the stack)
+  const Node4Hits h = node4_test(S, ts.node, ts.rf, tbound_f(ts.t_best));
+  unsigned leaves = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
+  while (leaves) {
+    const int k = __ffs(leaves) - 1;
+    leaves &= leaves - 1;
+    const int code = ~(k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3]);
+    const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
       const double t = rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id);
@@ -236,8 +241,12 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
         ts.best = id;
       }
     }
-    next = kNoChild;
   }
+  Node4Hits hn = h;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (h.code[k] < 0) hn.hit &= ~(1u << k);
+  int next = node4_order(hn, tbound_f(ts.t_best), stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return true;
     next = stack[--ts.sp];
@@ -248,19 +257,27 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
 __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack) {
-  int next;
-  if (ts.node >= 0) {
-    const float tb = tbound_f(ts.t_best);
-    const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
-    next = node4_order(h, tb, stack, ts.sp);
-  } else {
-    const int first = (~ts.node) >> 4, count = (~ts.node) & 15;
+  const float tb = tbound_f(ts.t_best);
+  const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
+  unsigned leaves = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
+  while (leaves) {
+    const int k = __ffs(leaves) - 1;
+    leaves &= leaves - 1;
+    const int code = ~(k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3]);
+    const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
       if (rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
-    next = kNoChild;
   }
+  Node4Hits hn = h;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (h.code[k] < 0) hn.hit &= ~(1u << k);
+  int next = node4_order(hn, tb, stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return 2;
     next = stack[--ts.sp];
@@ -272,7 +289,7 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* 
 constexpr int kRefill = 4;  // refill a warp's idle lanes once at least this many are idle
 
 template <bool kAny>
-__global__ void __launch_bounds__(128, 8) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
+__global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int total = *Q.count;
