@@ -247,8 +247,31 @@ __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* s
   return c[0];
 }
 
-// Closest hit: returns the original primitive id or -1; t_best in/out (fp64).
-// A step visits either one 4-wide node (four box tests) or one leaf (its primitives).
+// Hit leaf children of a visited node (bit k of the result: child k is a hit leaf).
+__device__ __forceinline__ unsigned node4_leaves(const Node4Hits& h) {
+  unsigned leaves = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
+  return leaves;
+}
+
+__device__ __forceinline__ int node4_code(const Node4Hits& h, int k) {
+  return k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3];
+}
+
+// h with only its inner (node) children left in the hit mask.
+__device__ __forceinline__ Node4Hits node4_inner(const Node4Hits& h) {
+  Node4Hits hn = h;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (h.code[k] < 0) hn.hit &= ~(1u << k);
+  return hn;
+}
+
+// Closest hit: returns the original primitive id or -1; t_best in/out (fp64). Every step
+// visits one 4-wide node: its hit leaf children are tested right away, its hit inner
+// children are visited nearest-first (exactly the persistent kernel's closest_step).
 template <bool kCount = false>
 __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, const V3& d, double& t_best,
                                             TravCount* cnt = nullptr) {
@@ -256,15 +279,13 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
   int best = -1;
   int stack[kStack];
   int sp = 0;
-  int code = 0;
+  int node = 0;
   for (;;) {
-    int next;
-    if (code >= 0) {
-      const Node4Hits h = node4_test(S, code, rf, tbound_f(t_best));
-      if (kCount) cnt->nodes += 1;
-      next = node4_order(h, tbound_f(t_best), stack, sp);
-    } else {
-      const int first = (~code) >> 4, count = (~code) & 15;
+    const Node4Hits h = node4_test(S, node, rf, tbound_f(t_best));
+    if (kCount) cnt->nodes += 1;
+    for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+      const int code = ~node4_code(h, __ffs(leaves) - 1);
+      const int first = code >> 4, count = code & 15;
       if (kCount) cnt->prims += count;
       for (int i = 0; i < count; ++i) {
         int id;
@@ -274,13 +295,13 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
           best = id;
         }
       }
-      next = kNoChild;
     }
+    int next = node4_order(node4_inner(h), tbound_f(t_best), stack, sp);
     if (next == kNoChild) {
       if (sp == 0) break;
       next = stack[--sp];
     }
-    code = next;
+    node = next;
   }
   return best;
 }
@@ -289,35 +310,34 @@ __device__ __forceinline__ int trace_closest(const SceneView& S, const V3& o, co
   return trace_closest_t<false>(S, o, d, t_best);
 }
 
-// Any hit with t in [kRayEps, t_max] (the boolean of Scene::occluded, scene.cpp:170-177).
+// Any hit with t in [kRayEps, t_max] (the boolean of Scene::occluded, scene.cpp:170-177);
+// same visiting order as trace_closest_t (the persistent kernel's any_step).
 template <bool kCount = false>
 __device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const V3& d, double t_max,
                                          TravCount* cnt = nullptr) {
   const RayF rf = make_rayf(o, d);
   int stack[kStack];
   int sp = 0;
-  int code = 0;
+  int node = 0;
   const float tb = tbound_f(t_max);
   for (;;) {
-    int next;
-    if (code >= 0) {
-      const Node4Hits h = node4_test(S, code, rf, tb);
-      if (kCount) cnt->nodes += 1;
-      next = node4_order(h, tb, stack, sp);
-    } else {
-      const int first = (~code) >> 4, count = (~code) & 15;
+    const Node4Hits h = node4_test(S, node, rf, tb);
+    if (kCount) cnt->nodes += 1;
+    for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+      const int code = ~node4_code(h, __ffs(leaves) - 1);
+      const int first = code >> 4, count = code & 15;
       for (int i = 0; i < count; ++i) {
         int id;
         if (kCount) cnt->prims += 1;
         if (rec_hit(S.recs + first + i, o, d, t_max, id) > 0.0) return true;
       }
-      next = kNoChild;
     }
+    int next = node4_order(node4_inner(h), tb, stack, sp);
     if (next == kNoChild) {
       if (sp == 0) break;
       next = stack[--sp];
     }
-    code = next;
+    node = next;
   }
   return false;
 }

@@ -224,14 +224,8 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
   // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
   // inner children are ordered nearest-first (the next node, then the stack)
   const Node4Hits h = node4_test(S, ts.node, ts.rf, tbound_f(ts.t_best));
-  unsigned leaves = 0u;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
-  while (leaves) {
-    const int k = __ffs(leaves) - 1;
-    leaves &= leaves - 1;
-    const int code = ~(k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3]);
+  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+    const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
@@ -242,11 +236,7 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
       }
     }
   }
-  Node4Hits hn = h;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (h.code[k] < 0) hn.hit &= ~(1u << k);
-  int next = node4_order(hn, tbound_f(ts.t_best), stack, ts.sp);
+  int next = node4_order(node4_inner(h), tbound_f(ts.t_best), stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return true;
     next = stack[--ts.sp];
@@ -259,25 +249,15 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
 __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack) {
   const float tb = tbound_f(ts.t_best);
   const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
-  unsigned leaves = 0u;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
-  while (leaves) {
-    const int k = __ffs(leaves) - 1;
-    leaves &= leaves - 1;
-    const int code = ~(k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3]);
+  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+    const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
       if (rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
   }
-  Node4Hits hn = h;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (h.code[k] < 0) hn.hit &= ~(1u << k);
-  int next = node4_order(hn, tb, stack, ts.sp);
+  int next = node4_order(node4_inner(h), tb, stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return 2;
     next = stack[--ts.sp];
