@@ -374,8 +374,8 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
 // so no round waits for the host; a round with no active run costs two empty launches.
 template <typename Eval>
 int recip_rounds(cudaStream_t stream, long long cap, int* nact, Eval&& eval_and_dfs) {
-  static const int first = std::getenv("PXG_RECIP_CHUNK") ? std::atoi(std::getenv("PXG_RECIP_CHUNK")) : 32;
-  static const int grow = std::getenv("PXG_RECIP_GROW") ? std::atoi(std::getenv("PXG_RECIP_GROW")) : 4;
+  static const int first = std::getenv("PXG_RECIP_CHUNK") ? std::atoi(std::getenv("PXG_RECIP_CHUNK")) : 16;
+  static const int grow = std::getenv("PXG_RECIP_GROW") ? std::atoi(std::getenv("PXG_RECIP_GROW")) : 2;
   static const bool verbose = std::getenv("PXG_PROFILE") != nullptr;
   int cur = 0, chunk = std::max(first, 1), rounds = 0;
   long long covered = 0;
