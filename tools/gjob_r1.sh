@@ -3,7 +3,7 @@
 set -x
 mkdir -p gpurun_out/prof
 python bench.py > gpurun_out/prof/bench_full.log 2>&1; tail -c 3000 gpurun_out/prof/bench_full.log
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 2 --warmup 8 --quick > gpurun_out/prof/ncu1.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 16 --warmup 8 --quick > gpurun_out/prof/ncu1.log 2>&1
 cap() {  # name regex skip
   ncu --set full --clock-control none --import-source on -k regex:$2 --launch-skip $3 --launch-count 1 -o /tmp/$1 -f python bench.py --steps 2 --warmup 8 --quick > gpurun_out/prof/ncu_$1.log 2>&1
   ncu -i /tmp/$1.ncu-rep --page raw --csv > gpurun_out/prof/$1_raw.csv 2>&1
