@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in CPP_SOURCES:
         obj = os.path.join(bdir, src + ".o")
-        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", *inc, "-c", os.path.join(CSRC, src),
+        cmd = ["g++", "-std=c++20", "-O3", "-pthread", "-fPIC", "-ffp-contract=off", *inc, "-c", os.path.join(CSRC, src),
                "-o", obj]
         _run(cmd, verbose)
         objs.append(obj)
@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         _run(cmd, verbose)
         objs.append(obj)
     tmp = OUT + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], verbose)
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread"], verbose)
     os.replace(tmp, OUT)
     return OUT
 

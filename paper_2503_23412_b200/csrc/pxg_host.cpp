@@ -11,6 +11,8 @@
 #include "pxg_host.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -111,14 +113,12 @@ struct Builder {
   // Builds [first, first+count) and returns the child code referencing it.
   int leaf_max = 1;  // measured best on C2 (fp64 primitive tests dominate); PXG_LEAF overrides
 
-  int build(int first, int count, const Box& bounds, int depth) {
-    max_depth_seen = std::max(max_depth_seen, depth);
-    if (count <= leaf_max || depth >= 56) {
-      if (count <= 15) return leaf_code(first, count);
-    }
+  // Binned SAH split of [first, first+count): partitions the range, returns mid and the
+  // child boxes.
+  void split(int first, int count, int& mid, Box& lb, Box& rb) {
     Box cb;
     for (int i = first; i < first + count; ++i) cb.grow(prims[i].cen, prims[i].cen);
-    int mid = -1;
+    mid = -1;
     const int kBins = 16;
     double best_cost = INFINITY;
     int best_axis = -1, best_bin = -1;
@@ -168,9 +168,18 @@ struct Builder {
       if (mid == first || mid == first + count) mid = -1;
     }
     if (mid < 0) mid = first + count / 2;  // degenerate centroids: split by position
-    Box lb, rb;
     for (int i = first; i < mid; ++i) lb.grow(prims[i].lo, prims[i].hi);
     for (int i = mid; i < first + count; ++i) rb.grow(prims[i].lo, prims[i].hi);
+  }
+
+  int build(int first, int count, const Box& bounds, int depth) {
+    max_depth_seen = std::max(max_depth_seen, depth);
+    if (count <= leaf_max || depth >= 56) {
+      if (count <= 15) return leaf_code(first, count);
+    }
+    int mid;
+    Box lb, rb;
+    split(first, count, mid, lb, rb);
     const int idx = static_cast<int>(nodes.size());
     nodes.push_back(HostNode{});
     int cl = build(first, mid - first, lb, depth + 1);
@@ -178,6 +187,80 @@ struct Builder {
     set_child(nodes[idx], 0, lb, cl);
     set_child(nodes[idx], 1, rb, cr);
     return idx;
+  }
+
+  // Parallel build (same tree as build(), node indices in a different order): the top
+  // levels are split here; every subtree below depth kParDepth (or smaller than kParMin
+  // primitives) is deferred, built by a worker thread into its own vectors, and spliced in.
+  struct Pending {
+    int first, count, depth, parent, side;
+    Box bounds;
+  };
+  static constexpr int kParDepth = 5, kParMin = 2048;
+
+  int plan(int first, int count, const Box& bounds, int depth, int parent, int side, std::vector<Pending>& pend) {
+    max_depth_seen = std::max(max_depth_seen, depth);
+    if (parent >= 0 && (depth >= kParDepth || count <= kParMin)) {
+      pend.push_back(Pending{first, count, depth, parent, side, bounds});
+      return 0;  // patched after the splice
+    }
+    if (count <= leaf_max || depth >= 56) {
+      if (count <= 15) return leaf_code(first, count);
+    }
+    int mid;
+    Box lb, rb;
+    split(first, count, mid, lb, rb);
+    const int idx = static_cast<int>(nodes.size());
+    nodes.push_back(HostNode{});
+    int cl = plan(first, mid - first, lb, depth + 1, idx, 0, pend);
+    int cr = plan(mid, first + count - mid, rb, depth + 1, idx, 1, pend);
+    set_child(nodes[idx], 0, lb, cl);
+    set_child(nodes[idx], 1, rb, cr);
+    return idx;
+  }
+
+  void build_parallel(int n, const Box& all) {
+    std::vector<Pending> pend;
+    plan(0, n, all, 0, -1, 0, pend);  // nodes is empty, so the root lands in slot 0
+    struct Part {
+      std::vector<HostNode> nodes;
+      std::vector<int> order;
+      int root = 0, depth = 0;
+    };
+    std::vector<Part> parts(pend.size());
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t t; (t = next.fetch_add(1)) < pend.size();) {
+        Part& P = parts[t];
+        Builder sub{prims, P.nodes, P.order, pad};
+        sub.leaf_max = leaf_max;
+        P.root = sub.build(pend[t].first, pend[t].count, pend[t].bounds, pend[t].depth);
+        P.depth = sub.max_depth_seen;
+      }
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned i = 1; i < hw && i < pend.size(); ++i) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    for (size_t t = 0; t < pend.size(); ++t) {
+      const Part& P = parts[t];
+      const int node_off = static_cast<int>(nodes.size()), order_off = static_cast<int>(order.size());
+      auto remap = [&](int code) {
+        if (code >= 0) return code + node_off;
+        const int x = ~code;
+        return ~((((x >> 4) + order_off) << 4) | (x & 15));
+      };
+      for (HostNode nd : P.nodes) {
+        nd.c0 = remap(nd.c0);
+        nd.c1 = remap(nd.c1);
+        nodes.push_back(nd);
+      }
+      order.insert(order.end(), P.order.begin(), P.order.end());
+      HostNode& par = nodes[pend[t].parent];
+      (pend[t].side == 0 ? par.c0 : par.c1) = remap(P.root);
+      max_depth_seen = std::max(max_depth_seen, P.depth);
+    }
   }
 };
 
@@ -348,7 +431,7 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
     r.c1 = ~0;
     h.bvh_depth = 1;
   } else {
-    B.build(0, n, all, 0);  // nodes is empty, so the root lands in slot 0
+    B.build_parallel(n, all);
     h.bvh_depth = B.max_depth_seen;
   }
   h.nodes4.clear();

@@ -799,6 +799,15 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
   auto* c = new pxg_ctx();
   c->device = device;
   int rc = guarded(c, [&]() {
+    // PXG_PROFILE: host timestamps of the creation phases (debugging aid)
+    static const bool prof = std::getenv("PXG_PROFILE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!prof) return;
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      std::fprintf(stderr, "[pxg] create %-12s %8.2f ms\n", what, ms);
+    };
     if (sd->max_depth < 1) throw InvalidErr{"scene: max_depth must be at least 1"};
     if (sd->max_depth + 1 > kMaxPath - 2 || sd->max_depth - 1 > kMaxLight - 1)
       throw InvalidErr{"pxg: max_depth above 16 is not supported"};
@@ -825,7 +834,9 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
+    mark("streams");
     finalize_scene(*sd, c->host);
+    mark("finalize+bvh");
     SceneHost& h = c->host;
     c->width = sd->width;
     c->height = sd->height;
@@ -1098,6 +1109,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
     c->d_diag_accept = c->zeros<unsigned long long>(kBuckets);
     c->d_diag_touched = c->zeros<int>(kBuckets);
+    mark("buffers");
     if (c->proxy_on) {
       const int np = std::max(c->P.pretrace_paths, 1000);
       k_pretrace<<<blocks(np, 64), 64, 0, c->stream>>>(c->S, c->M, c->seed, np, c->d_max_ratio, c->d_ratio_cnt,
@@ -1106,6 +1118,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       check_err(c, c->stream);
     }
     CK(cudaDeviceSynchronize());
+    mark("pretrace");
   });
   if (rc != PXG_OK) {
     g_global_err = c->err;
