@@ -265,9 +265,11 @@ def run_ours(args):
     dev_ms = float(t.item())
     value = W * H * args.steps * world / (dev_ms / 1e3) / 1e6
 
-    # ---- roofline: every traversal launch of 2 more passes timed + work-counted
+    # ---- roofline: every traversal launch of one batch cycle (8 more passes of Stage 2 and the
+    # one 8-pass Stage-1 batch they launch) timed + work-counted, so the launch mix is the
+    # steady-state one
     r.set_pass_limit(-1)
-    tr = r.measure_traversal(2) if not args.quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
+    tr = r.measure_traversal(BATCH) if not args.quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
     r.close()
     peak, peak_src = measured_peak_gbs()
     roof = {}

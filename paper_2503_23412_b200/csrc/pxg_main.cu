@@ -417,49 +417,73 @@ void read_stage1_timing(pxg_ctx* c, PoolSlot& sl) {
 // Stage-1 front of `pass` into `sl` on stream1: pool walks, priority selection, entries,
 // probes and bounds (proxy.cpp:684-714, 389-395). Bounds of pass p see the bucket maxima
 // after pass p-1's probes, so fronts run in pass order on the one stream.
-void stage1_front(pxg_ctx* c, int pass, PoolSlot& sl) {
+void stage1_fronts(pxg_ctx* c, int p0, int L) {
   cudaStream_t st = c->stream1;
   HostProbe hp(st);
-  CK(cudaStreamWaitEvent(st, sl.s2_done, 0));  // Stage 2 of the slot's previous pass is done
-  CK(cudaEventRecord(sl.t0, st));
-  CK(cudaMemsetAsync(sl.diag, 0, sizeof(long long) * kBuckets * 5, st));
-  CK(cudaMemsetAsync(sl.diag_touched, 0, sizeof(int) * kBuckets, st));
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    CK(cudaStreamWaitEvent(st, sl.s2_done, 0));  // Stage 2 of the slot's previous pass is done
+    sl.pass = p0 + b;
+  }
+  CK(cudaEventRecord(c->slot_of(p0).t0, st));
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    CK(cudaMemsetAsync(sl.diag, 0, sizeof(long long) * kBuckets * 5, st));
+    CK(cudaMemsetAsync(sl.diag_touched, 0, sizeof(int) * kBuckets, st));
+  }
   const int walks = c->n_walks;
-  CK(cudaMemsetAsync(c->d_ccount, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(c->d_ccount, 0, sizeof(int) * L, st));
   if (walks > 0) {
-    CK(cudaMemsetAsync(c->d_wctr, 0, sizeof(unsigned) * walks, st));
+    // the pool walks of all L passes as one wavefront: walk w of pass p on (POOL_WALK, p<<32|w)
+    const int nw = L * walks;
+    CK(cudaMemsetAsync(c->d_wctr, 0, sizeof(unsigned) * nw, st));
     PathSet W{c->d_wpool, c->d_wnv, c->d_wctr, c->d_wbeta, c->d_wpdf, c->seed,
-              (static_cast<uint64_t>(pass) << 32) + static_cast<uint64_t>(c->shard.walk_begin),
-              PXG_KIND_POOL_WALK, walks, c->max_depth - 1, 0};
+              (static_cast<uint64_t>(p0) << 32) + static_cast<uint64_t>(c->shard.walk_begin),
+              PXG_KIND_POOL_WALK, nw, c->max_depth - 1, 0, walks};
     trace_paths(c, W, c->wA, c->wB, st);
-    k_pool_keys<<<blocks(walks, 128), 128, 0, st>>>(c->d_wpool, c->d_wnv, walks, c->seed, pass,
-                                                    c->shard.walk_begin, c->d_ckey, c->d_cval, c->d_ccount,
-                                                    c->cand_cap);
+    k_pool_keys<<<blocks(nw, 128), 128, 0, st>>>(c->d_wpool, c->d_wnv, walks, L, c->seed, p0, c->shard.walk_begin,
+                                                 c->d_ckey, c->d_cval, c->d_ccount, c->cand_cap);
     ++c->launches;
     hp.mark("walks");
   }
-  // priority selection, entry count, raw count and kappa on the device (no host round trip)
+  // priority selection, entry count, raw count and kappa of every pass on the device
   const int budget = c->P.pool_budget;
-  k_pool_select<<<1, 1024, c->sel_smem, st>>>(c->d_ckey, c->d_cval, c->d_ccount, c->cand_cap, budget, c->sel_cap,
-                                              c->d_sel, sl.ps, c->d_err);
+  const int B1 = std::max(budget, 1);
+  FrontSet fs{};
+  fs.n = L;
+  for (int b = 0; b < L; ++b) fs.ps[b] = c->slot_of(p0 + b).ps;
+  k_pool_select<<<L, 1024, c->sel_smem, st>>>(c->d_ckey, c->d_cval, c->d_ccount, c->cand_cap, budget, c->sel_cap,
+                                              c->d_sel, fs, c->d_err);
   ++c->launches;
-  sl.pass = pass;
   hp.mark("select");
   if (budget > 0) {
     const int R = c->P.recip_repeats;
-    k_pool_entries<<<blocks(budget, 64), 64, 0, st>>>(c->M, sl.ps, c->d_sel, c->d_wpool, walks, c->shard.walk_begin,
-                                                      sl.inc, sl.prefix);
-    k_pool_probes<<<blocks(4 * budget, 64), 64, 0, st>>>(c->S, c->seed, pass, sl.ps, sl.inc, sl.prefix, c->d_probe,
-                                                         c->d_probe_ok, R);
-    k_pool_bounds<<<1, 512, (6 * sizeof(double) + 5 * sizeof(int)) * budget, st>>>(sl.ps, sl.inc, c->d_probe, c->d_probe_ok,
-                                                               c->d_max_ratio, c->d_ratio_cnt, c->d_touched,
-                                                               sl.bound, c->d_err);
-    c->launches += 3;
-    hp.mark("entries+bounds");
+    for (int b = 0; b < L; ++b) {  // entries and probes are independent across passes
+      PoolSlot& sl = c->slot_of(p0 + b);
+      k_pool_entries<<<blocks(budget, 64), 64, 0, st>>>(c->M, sl.ps, c->d_sel + static_cast<size_t>(b) * B1,
+                                                        c->d_wpool + static_cast<size_t>(b) * walks, L * walks,
+                                                        c->shard.walk_begin, sl.inc, sl.prefix);
+      k_pool_probes<<<blocks(4 * budget, 64), 64, 0, st>>>(c->S, c->seed, p0 + b, sl.ps, sl.inc, sl.prefix,
+                                                           c->d_probe + static_cast<size_t>(b) * 4 * B1,
+                                                           c->d_probe_ok + static_cast<size_t>(b) * 4 * B1, R);
+      c->launches += 2;
+    }
   }
-  // ratio statistics as of this pass (reported by pxg_read_stats; Stage 2 does not read them)
-  CK(cudaMemcpyAsync(sl.snap_max, c->d_max_ratio, sizeof(double) * kBuckets, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(sl.snap_rcnt, c->d_ratio_cnt, sizeof(long long) * kBuckets, cudaMemcpyDeviceToDevice, st));
+  // bounds in pass order: B of pass p sees the bucket maxima after pass p-1's probes
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    if (budget > 0) {
+      k_pool_bounds<<<1, 512, (6 * sizeof(double) + 5 * sizeof(int)) * budget, st>>>(
+          sl.ps, sl.inc, c->d_probe + static_cast<size_t>(b) * 4 * B1,
+          c->d_probe_ok + static_cast<size_t>(b) * 4 * B1, c->d_max_ratio, c->d_ratio_cnt, c->d_touched, sl.bound,
+          c->d_err);
+      ++c->launches;
+    }
+    // ratio statistics as of this pass (reported by pxg_read_stats; Stage 2 does not read them)
+    CK(cudaMemcpyAsync(sl.snap_max, c->d_max_ratio, sizeof(double) * kBuckets, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(sl.snap_rcnt, c->d_ratio_cnt, sizeof(long long) * kBuckets, cudaMemcpyDeviceToDevice, st));
+  }
+  hp.mark("entries+bounds");
 }
 
 // Stage 1 of passes [p0, p0 + L): the fronts in pass order, ONE set of reciprocal rounds
@@ -470,9 +494,9 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
   HostProbe hp(st);
   BatchSet bs{};
   bs.n = L;
+  stage1_fronts(c, p0, L);
   for (int b = 0; b < L; ++b) {
     PoolSlot& sl = c->slot_of(p0 + b);
-    stage1_front(c, p0 + b, sl);
     bs.p[b] = BatchPass{sl.inc, sl.prefix, sl.bound, sl.ps, p0 + b};
   }
   const int R = c->P.recip_repeats;
@@ -986,8 +1010,12 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       c->d_scan_tmp = c->alloc<char>(need);
       c->scan_tmp_bytes = need;
     }
+    {
+      const char* eb = std::getenv("PXG_BATCH");
+      c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchDefault));
+    }
     if (c->proxy_on && c->n_walks > 0) {
-      const size_t w = c->n_walks;
+      const size_t w = static_cast<size_t>(c->n_walks) * c->batch;  // the walks of a whole batch
       c->wA = make_queue(c, w);
       c->wB = make_queue(c, w);
       c->d_wpool = c->alloc<PV>(w * std::max(c->max_depth - 1, 1));
@@ -1029,9 +1057,9 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     // pool
     const int walks = c->shard.walk_end - c->shard.walk_begin;
     c->cand_cap = std::max(1, walks) * std::max(1, c->max_depth - 2);
-    c->d_ckey = c->alloc<unsigned long long>(c->cand_cap);
-    c->d_cval = c->alloc<unsigned>(c->cand_cap);
-    c->d_ccount = c->zeros<int>(1);
+    c->d_ckey = c->alloc<unsigned long long>(static_cast<size_t>(c->cand_cap) * c->batch);
+    c->d_cval = c->alloc<unsigned>(static_cast<size_t>(c->cand_cap) * c->batch);
+    c->d_ccount = c->zeros<int>(c->batch);
     if (c->P.pool_budget > 3072) throw InvalidErr{"pxg: pool_budget above 3072 is not supported"};
     {
       // device priority selection: 2 x budget expected keys below the first threshold
@@ -1049,9 +1077,9 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     }
     const int B = std::max(c->P.pool_budget, 1);
     const int R = std::max(c->P.recip_repeats, 1);
-    c->d_sel = c->alloc<unsigned>(B);
-    c->d_probe = c->zeros<double>(4 * B);
-    c->d_probe_ok = c->zeros<int>(4 * B);
+    c->d_sel = c->alloc<unsigned>(static_cast<size_t>(B) * c->batch);
+    c->d_probe = c->zeros<double>(4 * static_cast<size_t>(B) * c->batch);
+    c->d_probe_ok = c->zeros<int>(4 * static_cast<size_t>(B) * c->batch);
     for (PoolSlot& sl : c->slot) {
       sl.inc = c->zeros<IncHdr>(B);
       sl.prefix = c->alloc<PV>(static_cast<size_t>(B) * kMaxLight);
@@ -1068,10 +1096,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       sl.snap_max = c->zeros<double>(kBuckets);
       sl.snap_rcnt = c->zeros<long long>(kBuckets);
       for (cudaEvent_t* e : {&sl.s1_done, &sl.s2_done, &sl.t0, &sl.t1, &sl.r0, &sl.r1}) CK(cudaEventCreate(e));
-    }
-    {
-      const char* eb = std::getenv("PXG_BATCH");
-      c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchDefault));
     }
     const size_t NR = static_cast<size_t>(B) * R * c->batch;  // reciprocal runs of one Stage-1 batch
     c->d_run_est = c->zeros<double>(NR);

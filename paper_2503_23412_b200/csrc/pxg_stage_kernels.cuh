@@ -92,19 +92,30 @@ __device__ __forceinline__ uint64_t unit_stream(int pass, int walk) {
 
 __device__ __forceinline__ void set_err(int* err, int code) { atomicCAS(err, 0, code); }
 
+constexpr int kBatchSetMax = 32;  // passes per Stage-1 batch, at most
+
 // ------------------------------------------------------------------ Stage 1 kernels
 // Eligible prefix ends of the traced pool walks get a 64-bit priority key each
 // (the priority-reservoir replacement of Algorithm R, proxy.cpp:696-711).
-__global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, uint64_t seed, int pass, int walk_begin,
-                            unsigned long long* keys, unsigned* vals, int* count, int cap) {
+// All passes of a Stage-1 batch at once: walk i of the batch belongs to pass pass0 + i / n_walks
+// (the pool of the batch is vertex-major over L * n_walks paths); pass b's candidates go to
+// keys / vals + b * cap, counted in count[b].
+__global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L, uint64_t seed, int pass0,
+                            int walk_begin, unsigned long long* keys, unsigned* vals, int* count, int cap) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_walks) return;
-  const int w = walk_begin + i;
+  const int total = L * n_walks;
+  if (i >= total) return;
+  const int b = i / n_walks;
+  const int pass = pass0 + b;
+  const int w = walk_begin + i % n_walks;
+  keys += static_cast<size_t>(b) * cap;
+  vals += static_cast<size_t>(b) * cap;
+  count += b;
   const int n = wnv[i];
   int flag[kMaxLight], emitter[kMaxLight];
   double pdf[kMaxLight];
   for (int k = 0; k < n; ++k) {
-    const PV& v = wpool[static_cast<size_t>(k) * n_walks + i];
+    const PV& v = wpool[static_cast<size_t>(k) * total + i];
     flag[k] = v.flag;
     emitter[k] = v.emitter;
     pdf[k] = v.pdf_fwd;
@@ -153,9 +164,22 @@ __device__ void bitonic_sort_pairs(unsigned long long* k, unsigned* v, int n) {
 // (keys are i.i.d. uniform, so the first guess, 2 x budget / raw of the key range, almost
 // always lands); those keys are compacted and bitonic-sorted by (key, value), and the
 // values of the first `need` are sorted again. Writes n_ent, raw and kappa of the pass.
+// The PassStates of the passes of a Stage-1 batch (kernel parameter, by value).
+struct FrontSet {
+  PassState* ps[kBatchSetMax];
+  int n;
+};
+
 __global__ void __launch_bounds__(1024) k_pool_select(const unsigned long long* keys, const unsigned* vals,
                                                       const int* count, int cand_cap, int budget, int cap,
-                                                      unsigned* sel, PassState* ps, int* err) {
+                                                      unsigned* sel, const __grid_constant__ FrontSet fs, int* err) {
+  // block b selects pass b of the batch
+  const int bb = blockIdx.x;
+  keys += static_cast<size_t>(bb) * cand_cap;
+  vals += static_cast<size_t>(bb) * cand_cap;
+  count += bb;
+  sel += static_cast<size_t>(bb) * max(budget, 1);
+  PassState* ps = fs.ps[bb];
   extern __shared__ unsigned long long sk[];  // [cap] keys, then [cap] values
   unsigned* sv = reinterpret_cast<unsigned*>(sk + cap);
   __shared__ int s_cnt;
@@ -364,7 +388,6 @@ struct BatchPass {
 // The passes of one Stage-1 batch, passed BY VALUE as a __grid_constant__ kernel parameter
 // (no host-to-device copy, so enqueueing a batch never waits for the host). n == 0: the
 // two-point fixture (every run live, fixed bound).
-constexpr int kBatchSetMax = 32;
 struct BatchSet {
   BatchPass p[kBatchSetMax];
   int n;

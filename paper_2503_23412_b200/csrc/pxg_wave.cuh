@@ -27,11 +27,12 @@ struct PathSet {
   double* beta;      // [n*3]
   double* pdf_dir;   // [n]
   uint64_t seed;
-  uint64_t stream_base;  // stream of path i = stream_base + i
+  uint64_t stream_base;  // stream of path i = stream_base + (i / per_pass) << 32 + i % per_pass
   uint32_t kind;
   int n;
   int max_vertices;
   int eye;           // 1: eye sub-path rules (camera vertex, unit-density primary hit)
+  int per_pass;      // > 0: paths of several passes back to back (pool walks of a Stage-1 batch)
 };
 
 // Ray queue: slot j holds a ray for path[j]; traversal writes hit_prim/hit_t per slot.
@@ -46,7 +47,9 @@ struct RayQueue {
 
 __device__ __forceinline__ Rng path_rng(const PathSet& P, int i) {
   Rng r;
-  r.r = pxg_rng_make(P.seed, P.kind, 0, P.stream_base + static_cast<uint64_t>(i));
+  const uint64_t q = P.per_pass > 0 ? static_cast<uint64_t>(i / P.per_pass) : 0;
+  const uint64_t w = P.per_pass > 0 ? static_cast<uint64_t>(i % P.per_pass) : static_cast<uint64_t>(i);
+  r.r = pxg_rng_make(P.seed, P.kind, 0, P.stream_base + (q << 32) + w);
   r.r.i = P.ctr[i];
   return r;
 }
