@@ -148,10 +148,12 @@ struct pxg_ctx {
   int recip_rounds = 0;
   static constexpr int kBatchMax = kBatchSetMax;  // passes per Stage-1 batch (PXG_BATCH, default kBatchDefault)
   static constexpr int kBatchDefault = 8;
-  PoolSlot slot[2 * kBatchMax];        // ring: batch k uses half k & 1
+  static constexpr int kRing = 3;      // pool slots = kRing batches: Stage 1 up to ~2 batches ahead
+  PoolSlot slot[kRing * kBatchMax];   // ring of kRing * batch slots (the rest unallocated)
   int batch = kBatchMax;               // passes per batch (<= kBatchMax)
   int next_batch = 0;                  // first pass without a launched Stage 1
-  PoolSlot& slot_of(int pass) { return slot[pass % (2 * batch)]; }
+  int ring() const { return kRing * batch; }
+  PoolSlot& slot_of(int pass) { return slot[pass % ring()]; }
   int* d_err = nullptr;
   // diagnostics
   long long* d_diag = nullptr;  // [4000*5]: cols 2..4 written by k_pool_finish
@@ -451,23 +453,24 @@ void stage1_fronts(pxg_ctx* c, int p0, int L) {
   const int B1 = std::max(budget, 1);
   FrontSet fs{};
   fs.n = L;
-  for (int b = 0; b < L; ++b) fs.ps[b] = c->slot_of(p0 + b).ps;
+  for (int b = 0; b < L; ++b) {
+    PoolSlot& sl = c->slot_of(p0 + b);
+    fs.ps[b] = sl.ps;
+    fs.inc[b] = sl.inc;
+    fs.prefix[b] = sl.prefix;
+  }
   k_pool_select<<<L, 1024, c->sel_smem, st>>>(c->d_ckey, c->d_cval, c->d_ccount, c->cand_cap, budget, c->sel_cap,
                                               c->d_sel, fs, c->d_err);
   ++c->launches;
   hp.mark("select");
   if (budget > 0) {
     const int R = c->P.recip_repeats;
-    for (int b = 0; b < L; ++b) {  // entries and probes are independent across passes
-      PoolSlot& sl = c->slot_of(p0 + b);
-      k_pool_entries<<<blocks(budget, 64), 64, 0, st>>>(c->M, sl.ps, c->d_sel + static_cast<size_t>(b) * B1,
-                                                        c->d_wpool + static_cast<size_t>(b) * walks, L * walks,
-                                                        c->shard.walk_begin, sl.inc, sl.prefix);
-      k_pool_probes<<<blocks(4 * budget, 64), 64, 0, st>>>(c->S, c->seed, p0 + b, sl.ps, sl.inc, sl.prefix,
-                                                           c->d_probe + static_cast<size_t>(b) * 4 * B1,
-                                                           c->d_probe_ok + static_cast<size_t>(b) * 4 * B1, R);
-      c->launches += 2;
-    }
+    // entries and probes are independent across passes: one launch each for the batch
+    k_pool_entries<<<dim3(blocks(budget, 64), L), 64, 0, st>>>(c->M, fs, c->d_sel, B1, c->d_wpool, L * walks,
+                                                               walks, c->shard.walk_begin);
+    k_pool_probes<<<dim3(blocks(4 * budget, 64), L), 64, 0, st>>>(c->S, c->seed, p0, fs, c->d_probe,
+                                                                  c->d_probe_ok, 4 * B1, R);
+    c->launches += 2;
   }
   // bounds in pass order: B of pass p sees the bucket maxima after pass p-1's probes
   for (int b = 0; b < L; ++b) {
@@ -705,18 +708,18 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
     if (c->pass_limit >= 0) L = std::min(L, std::max(1, c->pass_limit - p0));
     return L;
   };
-  // Look-ahead: after every Stage-2 enqueue, Stage 1 is launched for every batch starting
-  // before passes_done + batch (within the pass limit), so each batch has about a batch of
-  // Stage-2 time to finish. Launched batches never reach passes_done + 2 * batch - 1: the
-  // slot ring keeps the last rendered pass's slot for the dump / diagnostics readers.
+  // Look-ahead: after every Stage-2 enqueue, Stage 1 is launched for every batch that fits in
+  // the slot ring (within the pass limit), so each batch has one to two batches of Stage-2
+  // time to finish even when the host runs only a few passes ahead (the pipelined pass_done
+  // loop). Launched batches never reach passes_done + ring - 1: the ring keeps the last
+  // rendered pass's slot for the dump / diagnostics readers.
   auto launch_ahead = [&]() {
     if (!c->proxy_on) return;
     for (;;) {
       const int q = c->passes_done, nb = c->next_batch;
-      if (nb >= q + c->batch) break;
       if (c->pass_limit >= 0 && nb >= c->pass_limit) break;
-      const int L = std::min(batch_len(nb), q + 2 * c->batch - 1 - nb);
-      if (L <= 0) break;
+      const int L = batch_len(nb);
+      if (nb + L > q + c->ring() - 1) break;  // a whole batch, as far ahead as the ring allows
       for (int i = 0; i < L; ++i) read_stage1_timing(c, c->slot_of(nb + i));
       run_stage1_batch(c, nb, L);
     }
@@ -754,7 +757,7 @@ void render_passes_impl(pxg_ctx* c, int npass, bool record_last, bool wait = tru
   float total = 0.f;
   CK(cudaEventElapsedTime(&total, c->ev_call[0], c->ev_call[1]));
   c->stage_ms[6] = total;
-  for (auto& sl : c->slot) read_stage1_timing(c, sl);
+  for (int i = 0; i < c->ring(); ++i) read_stage1_timing(c, c->slot[i]);
   check_err(c, c->stream);
 }
 
@@ -1080,7 +1083,8 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_sel = c->alloc<unsigned>(static_cast<size_t>(B) * c->batch);
     c->d_probe = c->zeros<double>(4 * static_cast<size_t>(B) * c->batch);
     c->d_probe_ok = c->zeros<int>(4 * static_cast<size_t>(B) * c->batch);
-    for (PoolSlot& sl : c->slot) {
+    for (int si = 0; si < c->ring(); ++si) {
+      PoolSlot& sl = c->slot[si];
       sl.inc = c->zeros<IncHdr>(B);
       sl.prefix = c->alloc<PV>(static_cast<size_t>(B) * kMaxLight);
       sl.kept = c->zeros<int>(B);

@@ -164,9 +164,11 @@ __device__ void bitonic_sort_pairs(unsigned long long* k, unsigned* v, int n) {
 // (keys are i.i.d. uniform, so the first guess, 2 x budget / raw of the key range, almost
 // always lands); those keys are compacted and bitonic-sorted by (key, value), and the
 // values of the first `need` are sorted again. Writes n_ent, raw and kappa of the pass.
-// The PassStates of the passes of a Stage-1 batch (kernel parameter, by value).
+// Per-pass pointers of a Stage-1 batch (kernel parameter, by value).
 struct FrontSet {
   PassState* ps[kBatchSetMax];
+  IncHdr* inc[kBatchSetMax];
+  PV* prefix[kBatchSetMax];
   int n;
 };
 
@@ -250,10 +252,17 @@ __global__ void __launch_bounds__(1024) k_pool_select(const unsigned long long* 
 }
 
 // Materialise the kept entries (dropout on the stored walk prefix, proxy.cpp:59-94).
-__global__ void k_pool_entries(Mapper M, const PassState* ps, const unsigned* sel, const PV* wpool, int n_walks,
-                               int walk_begin, IncHdr* inc, PV* prefix) {
+// blockIdx.y = pass b of the batch: its selection at sel + b * sel_stride, its walks at
+// wpool + b * n_walks_pass in the batch's vertex-major pool (stride n_walks).
+__global__ void k_pool_entries(Mapper M, const __grid_constant__ FrontSet fs, const unsigned* sel, int sel_stride,
+                               const PV* wpool, int n_walks, int n_walks_pass, int walk_begin) {
+  const int b = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= ps->n_ent) return;
+  if (k >= fs.ps[b]->n_ent) return;
+  sel += static_cast<size_t>(b) * sel_stride;
+  wpool += static_cast<size_t>(b) * n_walks_pass;
+  IncHdr* inc = fs.inc[b];
+  PV* prefix = fs.prefix[b];
   const int w = static_cast<int>(sel[k] >> 5), end = static_cast<int>(sel[k] & 31u);
   PV v[kMaxLight];
   for (int q = 0; q < end; ++q) v[q] = wpool[static_cast<size_t>(q) * n_walks + (w - walk_begin)];
@@ -267,10 +276,17 @@ __global__ void k_pool_entries(Mapper M, const PassState* ps, const unsigned* se
 
 // The four f/q probes of every entry (estimate_inverse_p, proxy.cpp:389-394), one thread
 // per probe on its own stream (PROBE, end | i << 8).
-__global__ void k_pool_probes(SceneView S, uint64_t seed, int pass, const PassState* ps, const IncHdr* inc,
-                              const PV* prefix, double* probe, int* probe_ok, int repeats) {
+// blockIdx.y = pass b of the batch (pass0 + b); probes of pass b at probe + b * probe_stride.
+__global__ void k_pool_probes(SceneView S, uint64_t seed, int pass0, const __grid_constant__ FrontSet fs,
+                              double* probe, int* probe_ok, int probe_stride, int repeats) {
+  const int b = blockIdx.y;
+  const int pass = pass0 + b;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 4 * ps->n_ent) return;
+  if (t >= 4 * fs.ps[b]->n_ent) return;
+  const IncHdr* inc = fs.inc[b];
+  const PV* prefix = fs.prefix[b];
+  probe += static_cast<size_t>(b) * probe_stride;
+  probe_ok += static_cast<size_t>(b) * probe_stride;
   const int k = t >> 2, i = t & 3;
   probe_ok[t] = 0;
   const IncHdr& h = inc[k];
