@@ -192,6 +192,7 @@ struct pxg_ctx {
   int dfs_blocks = 0;         // grid-stride warp-DFS grid
   int sel_cap = 0;            // shared-memory capacity (entries) of the pool selection
   size_t sel_smem = 0;
+  size_t fin_smem = 0;        // pool finish shared memory
   int* d_trav_next = nullptr;  // [8] ray fetch counters (per stream use)
   // traversal roofline measurement (pxg_measure_traversal)
   bool measure = false;
@@ -540,11 +541,10 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
   for (int b = 0; b < L; ++b) {
     PoolSlot& sl = c->slot_of(p0 + b);
     const size_t o = static_cast<size_t>(b) * stride;
-    k_pool_finish<<<1, 512, (sizeof(double) + 3 * sizeof(int)) * std::max(c->P.pool_budget, 0) + sizeof(int) * kS,
-                    st>>>(
-        R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq,
-        c->d_est_cnt, c->d_touched, sl.diag, sl.diag_touched, sl.kept, sl.label_start, sl.label_list, sl.ps,
-        sl.snap_sum, sl.snap_sq, sl.snap_cnt, c->d_max_ratio, c->d_ratio_cnt, sl.snap_max, sl.snap_rcnt);
+    k_pool_finish<<<1, 1024, c->fin_smem, st>>>(
+        R, sl.inc, sl.bound, c->d_run_est + o, c->d_run_trunc + o, c->d_sum_est, c->d_sum_sq, c->d_est_cnt,
+        c->d_touched, sl.diag, sl.diag_touched, sl.kept, sl.label_start, sl.label_list, sl.ps, sl.snap_sum,
+        sl.snap_sq, sl.snap_cnt);
     ++c->launches;
     CK(cudaEventRecord(sl.t1, st));
     CK(cudaEventRecord(sl.s1_done, st));
@@ -1075,8 +1075,12 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       const int b = std::max(c->P.pool_budget, 0);
       CK(cudaFuncSetAttribute(k_pool_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>((6 * sizeof(double) + 5 * sizeof(int)) * b)));
+      int n2 = 1;
+      while (n2 < b) n2 <<= 1;
+      c->fin_smem = sizeof(unsigned long long) * n2 + (sizeof(double) + 2 * sizeof(int)) * b +
+                    sizeof(int) * (kS + 1024);
       CK(cudaFuncSetAttribute(k_pool_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>((sizeof(double) + 3 * sizeof(int)) * b + sizeof(int) * kS)));
+                              static_cast<int>(c->fin_smem)));
     }
     const int B = std::max(c->P.pool_budget, 1);
     const int R = std::max(c->P.recip_repeats, 1);

@@ -648,29 +648,53 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
   }
 }
 
+// Sorts n (a power of two) 64-bit keys ascending in shared memory; all threads.
+__device__ void bitonic_sort_u64(unsigned long long* k, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj <= i) continue;
+        const unsigned long long a = k[i], b = k[ixj];
+        if ((a > b) == ((i & size) == 0)) {
+          k[i] = b;
+          k[ixj] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Per entry: mean and second moment of its runs, validity (proxy.cpp:409-427); per bucket
 // the estimate sums in pool order; the kept list and the per-label lists in pool order
-// (proxy.cpp:729-735); then the stats snapshot Stage 2 of this pass reads. One block.
-__global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, const double* est,
-                              const int* trunc, double* sum_est, double* sum_sq, long long* est_cnt, int* touched,
-                              long long* diag, int* diag_touched, int* kept, int* label_start, int* label_list,
-                              PassState* ps, double* snap_sum, double* snap_sq, long long* snap_cnt,
-                              const double* max_ratio, const long long* ratio_cnt, double* snap_max,
-                              long long* snap_rcnt) {
+// (proxy.cpp:729-735); then the stats snapshot Stage 2 of this pass reads. One block of
+// 1024 threads; the orders come from shared-memory sorts of (bucket | label, entry) keys, so
+// every bucket's sum runs over its entries in entry order exactly like the reference.
+__global__ void __launch_bounds__(1024) k_pool_finish(int repeats, IncHdr* inc, const double* bound,
+                                                      const double* est, const int* trunc, double* sum_est,
+                                                      double* sum_sq, long long* est_cnt, int* touched,
+                                                      long long* diag, int* diag_touched, int* kept, int* label_start,
+                                                      int* label_list, PassState* ps, double* snap_sum,
+                                                      double* snap_sq, long long* snap_cnt) {
   const int n_ent = ps->n_ent;
-  // shared: [n_ent] inverse_p (double), then [n_ent] valid flags, keys, labels, [kS] label counts
-  extern __shared__ double smd[];
-  double* s_inv = smd;
-  int* ok = reinterpret_cast<int*>(smd + n_ent);
-  int* s_key = ok + n_ent;
-  int* s_lab = s_key + n_ent;
+  int n2 = 1;
+  while (n2 < n_ent) n2 <<= 1;
+  // shared: [n2] sort keys (u64), [n_ent] inverse_p (double), [n_ent] valid flags, [n_ent]
+  // labels, [kS] label counts, [1024] scan
+  extern __shared__ unsigned long long smk[];
+  unsigned long long* sk = smk;
+  double* s_inv = reinterpret_cast<double*>(sk + n2);
+  int* ok = reinterpret_cast<int*>(s_inv + n_ent);
+  int* s_lab = ok + n_ent;
   int* lcount = s_lab + n_ent;
+  int* scan = lcount + kS;
   for (int s = threadIdx.x; s < kS; s += blockDim.x) lcount[s] = 0;
   for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
     IncHdr& h = inc[k];
     ok[k] = 0;
-    s_key[k] = h.key;
     s_lab[k] = h.s_label;
+    sk[k] = ~0ull;
     if (!h.valid) continue;
     const int key = h.key;
     diag_touched[key] = 1;
@@ -697,24 +721,21 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
     atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 2]), static_cast<unsigned long long>(repeats));
     if (!valid) atomicAdd(reinterpret_cast<unsigned long long*>(&diag[key * 5 + 4]), 1ull);
     ok[k] = valid ? 1 : 0;
+    if (valid) sk[k] = (static_cast<unsigned long long>(key) << 32) | static_cast<unsigned>(k);
   }
+  for (int k = n_ent + threadIdx.x; k < n2; k += blockDim.x) sk[k] = ~0ull;
   __syncthreads();
-  // bucket sums in pool order (SubspaceStats::update_estimate, subspace.cpp:64-70)
-  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
-    if (!ok[k]) continue;
-    const int key = s_key[k];
-    bool last = true;
-    for (int k2 = k + 1; k2 < n_ent; ++k2)
-      if (ok[k2] && s_key[k2] == key) {
-        last = false;
-        break;
-      }
-    if (!last) continue;
+  // bucket sums in pool order (SubspaceStats::update_estimate, subspace.cpp:64-70): after the
+  // sort by (bucket, entry) each bucket is one segment, summed by one thread in entry order
+  bitonic_sort_u64(sk, n2);
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (sk[i] == ~0ull) continue;
+    const int key = static_cast<int>(sk[i] >> 32);
+    if (i > 0 && static_cast<int>(sk[i - 1] >> 32) == key) continue;
     double se = sum_est[key], sq = sum_sq[key];
     long long cnt = est_cnt[key];
-    for (int k2 = 0; k2 <= k; ++k2) {
-      if (!ok[k2] || s_key[k2] != key) continue;
-      const double m = s_inv[k2];
+    for (int j = i; j < n2 && sk[j] != ~0ull && static_cast<int>(sk[j] >> 32) == key; ++j) {
+      const double m = s_inv[static_cast<unsigned>(sk[j])];
       se += m;
       sq += m * m;
       ++cnt;
@@ -724,33 +745,46 @@ __global__ void k_pool_finish(int repeats, IncHdr* inc, const double* bound, con
     est_cnt[key] = cnt;
     touched[key] = 1;
   }
-  // kept list and label lists, both in pool order
-  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
-    if (!ok[k]) continue;
-    int pos = 0;
-    for (int k2 = 0; k2 < k; ++k2) pos += ok[k2];
-    kept[pos] = k;
-    atomicAdd(&lcount[s_lab[k]], 1);
+  __syncthreads();
+  // kept list in entry order: block exclusive scan of the valid flags over chunks
+  const int chunk = (n_ent + blockDim.x - 1) / blockDim.x;
+  const int k0 = threadIdx.x * chunk;
+  int mine = 0;
+  for (int k = k0; k < min(n_ent, k0 + chunk); ++k) mine += ok[k];
+  scan[threadIdx.x] = mine;
+  __syncthreads();
+  for (int off = 1; off < static_cast<int>(blockDim.x); off <<= 1) {
+    const int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  {
+    int pos = scan[threadIdx.x] - mine;
+    for (int k = k0; k < min(n_ent, k0 + chunk); ++k)
+      if (ok[k]) kept[pos++] = k;
+  }
+  const int n_kept = scan[blockDim.x - 1];
+  // label lists: sort by (label, entry); label_start from the per-label counts
+  for (int k = threadIdx.x; k < n2; k += blockDim.x) {
+    if (k < n_ent && ok[k]) {
+      sk[k] = (static_cast<unsigned long long>(s_lab[k]) << 32) | static_cast<unsigned>(k);
+      atomicAdd(&lcount[s_lab[k]], 1);
+    } else {
+      sk[k] = ~0ull;
+    }
   }
   __syncthreads();
+  bitonic_sort_u64(sk, n2);
+  for (int i = threadIdx.x; i < n_kept; i += blockDim.x) label_list[i] = static_cast<int>(static_cast<unsigned>(sk[i]));
   if (threadIdx.x == 0) {
-    int acc = 0, nk = 0;
+    int acc = 0;
     for (int s = 0; s < kS; ++s) {
       label_start[s] = acc;
       acc += lcount[s];
     }
     label_start[kS] = acc;
-    for (int k = 0; k < n_ent; ++k) nk += ok[k];
-    ps->n_kept = nk;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < n_ent; k += blockDim.x) {
-    if (!ok[k]) continue;
-    const int sl = s_lab[k];
-    int pos = label_start[sl];
-    for (int k2 = 0; k2 < k; ++k2)
-      if (ok[k2] && s_lab[k2] == sl) ++pos;
-    label_list[pos] = k;
+    ps->n_kept = n_kept;
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
