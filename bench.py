@@ -48,29 +48,41 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tuning sweeps: skip roofline, e2e and cpu_baseline")
+    ap.add_argument("--e2e-spp", type=int, default=64,
+                    help="spp of the end-to-end render call (capped at the config's spp)")
     return ap.parse_args()
 
 
 CONFIGS = {
-    # name: (generator, kwargs, pool walks per pass)
-    "C1": ("cornell_c1", dict(resolution=256, max_depth=8), 65536),
-    "C2": ("cornell_c2", dict(resolution=512, max_depth=10), 262144),
+    # name: (BASELINE.json configs index, generator, kwargs, pool walks per pass; None = one
+    # per pixel, the reference default n_px, proj/src/proxy.cpp:674)
+    "C1": (0, "cornell_c1", dict(resolution=256, max_depth=8), 65536),
+    "C2": (1, "cornell_c2", dict(resolution=512, max_depth=10), 262144),
+    "C3": (2, "lens_room_c3", dict(resolution=1024, max_depth=12), None),
+    "C4": (3, "procedural_c4", dict(width=1920, height=1080, max_depth=12), None),
+    "C5": (4, "procedural_c5", dict(width=3840, height=2160, max_depth=16), 4 << 20),
 }
 
 
 def make_scene(cfg: str):
     from paper_2503_23412_b200 import scenes
-    gen, kw, walks = CONFIGS[cfg]
-    return getattr(scenes, gen)(**kw), walks
+    _, gen, kw, walks = CONFIGS[cfg]
+    sc = getattr(scenes, gen)(**kw)
+    return sc, (walks if walks is not None else sc.n_px)
 
 
 def config_json(cfg, sc, walks):
-    return {"workload": f"{cfg}: BASELINE.json configs[{1 if cfg == 'C2' else 0}], {sc.camera.width}x{sc.camera.height}, "
+    scene_mb = (sc.n_prims * 80 + 2 * sc.n_prims * 64) / 2**20  # primitive records + ~2 4-wide nodes/4 prims
+    return {"workload": f"{cfg}: BASELINE.json configs[{CONFIGS[cfg][0]}], {sc.camera.width}x{sc.camera.height}, "
                         f"max_depth {sc.settings.max_depth}, {walks} pool walks/pass, {sc.n_prims} prims, proxy on",
             "step": "1 progressive pass (1 sample per pixel)",
             "spp": sc.settings.spp,
-            "window": "default: warm-up passes 0..7, timed passes 8..63 of the config's 64-spp render",
-            "l2": "inputs larger than L2: per-pass vertex pools/queues ~1 GB >> 126 MB L2 (scene itself L2-resident)"}
+            "window": "warm-up passes 0..W-1 (W rounded up to the 8-pass Stage-1 batch), timed passes W..W+K-1 "
+                      "of the config's render",
+            "l2": ("inputs larger than L2: per-pass vertex pools/queues ~1 GB >> 126 MB L2 (scene itself "
+                   "L2-resident)" if scene_mb < 60 else
+                   f"inputs larger than L2: per-pass vertex pools/queues >> 126 MB L2; scene ~{scene_mb:.0f} MB "
+                   "of BVH + primitive records, not L2-resident")}
 
 
 def measured_peak_gbs():
@@ -300,7 +312,7 @@ def run_ours(args):
     # (N > 1: render_proxy_bdpt_distributed, K passes per rank, NCCL all-reduce per round)
     e2e = None
     reads = [0]
-    spp_e2e = sc.settings.spp  # one full render call of the config (C2: 64 spp)
+    spp_e2e = min(sc.settings.spp, args.e2e_spp)  # one render call (C2: the config's full 64 spp)
 
     def cb(done, img):
         reads[0] += img.nbytes

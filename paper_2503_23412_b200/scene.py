@@ -106,12 +106,12 @@ class Scene:
     def to_json(self) -> str:
         """Serialise in the reference schema; floats use repr so values round-trip exactly."""
         prims = []
-        for i in range(self.n_prims):
-            s = int(self.shape[i])
-            m = self.materials[int(self.mat[i])].name
-            a, b, c = self.a[i].tolist(), self.b[i].tolist(), self.c[i].tolist()
+        names = [m.name for m in self.materials]
+        A, B, C, Rr = self.a.tolist(), self.b.tolist(), self.c.tolist(), self.radius.tolist()
+        for s, mi, a, b, c, r in zip(self.shape.tolist(), self.mat.tolist(), A, B, C, Rr):
+            m = names[mi]
             if s == SPHERE:
-                prims.append({"shape": "sphere", "material": m, "center": a, "radius": float(self.radius[i])})
+                prims.append({"shape": "sphere", "material": m, "center": a, "radius": r})
             elif s == TRIANGLE:
                 prims.append({"shape": "triangle", "material": m, "p0": a, "p1": b, "p2": c})
             else:

@@ -13,6 +13,17 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-4  # per-path contribution tolerance (north star)
 
 
+_ORACLE_SCENES = {}
+
+
+def oracle_scene(oracle, key, sc):
+    """OracleScene per scene key, kept for the session (the 1M-triangle C4 geometry takes
+    ~20 s to serialise and load into the reference)."""
+    if key not in _ORACLE_SCENES:
+        _ORACLE_SCENES[key] = oracle.OracleScene(sc.to_json())
+    return _ORACLE_SCENES[key]
+
+
 def rel_err(a, b):
     return np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
 
@@ -56,13 +67,15 @@ TRAVERSAL_SCENES = {
     "c2": lambda: scenes.cornell_c2(64),
     "sphere_room": lambda: scenes.sphere_room(16),
     "caustic_box": lambda: scenes.caustic_box(16),
+    "c3": lambda: scenes.lens_room_c3(64),
+    "c4": lambda: scenes.procedural_c4(64, 36),
 }
 
 
 @pytest.mark.parametrize("name", list(TRAVERSAL_SCENES))
 def test_traversal_prim_ids_bit_exact(pxg, oracle, name):
     sc = TRAVERSAL_SCENES[name]()
-    o = oracle.OracleScene(sc.to_json())
+    o = oracle_scene(oracle, "geom_" + name, sc)
     rng = np.random.default_rng(1)
     prim_rays = _camera_rays(sc, 200000, rng)
     sec = _secondary_rays(o, prim_rays, rng)
@@ -100,6 +113,8 @@ BDPT_SCENES = {
     "glass_slab": lambda: scenes.glass_slab(16),
     "c1_small": lambda: scenes.cornell_c1(32, max_depth=8),
     "c2_small": lambda: scenes.cornell_c2(24, max_depth=10),
+    "c3_small": lambda: scenes.lens_room_c3(24, max_depth=12),
+    "c4_small": lambda: scenes.procedural_c4(40, 24, max_depth=12),
 }
 
 
@@ -108,7 +123,7 @@ def test_bdpt_matches_reference_per_pixel(pxg, oracle, name):
     """Proxy off: every pixel-sample equals the UNMODIFIED reference render_bdpt (same
     pixel streams) within 1e-4 relative; primitive-id trajectories are identical."""
     sc = BDPT_SCENES[name]()
-    o = oracle.OracleScene(sc.to_json())
+    o = oracle_scene(oracle, name, sc)
     spp = 3
     ref = o.render_bdpt(spp, 5)
     _, run = o.render(spp, 5, params={"enabled": 0}, threads=8, trace=True, trace_pass=spp - 1)
@@ -147,6 +162,8 @@ PROXY_SCENES = {
     # ... and budget > raw (every candidate kept; only the (walk, end) sort)
     "c1_budget3000": (lambda: scenes.cornell_c1(30, max_depth=8),
                       {"pretrace_paths": 4000, "light_walks": 6000, "pool_budget": 3000}),
+    "c3_small": (lambda: scenes.lens_room_c3(24, max_depth=12), {"pretrace_paths": 4000, "light_walks": 8000}),
+    "c4_small": (lambda: scenes.procedural_c4(40, 24, max_depth=12), {"pretrace_paths": 4000, "light_walks": 8000}),
 }
 
 
@@ -156,7 +173,7 @@ def test_proxy_render_matches_oracle(pxg, oracle, name):
     gated per-pass values equal the restated reference loop."""
     make, pd = PROXY_SCENES[name]
     sc = make()
-    o = oracle.OracleScene(sc.to_json())
+    o = oracle_scene(oracle, name, sc)
     spp = 3
     img_o, run = o.render(spp, 9, params=pd, threads=8, trace=True, pool_cap=max(400, pd.get("pool_budget", 400)))
     params = ProxyParams(**pd)

@@ -164,3 +164,14 @@ def test_config_generators(oracle):
     o = oracle.OracleScene(c1.to_json())
     assert o.n_prims == c1.n_prims
     assert abs(o.total_emitter_area - 0.0625) < 1e-15
+    c3 = scenes.lens_room_c3(8)
+    assert c3.n_prims == 6 + 2 * 19998 + 256 * 256 and len(c3.emitter_prim) == 256 * 256
+    lit = c3.emitter_radiance[:, 0]
+    assert set(np.unique(lit).tolist()) == {0.0, 20.0} and 0.48 < np.mean(lit > 0) < 0.52
+    o3 = oracle.OracleScene(c3.to_json())
+    assert o3.n_prims == c3.n_prims and abs(o3.total_emitter_area - 0.2) < 1e-9
+    c4 = scenes.procedural_c4(8, 8, instances=40)
+    assert len(c4.emitter_prim) == 4 and len(c4.materials) == 41
+    full = scenes.procedural_c4(8, 8)
+    assert 0.95e6 < full.n_prims < 1.1e6
+    assert np.array_equal(full.a, scenes.procedural_c4(8, 8).a)  # seeded, deterministic
