@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tuning sweeps: skip roofline, e2e and cpu_baseline")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M-triangle) device line in the C2 run")
     ap.add_argument("--e2e-spp", type=int, default=64,
                     help="spp of the end-to-end render call (capped at the config's spp)")
     return ap.parse_args()
@@ -94,13 +95,15 @@ def measured_peak_gbs():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+def ncu_traffic(cfg: str, kernel: str):
+    """DRAM bytes per launch of `kernel` on config `cfg` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), if any."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
-    except (OSError, ValueError):
+            v = json.load(f).get(cfg, {}).get(kernel)
+            return v.get("dram_bytes") if isinstance(v, dict) else v
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -210,6 +213,93 @@ def scene_bytes(sc):
                len(sc.materials) * 7 * 8 + sc.emitter_prim.nbytes + sc.emitter_radiance.nbytes)
 
 
+def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
+    """Device-resident throughput of `steps` passes after the warm-up (CUDA events on the
+    pass stream), then the traversal roofline over one more batch cycle."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_23412_b200.render import ProxyRenderer
+    W, H = sc.camera.width, sc.camera.height
+    r = ProxyRenderer(sc, seed, params, device=local)
+    acc = torch.zeros((H, W, 3), dtype=torch.float64, device="cuda") if world > 1 else None
+    # Stage 1 runs one batch (8 passes) ahead of Stage 2. Steady-state accounting: warm-up is
+    # rounded up to a batch multiple and ends with exactly one batch pre-computed; the timed
+    # call's look-ahead is capped so it computes Stage 1 for exactly K passes. The timed
+    # window therefore holds K passes of Stage 2 and K passes of Stage 1, like the pipeline
+    # in steady state.
+    BATCH = 8
+    warm = -(-max(warmup, 3) // BATCH) * BATCH
+    r.set_pass_limit(warm + BATCH)
+    for _ in range(warm):
+        r.render_passes(1)
+        if world > 1:
+            r.accum_to_device(acc.data_ptr())
+            dist.all_reduce(acc)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    r.set_pass_limit(warm + BATCH + steps)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world == 1:
+        r.render_passes(steps)
+        torch.cuda.synchronize()
+    else:
+        ev0.record()
+        for _ in range(steps):
+            r.render_passes(1)
+            r.accum_to_device(acc.data_ptr())
+            dist.all_reduce(acc)
+        ev1.record()
+        torch.cuda.synchronize()
+    stage_ms, counts = r.timing()
+    if world == 1:
+        dev_ms = float(stage_ms[6])  # first pass start -> last pass end on the device, host gaps included
+    else:
+        dev_ms = float(ev0.elapsed_time(ev1))
+    t = torch.tensor([dev_ms], device="cuda")
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    value = W * H * steps * world / (dev_ms / 1e3) / 1e6
+    free, total = torch.cuda.mem_get_info()
+    hbm_gb_used = round((total - free) / 1e9, 1)
+
+    # ---- roofline: every traversal launch of one batch cycle (8 more passes of Stage 2 and the
+    # one 8-pass Stage-1 batch they launch) timed + work-counted, so the launch mix is the
+    # steady-state one
+    r.set_pass_limit(-1)
+    tr = r.measure_traversal(BATCH) if not quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
+    r.close()
+    peak, peak_src = measured_peak_gbs()
+    roof = {}
+    for kind, kname in (("closest", "k_trav_persistent<0>"), ("anyhit", "k_trav_persistent<1>")):
+        m = tr[kind]
+        if m["launches"] <= 0 or m["ms"] <= 0:
+            continue
+        bytes_total = m["nodes"] * NODE_BYTES + m["prims"] * PRIM_BYTES
+        roof[kind] = {"kernel": kname, "launches": int(m["launches"]), "rays": int(m["rays"]),
+                      "bytes_per_ray": round(bytes_total / max(m["rays"], 1), 1),
+                      "nodes_per_ray": round(m["nodes"] / max(m["rays"], 1), 2),
+                      "prims_per_ray": round(m["prims"] / max(m["rays"], 1), 2),
+                      "bytes_per_launch": bytes_total / m["launches"], "ms_per_launch": m["ms"] / m["launches"],
+                      "achieved_gbs": bytes_total / (m["ms"] / 1e3) / 1e9, "ms_total": m["ms"]}
+    dom = max(roof, key=lambda k: roof[k]["ms_total"]) if roof else None
+    roofline = None
+    if dom:
+        d = roof[dom]
+        roofline = {"bound": "hbm", "achieved": round(d["achieved_gbs"], 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(d["achieved_gbs"] / peak, 4), "traffic": ncu_traffic(cfg, d["kernel"]),
+                    "kernel": d["kernel"], "peak_source": peak_src,
+                    "algorithmic_bytes": f"{NODE_BYTES} B per BVH node visit + {PRIM_BYTES} B per primitive test, "
+                                         "counted by an instrumented copy on the same rays",
+                    "per_kernel": roof}
+    return {"value": value, "dev_ms": dev_ms, "warm": warm, "counts": counts, "stage_ms": stage_ms,
+            "roofline": roofline, "hbm_gb_used": hbm_gb_used}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -232,80 +322,21 @@ def run_ours(args):
     # all-reduce per pass; N = 1 is the plain single-GPU render.
     from paper_2503_23412_b200.distributed import rank_seed
     seed = rank_seed(0, rank)
-    r = ProxyRenderer(sc, seed, params, device=local)
-    acc = torch.zeros((H, W, 3), dtype=torch.float64, device="cuda")
-    # Stage 1 runs one batch (8 passes) ahead of Stage 2. Steady-state accounting: warm-up is
-    # rounded up to a batch multiple and ends with exactly one batch pre-computed; the timed
-    # call's look-ahead is capped so it computes Stage 1 for exactly K passes. The timed
-    # window therefore holds K passes of Stage 2 and K passes of Stage 1, like the pipeline
-    # in steady state.
-    BATCH = 8
-    warm = -(-max(args.warmup, 3) // BATCH) * BATCH
-    r.set_pass_limit(warm + BATCH)
-    for _ in range(warm):
-        r.render_passes(1)
-        if world > 1:
-            r.accum_to_device(acc.data_ptr())
-            dist.all_reduce(acc)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    r.set_pass_limit(warm + BATCH + args.steps)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        if world == 1:
-            r.render_passes(args.steps)
-            torch.cuda.synchronize()
-        else:
-            ev0.record()
-            for _ in range(args.steps):
-                r.render_passes(1)
-                r.accum_to_device(acc.data_ptr())
-                dist.all_reduce(acc)
-            ev1.record()
-            torch.cuda.synchronize()
-    stage_ms, counts = r.timing()
-    if world == 1:
-        dev_ms = float(stage_ms[6])  # first pass start -> last pass end on the device, host gaps included
-    else:
-        dev_ms = float(ev0.elapsed_time(ev1))
-    t = torch.tensor([dev_ms], device="cuda")
-    if world > 1:
-        dist.barrier()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms = float(t.item())
-    value = W * H * args.steps * world / (dev_ms / 1e3) / 1e6
-
-    # ---- roofline: every traversal launch of one batch cycle (8 more passes of Stage 2 and the
-    # one 8-pass Stage-1 batch they launch) timed + work-counted, so the launch mix is the
-    # steady-state one
-    r.set_pass_limit(-1)
-    tr = r.measure_traversal(BATCH) if not args.quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
-    r.close()
-    peak, peak_src = measured_peak_gbs()
-    roof = {}
-    for kind, kname in (("closest", "k_trav_persistent<0>"), ("anyhit", "k_trav_persistent<1>")):
-        m = tr[kind]
-        if m["launches"] <= 0 or m["ms"] <= 0:
-            continue
-        bytes_total = m["nodes"] * NODE_BYTES + m["prims"] * PRIM_BYTES
-        roof[kind] = {"kernel": kname, "launches": int(m["launches"]), "rays": int(m["rays"]),
-                      "bytes_per_ray": round(bytes_total / max(m["rays"], 1), 1),
-                      "nodes_per_ray": round(m["nodes"] / max(m["rays"], 1), 2),
-                      "prims_per_ray": round(m["prims"] / max(m["rays"], 1), 2),
-                      "bytes_per_launch": bytes_total / m["launches"], "ms_per_launch": m["ms"] / m["launches"],
-                      "achieved_gbs": bytes_total / (m["ms"] / 1e3) / 1e9, "ms_total": m["ms"]}
-    dom = max(roof, key=lambda k: roof[k]["ms_total"]) if roof else None
-    roofline = None
-    if dom:
-        d = roof[dom]
-        roofline = {"bound": "hbm", "achieved": round(d["achieved_gbs"], 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(d["achieved_gbs"] / peak, 4), "traffic": ncu_traffic(d["kernel"]),
-                    "kernel": d["kernel"], "peak_source": peak_src,
-                    "algorithmic_bytes": f"{NODE_BYTES} B per BVH node visit + {PRIM_BYTES} B per primitive test, "
-                                         "counted by an instrumented copy on the same rays",
-                    "per_kernel": roof}
+        dev = measure_device(sc, params, seed, args.steps, args.warmup, world, local, args.quick, args.config)
+    value, dev_ms, warm, counts, stage_ms, roofline = (dev[k] for k in ("value", "dev_ms", "warm", "counts",
+                                                                        "stage_ms", "roofline"))
+    # The north star's roofline target is quoted on the 1M-triangle scene (C4, BASELINE.json
+    # configs[3]): the default C2 line also carries a C4 device measurement (same method).
+    north_star_scene = None
+    if args.config == "C2" and world == 1 and not args.quick and not args.no_c4:
+        sc4, walks4 = make_scene("C4")
+        d4 = measure_device(sc4, ProxyParams(light_walks=walks4), seed, 16, 8, 1, local, False, "C4")
+        north_star_scene = {"config": config_json("C4", sc4, walks4)["workload"], "value": round(d4["value"], 4),
+                            "unit": "Msamples/s", "steps": 16, "warmup": d4["warm"],
+                            "ms_per_step": round(d4["dev_ms"] / 16, 4), "roofline": d4["roofline"],
+                            "hbm_gb_used": d4["hbm_gb_used"]}
+        del sc4
 
     # ---- end to end through the public API: render_proxy_bdpt(scene arrays on the host, spp=K)
     # with the pass_done callback reading the running mean image back every pass
@@ -381,6 +412,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(counts[0]),
         "roofline": roofline,
+        "hbm_gb_used": dev["hbm_gb_used"],
+        "north_star_scene": north_star_scene,
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
         "stage_ms": {"stage1_batches_total": round(float(stage_ms[0]), 3),

@@ -162,6 +162,13 @@ int pxg_dump_pool(pxg_ctx* ctx, int cap, int* n, long long* raw, int* walk, int*
 int pxg_intersect(pxg_ctx* ctx, int n, const double* rays, const double* tmax, int* prim, double* t);
 int pxg_occluded(pxg_ctx* ctx, int n, const double* segs, int* occ);
 
+/* proxima::render_pt (proj/include/proxima/transport.hpp:88, proj/src/transport.cpp:272-381)
+ * on the device for this context's pixels: the unidirectional path tracer with NEE, the
+ * converged reference of the relMSE checks. rgb[n*3] = mean over `chunks` independent
+ * renders; chunk c is render_pt(spp, seed ^ c*0x9E3779B97F4A7C15), so chunks = 1 is exactly
+ * the reference's render_pt(scene, spp, seed) on the same Philox pixel streams. */
+int pxg_render_pt(pxg_ctx* ctx, int spp, uint64_t seed, int chunks, double* rgb);
+
 /* Reciprocal estimator on the two-point fixture f = {1,3}, q = 1/2 (the reference's own
  * known-answer case, proj/tests/test_recip.cpp:16-23), run i on stream (seed, RECIP, 0, i). */
 int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double* est,

@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["pxg_main.cu"]
 CPP_SOURCES = ["pxg_host.cpp"]
-HEADERS = ["pxg_stage_kernels.cuh", "pxg_proxy_wave.cuh", "pxg_wave.cuh", "pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
+HEADERS = ["pxg_pt.cuh", "pxg_stage_kernels.cuh", "pxg_proxy_wave.cuh", "pxg_wave.cuh", "pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
 
 
 def _inputs():

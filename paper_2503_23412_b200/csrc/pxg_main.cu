@@ -10,6 +10,7 @@
 #include <utility>
 
 #include "pxg_stage_kernels.cuh"
+#include "pxg_pt.cuh"
 
 // ------------------------------------------------------------------ context
 // Pool state of one pass, double-buffered: Stage 1 of pass p+1 (stream s1) fills one slot
@@ -1418,6 +1419,30 @@ int pxg_intersect(pxg_ctx* c, int n, const double* rays, const double* tmax, int
     if (dt) cudaFree(dt);
     cudaFree(dp);
     cudaFree(dtt);
+  });
+}
+
+int pxg_render_pt(pxg_ctx* c, int spp, uint64_t seed, int chunks, double* rgb) {
+  return guarded(c, [&]() {
+    if (!rgb) throw InvalidErr{"pxg_render_pt: null output"};
+    if (chunks < 1) throw InvalidErr{"pxg_render_pt: chunks must be >= 1"};
+    // render_image's `spp <= 0 -> scene.settings.spp` (transport.cpp:358) is resolved by the
+    // caller: pxg_scene_desc carries no Settings::spp
+    if (spp <= 0) throw InvalidErr{"pxg_render_pt: spp must be >= 1"};
+    const int n = c->n;
+    const size_t per = static_cast<size_t>(n) * 3;
+    double* dparts = dalloc<double>(per * chunks);
+    double* dout = dalloc<double>(per);
+    const long long threads = static_cast<long long>(n) * chunks;
+    k_render_pt<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, c->stream>>>(c->S, c->max_depth, c->row0, n,
+                                                                                       chunks, spp, seed, dparts);
+    CK(cudaGetLastError());
+    k_pt_reduce<<<blocks(static_cast<long long>(per), 256), 256, 0, c->stream>>>(n, chunks, dparts, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(rgb, dout, sizeof(double) * per, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dparts);
+    cudaFree(dout);
   });
 }
 

@@ -281,6 +281,15 @@ class ProxyRenderer:
                                           _dp(t)))
         return prim, t
 
+    def render_pt(self, spp: int, seed: int, chunks: int = 1) -> np.ndarray:
+        """proxima::render_pt (proj/src/transport.cpp:376-381) on the device for this
+        context's pixels; `chunks` > 1 averages independent renders (see include/pxg.h)."""
+        if spp <= 0:
+            spp = self.scene.settings.spp
+        out = np.zeros((self.n, 3))
+        self._check(self._L.pxg_render_pt(self._ctx, spp, seed & (2**64 - 1), chunks, _dp(out)))
+        return out.reshape(-1, self.scene.camera.width, 3)
+
     def occluded(self, segs: np.ndarray):
         segs = np.ascontiguousarray(segs, np.float64)
         occ = np.zeros(segs.shape[0], np.int32)
@@ -338,6 +347,12 @@ def render_proxy_bdpt(scene: Scene, spp: int, seed: int, params: ProxyParams | N
 def render_bdpt(scene: Scene, spp: int, seed: int, device: int = 0) -> np.ndarray:
     """proxima::render_bdpt (proj/src/transport.cpp:380-386): the proxy renderer with proxy off."""
     return render_proxy_bdpt(scene, spp, seed, ProxyParams(enabled=False), device=device)
+
+
+def render_pt(scene: Scene, spp: int, seed: int, chunks: int = 1, device: int = 0) -> np.ndarray:
+    """proxima::render_pt(scene, spp, seed) (proj/include/proxima/transport.hpp:88) on the GPU."""
+    with ProxyRenderer(scene, seed, ProxyParams(enabled=False), device=device) as r:
+        return r.render_pt(spp, seed, chunks)
 
 
 def recip_twopoint(n: int, bound: float, cap: int = 10000, seed: int = 1):
