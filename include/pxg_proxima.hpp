@@ -158,4 +158,26 @@ inline Image render_proxy_bdpt_gpu(const Scene& scene, int spp, uint64_t seed, c
   return to_image();
 }
 
+// Same signature and behaviour as proxima::render_pt (proj/include/proxima/transport.hpp:88),
+// computed on the GPU (per pixel identical to the reference on the same RNG streams).
+inline Image render_pt_gpu(const Scene& scene, int spp, uint64_t seed, int device = 0) {
+  if (spp <= 0) spp = scene.settings.spp;
+  PxgSceneArrays arrays(scene);
+  pxg_params p;
+  pxg_default_params(&p);
+  p.enabled = 0;
+  pxg_ctx* ctx = nullptr;
+  pxg_throw(pxg_create(&arrays.desc, &p, seed, device, nullptr, &ctx), nullptr);
+  struct Guard {
+    pxg_ctx* c;
+    ~Guard() { pxg_destroy(c); }
+  } guard{ctx};
+  const int w = scene.camera.width, h = scene.camera.height;
+  std::vector<double> rgb(static_cast<size_t>(w) * h * 3);
+  pxg_throw(pxg_render_pt(ctx, spp, seed, 1, rgb.data()), ctx);
+  Image img(w, h);
+  for (size_t i = 0; i < img.pixels.size(); ++i) img.pixels[i] = Vec3(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+  return img;
+}
+
 }  // namespace proxima

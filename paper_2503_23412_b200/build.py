@@ -36,10 +36,12 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """`out` / `defines` (-DNAME=V for the device code): A/B variants of the same sources for
+    tuning runs (loaded through PXG_LIBRARY); the shipped library is the default build."""
+    if out == OUT and not defines and not force and up_to_date():
         return OUT
-    bdir = os.path.join(HERE, "_build")
+    bdir = os.path.join(HERE, "_build" if out == OUT else "_build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(bdir, exist_ok=True)
     inc = ["-I", os.path.join(REPO, "include"), "-I", CSRC]
     objs = []
@@ -52,14 +54,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in CU_SOURCES:
         obj = os.path.join(bdir, src + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "--expt-relaxed-constexpr",
-               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc, "-c", os.path.join(CSRC, src),
+               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *defines, *inc, "-c", os.path.join(CSRC, src),
                "-o", obj]
         _run(cmd, verbose)
         objs.append(obj)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread"], verbose)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 def _run(cmd, verbose):
@@ -74,5 +76,8 @@ def _run(cmd, verbose):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    # python -m paper_2503_23412_b200.build [--force] [-v] [--out PATH -DNAME=V ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else OUT
+    defs = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=os.path.abspath(out), defines=defs))

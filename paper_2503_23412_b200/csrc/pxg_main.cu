@@ -903,6 +903,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     SceneView& S = c->S;
     S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
     S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
+    if (reinterpret_cast<uintptr_t>(S.nodes4) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
     S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
     S.prim_mat = c->upload(h.prim_mat);
     S.prim_emitter = c->upload(h.prim_emitter);

@@ -34,7 +34,7 @@ struct alignas(16) BvhNode {
 
 // 4-wide node (128 B): child boxes as SoA float4 (lo x, lo y, lo z, hi x, hi y, hi z) so a
 // step is 7 independent 16-byte loads; child codes as in BvhNode.
-struct alignas(16) BvhNode4 {
+struct alignas(32) BvhNode4 {
   float lo[3][4];
   float hi[3][4];
   int child[4];
@@ -111,14 +111,17 @@ PXD double triangle_hit(const V3& a, const V3& e1, const V3& e2, const V3& o, co
 }
 
 #if defined(__CUDACC__)
-__device__ __forceinline__ double rec_hit(const PrimRec* __restrict__ rp, const V3& o, const V3& d,
-                                          double t_max, int& id) {
-  const double2* q = reinterpret_cast<const double2*>(rp);
-  double2 w0 = __ldg(q + 0), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3);
-  int2 tail = __ldg(reinterpret_cast<const int2*>(q + 4) + 1);
-  double2 w4 = __ldg(q + 4);
-  id = tail.y;
-  const int shape = tail.x;
+// Primitive test of leaf-ordered record k: 5 x 16-byte loads (a split 64 B + 16 B layout with
+// two 32-byte loads measured slower on C4, 26.9 vs 27.4 Msamples/s). The fp64 test is the
+// reference's, op for op.
+__device__ __forceinline__ double rec_hit(const SceneView& S, int k, const V3& o, const V3& d, double t_max,
+                                          int& id) {
+  const double2* q = reinterpret_cast<const double2*>(S.recs + k);
+  const double2 w0 = __ldg(q + 0), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3);
+  const double2 w4 = __ldg(q + 4);
+  const int2 si = *reinterpret_cast<const int2*>(&w4.y);
+  const int shape = si.x;
+  id = si.y;
   if (shape == kSphere) {
     const double c[3] = {w0.x, w0.y, w1.x};
     return sphere_hit(c, w1.y, o, d, t_max);
@@ -187,10 +190,37 @@ struct Node4Hits {
   unsigned hit;  // bit k: child k's box is hit
 };
 
+#ifndef PXG_NODE256
+#define PXG_NODE256 1
+#endif
+
+// 32-byte non-coherent global load (sm_100: LDG.E.ENL2.256). Scattered node fetches are bound
+// by the L1 data pipe's wavefronts, one per distinct line per load instruction, so fetching a
+// node in 3 x 32 B + 1 x 16 B loads instead of 7 x 16 B cuts the pipe's work per visit.
+__device__ __forceinline__ void ldg256(const void* p, float4& a, float4& b) {
+  unsigned r0, r1, r2, r3, r4, r5, r6, r7;
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+               : "l"(p));
+  a = make_float4(__uint_as_float(r0), __uint_as_float(r1), __uint_as_float(r2), __uint_as_float(r3));
+  b = make_float4(__uint_as_float(r4), __uint_as_float(r5), __uint_as_float(r6), __uint_as_float(r7));
+}
+
+// kWide: 256-bit loads. Only the persistent traversal kernels use them: ptxas 12.9 crashes
+// (segfault) when the v8 load sits in the __noinline__ trace_closest_t / trace_any_t shared
+// by several kernels, so those keep the 128-bit loads.
+template <bool kWide = false>
 __device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, const RayF& rf, float tb) {
   const float4* __restrict__ q = reinterpret_cast<const float4*>(S.nodes4 + node);
-  const float4 lx = __ldg(q + 0), ly = __ldg(q + 1), lz = __ldg(q + 2);
-  const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
+  float4 lx, ly, lz, hx, hy, hz;
+  if (kWide && PXG_NODE256) {
+    ldg256(q + 0, lx, ly);
+    ldg256(q + 2, lz, hx);
+    ldg256(q + 4, hy, hz);
+  } else {
+    lx = __ldg(q + 0), ly = __ldg(q + 1), lz = __ldg(q + 2);
+    hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
+  }
   const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
   Node4Hits r;
   r.hit = 0u;
@@ -289,7 +319,7 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
       if (kCount) cnt->prims += count;
       for (int i = 0; i < count; ++i) {
         int id;
-        const double t = rec_hit(S.recs + first + i, o, d, t_best, id);
+        const double t = rec_hit(S, first + i, o, d, t_best, id);
         if (t > 0.0 && (t < t_best || id > best)) {
           t_best = t;
           best = id;
@@ -329,7 +359,7 @@ __device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const 
       for (int i = 0; i < count; ++i) {
         int id;
         if (kCount) cnt->prims += 1;
-        if (rec_hit(S.recs + first + i, o, d, t_max, id) > 0.0) return true;
+        if (rec_hit(S, first + i, o, d, t_max, id) > 0.0) return true;
       }
     }
     int next = node4_order(node4_inner(h), tb, stack, sp);

@@ -226,13 +226,13 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
 __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack) {
   // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
   // inner children are ordered nearest-first (the next node, then the stack)
-  const Node4Hits h = node4_test(S, ts.node, ts.rf, tbound_f(ts.t_best));
+  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tbound_f(ts.t_best));
   for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
-      const double t = rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id);
+      const double t = rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id);
       if (t > 0.0 && (t < ts.t_best || id > ts.best)) {
         ts.t_best = t;
         ts.best = id;
@@ -251,13 +251,13 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
 __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack) {
   const float tb = tbound_f(ts.t_best);
-  const Node4Hits h = node4_test(S, ts.node, ts.rf, tb);
+  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
   for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
-      if (rec_hit(S.recs + first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
+      if (rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
   }
   int next = node4_order(node4_inner(h), tb, stack, ts.sp);

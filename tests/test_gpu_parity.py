@@ -16,9 +16,10 @@ REL_TOL = 1e-4  # per-path contribution tolerance (north star)
 _ORACLE_SCENES = {}
 
 
-def oracle_scene(oracle, key, sc):
-    """OracleScene per scene key, kept for the session (the 1M-triangle C4 geometry takes
-    ~20 s to serialise and load into the reference)."""
+def oracle_scene(oracle, name, sc):
+    """OracleScene per scene, kept for the session (the 1M-triangle C4 geometry takes ~20 s
+    to serialise and load into the reference)."""
+    key = (name, sc.n_prims, sc.camera.width, sc.camera.height, sc.settings.max_depth, float(sc.a.sum()))
     if key not in _ORACLE_SCENES:
         _ORACLE_SCENES[key] = oracle.OracleScene(sc.to_json())
     return _ORACLE_SCENES[key]
