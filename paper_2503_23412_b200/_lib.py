@@ -114,7 +114,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = [
-    "pxg_default_params", "pxg_abi_version", "pxg_device_count", "pxg_create", "pxg_destroy", "pxg_last_error",
+    "pxg_default_params", "pxg_abi_version", "pxg_node_bytes", "pxg_device_count", "pxg_create", "pxg_destroy", "pxg_last_error",
     "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_render_passes_async", "pxg_snapshot_mean", "pxg_read_snapshot",
     "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_read_diag",
     "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_intersect", "pxg_occluded",

@@ -114,27 +114,28 @@ struct Builder {
   int leaf_max = 1;  // measured best on C2 (fp64 primitive tests dominate); PXG_LEAF overrides
 
   // Binned SAH split of [first, first+count): partitions the range, returns mid and the
-  // child boxes.
+  // child boxes. PXG_SAH_BINS overrides the bin count (tuning experiments).
+  static constexpr int kMaxBins = 64;
   void split(int first, int count, int& mid, Box& lb, Box& rb) {
     Box cb;
     for (int i = first; i < first + count; ++i) cb.grow(prims[i].cen, prims[i].cen);
     mid = -1;
-    const int kBins = 16;
+    static const int kBins = std::getenv("PXG_SAH_BINS") ? std::max(2, std::min(kMaxBins, std::atoi(std::getenv("PXG_SAH_BINS")))) : 16;
     double best_cost = INFINITY;
     int best_axis = -1, best_bin = -1;
     for (int axis = 0; axis < 3; ++axis) {
       const double lo = comp(cb.lo, axis), hi = comp(cb.hi, axis);
       if (!(hi > lo)) continue;
-      Box bb[kBins];
-      int cnt[kBins] = {0};
+      Box bb[kMaxBins];
+      int cnt[kMaxBins] = {0};
       const double scale = kBins / (hi - lo);
       for (int i = first; i < first + count; ++i) {
         int b = std::min(kBins - 1, static_cast<int>((comp(prims[i].cen, axis) - lo) * scale));
         bb[b].grow(prims[i].lo, prims[i].hi);
         ++cnt[b];
       }
-      Box left[kBins];
-      int lc[kBins];
+      Box left[kMaxBins];
+      int lc[kMaxBins];
       Box acc;
       int ac = 0;
       for (int b = 0; b < kBins; ++b) {
@@ -330,6 +331,48 @@ struct Collapser {
   }
 };
 
+// Quantises a 4-wide node's child boxes to 8 bits per plane: origin = the lower corner of
+// the children's union (fp32), grid step 2^e per axis with 255 * 2^e >= extent, lower planes
+// rounded down and upper planes rounded up, so every decoded box contains its fp32 box
+// (checked exactly in double). Empty children (lo > hi) keep their codes, which test nothing.
+HostNode4Q quantize_node(const HostNode4& w) {
+  HostNode4Q q{};
+  float ulo[3] = {INFINITY, INFINITY, INFINITY}, uhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  bool valid[4];
+  for (int k = 0; k < 4; ++k) {
+    valid[k] = w.lo[0][k] <= w.hi[0][k] && w.lo[1][k] <= w.hi[1][k] && w.lo[2][k] <= w.hi[2][k];
+    if (!valid[k]) continue;
+    for (int a = 0; a < 3; ++a) {
+      ulo[a] = std::min(ulo[a], w.lo[a][k]);
+      uhi[a] = std::max(uhi[a], w.hi[a][k]);
+    }
+  }
+  for (int a = 0; a < 3; ++a) {
+    if (!(ulo[a] <= uhi[a])) ulo[a] = uhi[a] = 0.f;
+    q.origin[a] = ulo[a];
+    const double ext = static_cast<double>(uhi[a]) - static_cast<double>(ulo[a]);
+    int e = -126;
+    while (e < 127 && std::ldexp(255.0, e) < ext) ++e;
+    q.exps |= static_cast<unsigned>(e + 127) << (8 * a);
+    const double step = std::ldexp(1.0, e);
+    for (int k = 0; k < 4; ++k) {
+      unsigned lo = 255u, hi = 0u;
+      if (valid[k]) {
+        const double l = std::floor((static_cast<double>(w.lo[a][k]) - ulo[a]) / step);
+        const double u = std::ceil((static_cast<double>(w.hi[a][k]) - ulo[a]) / step);
+        lo = static_cast<unsigned>(std::max(0.0, std::min(255.0, l)));
+        hi = static_cast<unsigned>(std::max(0.0, std::min(255.0, u)));
+        if (!(static_cast<double>(ulo[a]) + lo * step <= w.lo[a][k] && static_cast<double>(ulo[a]) + hi * step >= w.hi[a][k]))
+          throw std::runtime_error("quantize_node: box not contained");
+      }
+      q.qlo[a] |= lo << (8 * k);
+      q.qhi[a] |= hi << (8 * k);
+    }
+  }
+  for (int k = 0; k < 4; ++k) q.child[k] = w.child[k];
+  return q;
+}
+
 }  // namespace
 
 void finalize_scene(const SceneDesc& d, SceneHost& h) {
@@ -437,6 +480,8 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
   h.nodes4.clear();
   h.nodes4.reserve(h.nodes.size() / 2 + 2);
   Collapser{h.nodes, h.nodes4}.build(0);
+  h.nodes4q.resize(h.nodes4.size());
+  for (size_t k = 0; k < h.nodes4.size(); ++k) h.nodes4q[k] = quantize_node(h.nodes4[k]);
   // leaf-ordered exact records
   h.recs.resize(n);
   for (int k = 0; k < n; ++k) {

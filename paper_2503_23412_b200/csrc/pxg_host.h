@@ -36,6 +36,19 @@ struct alignas(16) HostNode4 {
 };
 static_assert(sizeof(HostNode4) == 128, "node4 size");
 
+// Layout-identical to pxg::BvhNode4Q (pxg_scene.cuh), 64 B: the same 4-wide node with its
+// child boxes quantised to 8 bits per plane on a per-node grid (origin + q * 2^e per axis,
+// rounded outward, so the quantised boxes contain the fp32 boxes).
+struct alignas(32) HostNode4Q {
+  float origin[3];
+  unsigned exps;     // byte a: biased exponent of the axis-a grid step 2^(e-127)
+  int child[4];
+  unsigned qlo[3];   // byte k of qlo[a]: child k's lower plane on axis a
+  unsigned qhi[3];
+  unsigned pad[2];
+};
+static_assert(sizeof(HostNode4Q) == 64, "node4q size");
+
 struct SceneHost {
   std::vector<int> prim_mat, prim_shape, prim_emitter;
   std::vector<double> prim_geo;     // [n][3]
@@ -48,6 +61,7 @@ struct SceneHost {
   double tan_half = 0.0, aspect = 1.0;
   std::vector<HostNode> nodes;
   std::vector<HostNode4> nodes4;
+  std::vector<HostNode4Q> nodes4q;
   std::vector<int> order;
   std::vector<HostRec> recs;
   int bvh_depth = 0;

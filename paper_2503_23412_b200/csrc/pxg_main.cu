@@ -805,6 +805,8 @@ void pxg_default_params(pxg_params* p) {
 
 int pxg_abi_version(void) { return PXG_ABI_VERSION; }
 
+int pxg_node_bytes(void) { return PXG_NODEQ ? static_cast<int>(sizeof(BvhNode4Q)) : static_cast<int>(sizeof(BvhNode4)); }
+
 int pxg_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -904,6 +906,8 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
     S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
     if (reinterpret_cast<uintptr_t>(S.nodes4) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
+    S.nodes4q = reinterpret_cast<const BvhNode4Q*>(c->upload(h.nodes4q));
+    if (reinterpret_cast<uintptr_t>(S.nodes4q) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
     S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
     S.prim_mat = c->upload(h.prim_mat);
     S.prim_emitter = c->upload(h.prim_emitter);

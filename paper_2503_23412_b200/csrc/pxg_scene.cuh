@@ -41,6 +41,18 @@ struct alignas(32) BvhNode4 {
   int pad[4];
 };
 
+// Quantised 4-wide node (64 B, two 32-byte loads): child planes on a per-node grid,
+// plane = origin + q * 2^(e-127) per axis (q = byte k of qlo/qhi), rounded outward on the host
+// so the decoded boxes contain the fp32 boxes of BvhNode4 (pxg_host.cpp quantize_node).
+struct alignas(32) BvhNode4Q {
+  float origin[3];
+  unsigned exps;
+  int child[4];
+  unsigned qlo[3];
+  unsigned qhi[3];
+  unsigned pad[2];
+};
+
 struct alignas(16) PrimRec {
   double a[3];
   double e1[3];
@@ -52,6 +64,7 @@ struct alignas(16) PrimRec {
 struct SceneView {
   const BvhNode* nodes;
   const BvhNode4* nodes4;
+  const BvhNode4Q* nodes4q;
   const PrimRec* recs;
   const int* prim_mat;       // [n_prims]
   const int* prim_emitter;   // [n_prims] emitter index or -1
@@ -209,8 +222,61 @@ __device__ __forceinline__ void ldg256(const void* p, float4& a, float4& b) {
 // kWide: 256-bit loads. Only the persistent traversal kernels use them: ptxas 12.9 crashes
 // (segfault) when the v8 load sits in the __noinline__ trace_closest_t / trace_any_t shared
 // by several kernels, so those keep the 128-bit loads.
+#ifndef PXG_NODEQ
+#define PXG_NODEQ 1
+#endif
+
+__device__ __forceinline__ float qbyte(unsigned w, int k) { return static_cast<float>((w >> (8 * k)) & 0xffu); }
+
+// Box tests of a quantised node: per axis t = q * (step * inv) + (origin - o) * inv, i.e. the
+// slab distance of the decoded plane (one FFMA per plane after 2 per axis), conservative
+// like box_f (the fp32 rounding is far inside the boxes' padding, see box_f).
+// kWide: two 32-byte loads (persistent kernels); otherwise four 16-byte loads (the
+// __noinline__ single-ray traversal, where ptxas 12.9 rejects the 32-byte form, see below).
+template <bool kWide>
+__device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, const RayF& rf, float tb) {
+  float4 a, b, c, d;
+  if (kWide) {
+    ldg256(S.nodes4q + node, a, b);
+    ldg256(reinterpret_cast<const char*>(S.nodes4q + node) + 32, c, d);
+  } else {
+    const float4* q = reinterpret_cast<const float4*>(S.nodes4q + node);
+    a = __ldg(q + 0);
+    b = __ldg(q + 1);
+    c = __ldg(q + 2);
+    d = __ldg(q + 3);
+  }
+  const unsigned ex = __float_as_uint(a.w);
+  const float sx = __uint_as_float((ex & 0xffu) << 23), sy = __uint_as_float(((ex >> 8) & 0xffu) << 23),
+              sz = __uint_as_float(((ex >> 16) & 0xffu) << 23);
+  const float Ax = sx * rf.ix, Ay = sy * rf.iy, Az = sz * rf.iz;
+  const float Bx = __fmaf_rn(a.x, rf.ix, rf.nx), By = __fmaf_rn(a.y, rf.iy, rf.ny), Bz = __fmaf_rn(a.z, rf.iz, rf.nz);
+  const unsigned lxw = __float_as_uint(c.x), lyw = __float_as_uint(c.y), lzw = __float_as_uint(c.z);
+  const unsigned hxw = __float_as_uint(c.w), hyw = __float_as_uint(d.x), hzw = __float_as_uint(d.y);
+  Node4Hits r;
+  r.hit = 0u;
+  r.code[0] = __float_as_int(b.x);
+  r.code[1] = __float_as_int(b.y);
+  r.code[2] = __float_as_int(b.z);
+  r.code[3] = __float_as_int(b.w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float tx0 = __fmaf_rn(qbyte(lxw, k), Ax, Bx), tx1 = __fmaf_rn(qbyte(hxw, k), Ax, Bx);
+    const float ty0 = __fmaf_rn(qbyte(lyw, k), Ay, By), ty1 = __fmaf_rn(qbyte(hyw, k), Ay, By);
+    const float tz0 = __fmaf_rn(qbyte(lzw, k), Az, Bz), tz1 = __fmaf_rn(qbyte(hzw, k), Az, Bz);
+    const float t0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+    const float t1 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tb));
+    if (t0 <= t1) r.hit |= 1u << k;
+    r.tn[k] = t0;
+  }
+  return r;
+}
+
 template <bool kWide = false>
 __device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, const RayF& rf, float tb) {
+  // the single-ray path keeps the 128 B nodes: 4 x 16 B loads of the quantised node plus its
+  // decode measured 1% slower there (C4, same box)
+  if (kWide && PXG_NODEQ) return node4q_test<true>(S, node, rf, tb);
   const float4* __restrict__ q = reinterpret_cast<const float4*>(S.nodes4 + node);
   float4 lx, ly, lz, hx, hy, hz;
   if (kWide && PXG_NODE256) {
@@ -275,6 +341,30 @@ __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* s
   for (int k = 3; k >= 1; --k)
     if (c[k] != kNoChild && sp < kStack) stack[sp++] = c[k];
   return c[0];
+}
+
+#ifndef PXG_PREFETCH
+#define PXG_PREFETCH 0  // measured: -1% on C2 and C4
+#endif
+
+// The nearest hit inner child of h (kNoChild if none), before the leaf tests of the step
+// tighten t_best: its node is prefetched into L1 so the fetch latency overlaps the fp64
+// primitive tests (the visit order itself is decided after them, as before).
+__device__ __forceinline__ void node4_prefetch_nearest(const SceneView& S, const Node4Hits& h) {
+#if PXG_PREFETCH
+  float bt = __int_as_float(0x7f800000);
+  int bc = kNoChild;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool ok = (h.hit >> k & 1u) && h.code[k] >= 0 && h.tn[k] < bt;
+    bt = ok ? h.tn[k] : bt;
+    bc = ok ? h.code[k] : bc;
+  }
+  if (bc != kNoChild) {
+    if (PXG_NODEQ) asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4q + bc));
+    else asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4 + bc));
+  }
+#endif
 }
 
 // Hit leaf children of a visited node (bit k of the result: child k is a hit leaf).

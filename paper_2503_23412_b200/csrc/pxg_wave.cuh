@@ -223,13 +223,18 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
 
 // Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
 // ts.node holds a child code: >= 0 a 4-wide node, < 0 a leaf.
-__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack) {
+template <bool kCount = false>
+__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack, TravCount* cnt = nullptr) {
   // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
   // inner children are ordered nearest-first (the next node, then the stack)
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tbound_f(ts.t_best));
-  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+  if (kCount) cnt->nodes += 1;
+  const unsigned leaves0 = node4_leaves(h);
+  if (leaves0) node4_prefetch_nearest(S, h);
+  for (unsigned leaves = leaves0; leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
+    if (kCount) cnt->prims += count;
     for (int i = 0; i < count; ++i) {
       int id;
       const double t = rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id);
@@ -249,14 +254,19 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
 }
 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
-__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack) {
+template <bool kCount = false>
+__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack, TravCount* cnt = nullptr) {
   const float tb = tbound_f(ts.t_best);
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
-  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
+  if (kCount) cnt->nodes += 1;
+  const unsigned leaves0 = node4_leaves(h);
+  if (leaves0) node4_prefetch_nearest(S, h);
+  for (unsigned leaves = leaves0; leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
       int id;
+      if (kCount) cnt->prims += 1;
       if (rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
   }
@@ -317,16 +327,19 @@ __global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueu
   }
 }
 
-// Instrumented copies of the traversal kernels for the roofline measurement: the same
-// traversal code on the same queue, counting node visits (128 B 4-wide nodes) and primitive tests
-// (80 B each). Launched after the timed launch; results are identical and discarded.
+// Instrumented copies of the traversal kernels for the roofline measurement: the same step
+// functions on the same queue, counting node visits (pxg_node_bytes() each: 64 B quantised
+// 4-wide nodes) and primitive tests (80 B each). Launched after the timed launch; results
+// are identical and discarded.
 __global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, unsigned long long* acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *Q.count) return;
-  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
-  double t_best = r1.z;
+  TravState ts;
+  int stack[kStack];
+  trav_init(ts, Q, j);
   TravCount c{0, 0};
-  trace_closest_t<true>(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), t_best, &c);
+  while (!closest_step<true>(S, ts, stack, &c)) {
+  }
   atomicAdd(acc + 0, 1ull);
   atomicAdd(acc + 1, c.nodes);
   atomicAdd(acc + 2, c.prims);
@@ -335,9 +348,12 @@ __global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, 
 __global__ void __launch_bounds__(128) k_anyhit_count(SceneView S, RayQueue Q, unsigned long long* acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *Q.count) return;
-  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  TravState ts;
+  int stack[kStack];
+  trav_init(ts, Q, j);
   TravCount c{0, 0};
-  trace_any_t<true>(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), r1.z, &c);
+  while (any_step<true>(S, ts, stack, &c) == 0) {
+  }
   atomicAdd(acc + 0, 1ull);
   atomicAdd(acc + 1, c.nodes);
   atomicAdd(acc + 2, c.prims);
