@@ -190,6 +190,9 @@ struct pxg_ctx {
   int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
+  int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
+  PV* d_rw_scratch = nullptr; // candidate vertices of k_recip_eval_wave: [wave_blocks][kRW][4]
+  double* d_rw_ends = nullptr; // its visibility segment endpoints: [wave_blocks][kRW][10][6]
   int dfs_blocks = 0;         // grid-stride warp-DFS grid
   int sel_cap = 0;            // shared-memory capacity (entries) of the pool selection
   size_t sel_smem = 0;
@@ -515,9 +518,14 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
     k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, bs, c->d_rstate, c->d_ract[0], c->d_rnact,
                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc);
     c->recip_rounds = recip_rounds(st, cap, c->d_rnact, [&](int cur, int chunk) {
-      k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
-          c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
-          c->d_rn, c->d_re);
+      if (c->wave_blocks > 0)
+        k_recip_eval_wave<<<c->wave_blocks, kRW, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur],
+                                                          c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn,
+                                                          c->d_re, c->d_rw_scratch, c->d_rw_ends);
+      else
+        k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
+            c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
+            c->d_rn, c->d_re);
       k_recip_dfs_warp<128><<<c->dfs_blocks, 128, 0, st>>>(R, stride, cap, bs, 0.0, c->d_ract[cur],
                                                     c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
                                                     c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
@@ -1142,6 +1150,15 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, k_recip_dfs_warp<128>, 128, 0));
       c->eval_blocks = std::max(1, sms * std::max(pe, 1));
       c->dfs_blocks = std::max(1, sms * std::max(pd, 1));
+      // PXG_RECIP_WAVE=0 selects the thread-per-node evaluation (A/B experiments)
+      static const bool wave = !std::getenv("PXG_RECIP_WAVE") || std::atoi(std::getenv("PXG_RECIP_WAVE")) != 0;
+      if (wave && c->proxy_on) {
+        int pw = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k_recip_eval_wave, kRW, 0));
+        c->wave_blocks = std::max(1, sms * std::max(pw, 1));
+        c->d_rw_scratch = c->alloc<PV>(static_cast<size_t>(c->wave_blocks) * kRW * 4);
+        c->d_rw_ends = c->alloc<double>(static_cast<size_t>(c->wave_blocks) * kRW * 60);
+      }
     }
     c->d_diag = c->zeros<long long>(kBuckets * 5);
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);

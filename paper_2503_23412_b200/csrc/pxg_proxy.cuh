@@ -138,8 +138,19 @@ struct Cand {
   bool escaped;
 };
 
+// Visibility of segment (a, b) as the reference evaluates it (visible(a, b), scene.hpp:86-87).
+// `seg` names the segment within one node evaluation (0-3: support chain, 4: control -> g0,
+// 5-9: target chain), so the reciprocal-node wavefront can trace them all as one queue and
+// replay the same code with the results (k_recip_eval_wave).
+struct VisDirect {
+  const SceneView* S;
+  __device__ __forceinline__ bool operator()(int, const V3& a, const V3& b) const { return visible(*S, a, b); }
+};
+
 // support_pdf (proxy.cpp:153-209)
-__device__ __forceinline__ double support_pdf(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g) {
+template <class Vis>
+__device__ __forceinline__ double support_pdf_v(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g,
+                                                const Vis& vis) {
   const int u = h.u;
   const PV* hc = inc_control(h, prefix);
   const PV& y = h.spec_end;
@@ -158,7 +169,7 @@ __device__ __forceinline__ double support_pdf(const SceneView& S, const IncHdr& 
       V3 dir = d / len;
       double pdf_w = (j == 0) ? sphere_cosine_pdf(y.n, dir)
                               : pdf_bsdf(S.materials[prev->mat], prev->n, normalize(before->p - prev->p), dir);
-      if (pdf_w <= 0.0 || !visible(S, prev->p, nxt.p)) {
+      if (pdf_w <= 0.0 || !vis(j, prev->p, nxt.p)) {
         q_fs = 0.0;
         break;
       }
@@ -178,10 +189,14 @@ __device__ __forceinline__ double support_pdf(const SceneView& S, const IncHdr& 
       V3 dir = d / len;
       double pdf_w = h.has_cdir ? pdf_bsdf(S.materials[hc->mat], hc->n, -h.cdir, dir)
                                 : light_direction_pdf(hc->n, dir);
-      if (pdf_w > 0.0 && visible(S, hc->p, g[0].p)) q_other = to_area_density(pdf_w, hc->p, g[0].p, g[0].n);
+      if (pdf_w > 0.0 && vis(4, hc->p, g[0].p)) q_other = to_area_density(pdf_w, hc->p, g[0].p, g[0].n);
     }
   }
   return 0.5 * (q_other + q_fs);
+}
+
+__device__ __forceinline__ double support_pdf(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g) {
+  return support_pdf_v(S, h, prefix, g, VisDirect{&S});
 }
 
 // support_sample (proxy.cpp:211-269)
@@ -261,7 +276,9 @@ __device__ __forceinline__ void support_sample(const SceneView& S, const IncHdr&
 }
 
 // target_density (proxy.cpp:106-151); g has exactly u vertices.
-__device__ __forceinline__ double target_density(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g) {
+template <class Vis>
+__device__ __forceinline__ double target_density_v(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g,
+                                                   const Vis& vis) {
   const int u = h.u;
   for (int i = 0; i + 1 < u; ++i)
     if (!specmat(S, g[i])) return 0.0;
@@ -284,7 +301,7 @@ __device__ __forceinline__ double target_density(const SceneView& S, const IncHd
     V3 dir = d / len;
     double pdf_w = (!hc || !h.has_cdir) ? light_direction_pdf(a.n, dir)
                                         : pdf_bsdf(S.materials[a.mat], a.n, -h.cdir, dir);
-    if (pdf_w <= 0.0 || !visible(S, a.p, b.p)) return 0.0;
+    if (pdf_w <= 0.0 || !vis(5, a.p, b.p)) return 0.0;
     f *= to_area_density(pdf_w, a.p, b.p, b.n);
   }
   for (int k = 1; k + 1 < m; ++k) {
@@ -295,10 +312,14 @@ __device__ __forceinline__ double target_density(const SceneView& S, const IncHd
     double len = length(d);
     if (len <= 0.0) return 0.0;
     double pdf_w = pdf_bsdf(S.materials[a.mat], a.n, wi, d / len);
-    if (pdf_w <= 0.0 || !visible(S, a.p, b.p)) return 0.0;
+    if (pdf_w <= 0.0 || !vis(5 + k, a.p, b.p)) return 0.0;
     f *= to_area_density(pdf_w, a.p, b.p, b.n);
   }
   return f;
+}
+
+__device__ __forceinline__ double target_density(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g) {
+  return target_density_v(S, h, prefix, g, VisDirect{&S});
 }
 
 

@@ -453,6 +453,268 @@ __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride
   }
 }
 
+// Phase A as a block-local wavefront (same values as k_recip_eval, bit for bit). A node's
+// draw_g is a chain of up to 4 closest-hit rays (support_sample) and up to 10 visibility rays
+// (support_pdf + target_density); one thread per node running them back to back leaves most
+// lanes idle (nodes escape after 1 ray or run all 14). Here a block takes 128 nodes at a time:
+// every node's glue code runs on its own thread, but each ray phase traces only the rays that
+// exist, compacted onto the first threads of the block: (1) sampling chain, <= 4 rounds of
+// compacted closest-hit rays; (2) the visibility segments of every node (the density code run
+// with a functor that records them and their endpoints, VisDirect's segment ids) as one
+// compacted any-hit list; (3) the density code run again with the traced results. Candidate
+// vertices and segment endpoints live in a global scratch slot per (block, node).
+// Scene::intersect / visible through the persistent kernels' step functions (quantised
+// nodes, 32-byte loads), inlined: same hits as intersect() / visible() (closest hit with the
+// id tie rule and the any-hit boolean do not depend on the visiting order).
+__device__ __forceinline__ bool wave_intersect(const SceneView& S, const V3& o, const V3& d, Hit& hit) {
+  TravState ts;
+  ts.o = o;
+  ts.d = d;
+  ts.rf = make_rayf(o, d);
+  ts.t_best = 1e30;
+  ts.best = -1;
+  ts.node = 0;
+  ts.sp = 0;
+  int stack[kStack];
+  while (!closest_step(S, ts, stack)) {
+  }
+  if (ts.best < 0) return false;
+  hit.t = ts.t_best;
+  hit.p = o + ts.t_best * d;
+  hit.prim = ts.best;
+  hit.n = prim_normal(S, ts.best, hit.p);
+  hit.material = S.prim_mat[ts.best];
+  hit.emitter = S.prim_emitter[ts.best];
+  return true;
+}
+
+__device__ __forceinline__ bool wave_visible(const SceneView& S, const V3& from, const V3& to) {
+  const V3 d = to - from;
+  const double dist = length(d);
+  if (dist < kRayEps) return true;
+  TravState ts;
+  ts.o = from;
+  ts.d = d / dist;
+  ts.rf = make_rayf(ts.o, ts.d);
+  ts.t_best = dist * (1.0 - 1e-6);
+  ts.best = -1;
+  ts.node = 0;
+  ts.sp = 0;
+  int stack[kStack];
+  int r;
+  while ((r = any_step(S, ts, stack)) == 0) {
+  }
+  return r != 1;
+}
+
+constexpr int kRW = 128;  // nodes per block batch = threads per block
+enum { kRWNone = 0, kRWRay = 1, kRWSampled = 2, kRWEscaped = 3 };
+
+struct VisRecord {  // phase 2a: record every segment the density code asks for, answer "visible"
+  unsigned* mask;
+  double* ends;  // [10][6]: the segment's endpoints a, b
+  __device__ __forceinline__ bool operator()(int seg, const V3& a, const V3& b) const {
+    *mask |= 1u << seg;
+    double* e = ends + 6 * seg;
+    e[0] = a.x, e[1] = a.y, e[2] = a.z, e[3] = b.x, e[4] = b.y, e[5] = b.z;
+    return true;
+  }
+};
+struct VisReplay {  // phase 2c: answer from the traced results
+  unsigned vis;
+  __device__ __forceinline__ bool operator()(int seg, const V3&, const V3&) const { return (vis >> seg) & 1u; }
+};
+__global__ void __launch_bounds__(kRW) k_recip_eval_wave(SceneView S, uint64_t seed, int repeats, int stride,
+                                                          long long cap, const __grid_constant__ BatchSet bs,
+                                                          const int* active, const int* n_active, int chunk,
+                                                          const RunState* st, double* g, long long* nsplit,
+                                                          int* nerr, PV* scratch, double* seg_ends) {
+  __shared__ int s_j[kRW], s_k[kRW];
+  __shared__ unsigned s_ctr[kRW], s_need[kRW], s_vis[kRW];
+  __shared__ unsigned char s_state[kRW], s_strand[kRW], s_step[kRW];
+  __shared__ int s_src[kRW];  // ray origin: -1 spec_end, -2 control vertex, j >= 0 candidate vertex j
+  __shared__ double s_dir[kRW][3];
+  __shared__ short s_list[kRW];
+  __shared__ unsigned short s_seg[kRW * 10];
+  __shared__ int s_n, s_nseg;
+  const int t = threadIdx.x;
+  PV* gv = scratch + (static_cast<size_t>(blockIdx.x) * kRW + t) * 4;  // this thread's node's candidate
+  double* ends_block = seg_ends + static_cast<size_t>(blockIdx.x) * kRW * 60;  // [node][seg][6]
+  const long long total = static_cast<long long>(*n_active) * chunk;
+  for (long long base = static_cast<long long>(blockIdx.x) * kRW; base < total;
+       base += static_cast<long long>(gridDim.x) * kRW) {
+    // ---- setup + first ray of support_sample (proxy.cpp:211-269)
+    const long long tid = base + t;
+    int j = -1, k = -1;
+    unsigned char state = kRWNone;
+    if (tid < total) {
+      j = active[tid / chunk];
+      const long long kk = st[j].avail + tid % chunk;
+      if (kk < cap) k = static_cast<int>(kk);
+    }
+    if (k >= 0) {
+      const BatchPass& P = bs.p[j / stride];
+      const int w = j % stride;
+      const int e = w / repeats, r = w % repeats;
+      const IncHdr& h = P.inc[e];
+      const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+      Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k), pxg_recip_stream(P.pass, h.walk, h.end, r));
+      const PV* hc = inc_control(h, pre);
+      const int strand = (h.u == 1) ? static_cast<int>(nr.next_below(2)) : 0;
+      s_strand[t] = static_cast<unsigned char>(strand);
+      s_step[t] = 0;
+      if (strand == 1 && hc == nullptr) {
+        LightPoint lp = sample_light_point(S, nr);
+        PV v;
+        v.p = lp.p;
+        v.n = lp.n;
+        v.wi = v3(0.0);
+        v.thr = v3(1.0);
+        v.pdf_fwd = 0.0;
+        v.mat = S.prim_mat[lp.prim];
+        v.prim = lp.prim;
+        v.emitter = S.prim_emitter[lp.prim];
+        v.flag = kLight;
+        v.pad = 0.0;
+        gv[0] = v;
+        state = kRWSampled;
+      } else if (strand == 1) {
+        V3 dir;
+        state = kRWRay;
+        if (h.has_cdir) {
+          BsdfSample b = sample_bsdf(S.materials[hc->mat], hc->n, -h.cdir, nr);
+          if (!b.valid || b.pdf <= 0.0) state = kRWEscaped;
+          dir = b.wo;
+        } else {
+          dir = sample_cosine_hemisphere(hc->n, nr);
+        }
+        s_src[t] = -2;
+        s_dir[t][0] = dir.x, s_dir[t][1] = dir.y, s_dir[t][2] = dir.z;
+      } else {
+        V3 axis = nr.next_double() < 0.5 ? h.spec_end.n : -h.spec_end.n;
+        V3 dir = sample_cosine_hemisphere(axis, nr);
+        s_src[t] = -1;
+        s_dir[t][0] = dir.x, s_dir[t][1] = dir.y, s_dir[t][2] = dir.z;
+        state = kRWRay;
+      }
+      s_ctr[t] = nr.r.i;
+    }
+    s_j[t] = j;
+    s_k[t] = k;
+    s_state[t] = state;
+    // ---- (1) sampling chain: <= 4 rounds of compacted closest-hit rays
+    for (int round = 0; round < 4; ++round) {
+      if (t == 0) s_n = 0;
+      __syncthreads();
+      if (s_state[t] == kRWRay) s_list[atomicAdd(&s_n, 1)] = static_cast<short>(t);
+      __syncthreads();
+      const int nray = s_n;
+      if (nray == 0) break;  // block-uniform
+      if (t < nray) {
+        const int q = s_list[t];
+        const int jq = s_j[q];
+        const BatchPass& P = bs.p[jq / stride];
+        const int e = (jq % stride) / repeats;
+        const IncHdr& h = P.inc[e];
+        const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+        PV* gq = scratch + (static_cast<size_t>(blockIdx.x) * kRW + q) * 4;
+        const int src = s_src[q];
+        const V3 o = src == -1 ? h.spec_end.p : (src == -2 ? inc_control(h, pre)->p : gq[src].p);
+        const V3 d = v3(s_dir[q][0], s_dir[q][1], s_dir[q][2]);
+        Hit hit;
+        if (!wave_intersect(S, o, d, hit)) {
+          s_state[q] = kRWEscaped;
+        } else {
+          gq[s_strand[q] == 1 ? 0 : s_step[q]] = vertex_from_hit(S, hit, -d);
+          s_state[q] = kRWSampled;  // provisional: the glue below decides
+        }
+      }
+      __syncthreads();
+      // glue: continue the chain of the nodes that just got a vertex (strand 0, u > step+1)
+      if (k >= 0 && state == kRWRay) {
+        state = s_state[t];
+        if (state == kRWSampled && s_strand[t] == 0) {
+          const BatchPass& P = bs.p[j / stride];
+          const int e = (j % stride) / repeats;
+          const IncHdr& h = P.inc[e];
+          const int step = s_step[t] + 1;
+          s_step[t] = static_cast<unsigned char>(step);
+          if (step < h.u) {
+            Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(k),
+                              pxg_recip_stream(P.pass, h.walk, h.end, (j % stride) % repeats));
+            nr.r.i = s_ctr[t];
+            const PV& prev = gv[step - 1];
+            BsdfSample b = sample_bsdf(S.materials[prev.mat], prev.n, prev.wi, nr);
+            s_ctr[t] = nr.r.i;
+            if (!b.valid || b.pdf <= 0.0) {
+              state = kRWEscaped;
+            } else {
+              s_src[t] = step - 1;
+              s_dir[t][0] = b.wo.x, s_dir[t][1] = b.wo.y, s_dir[t][2] = b.wo.z;
+              state = kRWRay;
+            }
+          }
+        }
+        s_state[t] = state;
+      }
+    }
+    // ---- (2a) record the visibility segments the densities ask for
+    if (t == 0) s_nseg = 0;
+    __syncthreads();
+    unsigned need = 0;
+    if (k >= 0 && state == kRWSampled) {
+      const BatchPass& P = bs.p[j / stride];
+      const int e = (j % stride) / repeats;
+      const IncHdr& h = P.inc[e];
+      const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+      const VisRecord rec{&need, ends_block + t * 60};
+      const double q = support_pdf_v(S, h, pre, gv, rec);
+      if (q > 0.0) target_density_v(S, h, pre, gv, rec);
+      for (unsigned m = need; m; m &= m - 1)
+        s_seg[atomicAdd(&s_nseg, 1)] = static_cast<unsigned short>(t * 16 + (__ffs(m) - 1));
+    }
+    s_need[t] = need;
+    s_vis[t] = 0u;
+    __syncthreads();
+    // ---- (2b) trace the recorded segments, compacted over the block
+    const int nseg = s_nseg;
+    for (int i = t; i < nseg; i += kRW) {
+      const int q = s_seg[i] >> 4, sg = s_seg[i] & 15;
+      const double* e = ends_block + q * 60 + 6 * sg;
+      if (wave_visible(S, v3(e[0], e[1], e[2]), v3(e[3], e[4], e[5]))) atomicOr(&s_vis[q], 1u << sg);
+    }
+    __syncthreads();
+    // ---- (2c) the densities with the traced visibilities; draw_g (recip.hpp:69-77), split
+    if (k >= 0) {
+      const BatchPass& P = bs.p[j / stride];
+      const int w = j % stride;
+      const int e = w / repeats, r = w % repeats;
+      const IncHdr& h = P.inc[e];
+      const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+      const double B = P.bound[e];
+      double qx = 1.0, fx = 0.0;
+      if (state == kRWSampled) {
+        const VisReplay vr{s_vis[t]};
+        qx = support_pdf_v(S, h, pre, gv, vr);
+        if (!(qx > 0.0)) qx = 1.0;  // escaped (support_sample's q <= 0 branch)
+        else fx = target_density_v(S, h, pre, gv, vr);
+      }
+      int err = 0;
+      if (!isfinite(fx) || fx < 0.0) err = kErrIntegrand;
+      else if (!isfinite(qx) || qx <= 0.0) err = kErrSupport;
+      const double gval = 1.0 - fx / (B * qx);
+      long long n = 0;
+      if (!err) {
+        Rng sr = make_rng(seed, PXG_KIND_RECIP_SPLIT, static_cast<uint32_t>(k), pxg_recip_stream(P.pass, h.walk, h.end, r));
+        n = split_count(gval, sr, err);
+      }
+      const size_t o = static_cast<size_t>(j) * cap + k;
+      store_node(g + o, nsplit + o, nerr + o, gval, B, n, err);
+    }
+    __syncthreads();  // s_* reused by the next batch
+  }
+}
+
 // The two-point fixture f = {1, 3}, q = 1/2 (proj/tests/test_recip.cpp:16-23) as Phase A.
 __global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, const int* active, const int* n_active,
                                 int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
@@ -615,8 +877,17 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
     }
     const int slot = static_cast<int>(s.depth % W);
     const double pa = sa[slot] + static_cast<double>(sg[slot]) * s.ret;
-    const long long rem = sr[slot];
+    long long rem = sr[slot];
     sa[slot] = pa;
+    // Once cost reaches the cap, every further main_tree call returns 0 from its guard
+    // (recip.hpp:79-85) and adds sgn * 0.0 to its parent, which leaves the parent's sum
+    // unchanged (it is never -0.0). The reference still loops over all remaining split
+    // children (up to |g| of them); here they are skipped, with the same truncation flag.
+    if (rem > 0 && s.cost >= cap) {
+      s.truncated = 1;
+      rem = 0;
+      sr[slot] = 0;
+    }
     if (rem > 0) {
       sr[slot] = rem - 1;
       ++s.depth;
