@@ -35,12 +35,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "Msamples/s (full proxy-BDPT px samples)"
-PRIM_BYTES = 80  # PrimRec (csrc/pxg_scene.cuh); node bytes: pxg_node_bytes() (64 B BvhNode4Q)
-
-
-def node_bytes():
-    from paper_2503_23412_b200 import _lib
-    return int(_lib.lib().pxg_node_bytes())
+PRIM_BYTES = 80  # PrimRec (csrc/pxg_scene.cuh); node bytes per context: pxg_node_bytes (64 or 128)
 
 
 def parse():
@@ -277,6 +272,7 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
     # steady-state one
     r.set_pass_limit(-1)
     tr = r.measure_traversal(BATCH) if not quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
+    nb = r.node_bytes()
     r.close()
     peak, peak_src = measured_peak_gbs()
     roof = {}
@@ -284,7 +280,7 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
         m = tr[kind]
         if m["launches"] <= 0 or m["ms"] <= 0:
             continue
-        bytes_total = m["nodes"] * node_bytes() + m["prims"] * PRIM_BYTES
+        bytes_total = m["nodes"] * nb + m["prims"] * PRIM_BYTES
         roof[kind] = {"kernel": kname, "launches": int(m["launches"]), "rays": int(m["rays"]),
                       "bytes_per_ray": round(bytes_total / max(m["rays"], 1), 1),
                       "nodes_per_ray": round(m["nodes"] / max(m["rays"], 1), 2),
@@ -298,7 +294,7 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
         roofline = {"bound": "hbm", "achieved": round(d["achieved_gbs"], 1), "peak": peak, "unit": "GB/s",
                     "frac": round(d["achieved_gbs"] / peak, 4), "traffic": ncu_traffic(cfg, d["kernel"]),
                     "kernel": d["kernel"], "peak_source": peak_src,
-                    "algorithmic_bytes": f"{node_bytes()} B per BVH node visit + {PRIM_BYTES} B per primitive test, "
+                    "algorithmic_bytes": f"{nb} B per BVH node visit + {PRIM_BYTES} B per primitive test, "
                                          "counted by an instrumented copy on the same rays",
                     "per_kernel": roof}
     return {"value": value, "dev_ms": dev_ms, "warm": warm, "counts": counts, "stage_ms": stage_ms,

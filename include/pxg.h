@@ -120,14 +120,15 @@ int pxg_snapshot_mean(pxg_ctx* ctx, int slot);
 int pxg_read_snapshot(pxg_ctx* ctx, int slot, double* rgb, int* passes_done);
 /* Renders `n` passes in measurement mode: every traversal launch (closest hit / any hit)
  * is bracketed by CUDA events on its stream and followed by an instrumented copy on the
- * same rays that counts 4-wide BVH node visits (pxg_node_bytes() each) and primitive tests
+ * same rays that counts 4-wide BVH node visits (pxg_node_bytes(ctx) each) and primitive tests
  * (80 B each).
  * out[10] = {closest: ms, launches, rays, node visits, prim tests,
  *            any-hit: ms, launches, rays, node visits, prim tests}. */
 int pxg_measure_traversal(pxg_ctx* ctx, int n, double* out);
-/* Bytes of one BVH node visit of the persistent traversal kernels (the roofline's
- * algorithmic bytes per node: 64 for the quantised 4-wide node). */
-int pxg_node_bytes(void);
+/* Bytes of one BVH node visit of this context's persistent traversal kernels (the
+ * roofline's algorithmic bytes per node): 64 for the quantised 4-wide node (scenes whose
+ * 128 B node array exceeds 16 MB), 128 otherwise. */
+int pxg_node_bytes(const pxg_ctx* ctx);
 int pxg_synchronize(pxg_ctx* ctx);
 
 /* Running mean acc/done over this context's rows, row-major fp64 RGB, y = 0 top

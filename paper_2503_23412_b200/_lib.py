@@ -105,6 +105,7 @@ def lib():
     L.pxg_dump_pool.argtypes = [C.c_void_p, C.c_int, _IP, _LP, _IP, _IP, _IP, _DP, _DP, _DP]
     L.pxg_intersect.argtypes = [C.c_void_p, C.c_int, _DP, _DP, _IP, _DP]
     L.pxg_occluded.argtypes = [C.c_void_p, C.c_int, _DP, _IP]
+    L.pxg_node_bytes.argtypes = [C.c_void_p]
     L.pxg_render_pt.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int, _DP]
     L.pxg_recip_twopoint.argtypes = [C.c_int, C.c_double, C.c_longlong, C.c_uint64, _DP, _LP, _IP]
     L.pxg_rng_draws.argtypes = [C.c_uint64, C.c_uint, C.c_uint, C.c_uint64, C.c_int, C.POINTER(C.c_uint)]

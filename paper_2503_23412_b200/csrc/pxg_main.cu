@@ -94,6 +94,21 @@ struct pxg_ctx {
   pxg_shard shard{};
   uint64_t seed = 0;
   int width = 0, height = 0, max_depth = 0, n = 0, n_px_total = 0, row0 = 0, rows = 0;
+  // Stage-2 row tiles: a pass runs Stage 2 over [row0_ctx, row0_ctx + rows_ctx) in tiles of
+  // tile_rows rows (a multiple of the 10-row gate grid) so the per-pixel working set of a
+  // 4K depth-16 image fits in HBM. Per-pixel state that outlives a tile (RNG counters, film,
+  // the pass values and gamma contributions in pixel order, the gate grid) is full-size; the
+  // vertex pools, connection slots and queues are tile-size. n / row0 / rows / n_cells and the
+  // full-size pointers below describe the active tile while Stage 2 is enqueued, the whole
+  // context otherwise (activate_tile / activate_ctx).
+  int n_ctx = 0, row0_ctx = 0, rows_ctx = 0, n_cells_ctx = 0, tile_rows = 0, ntiles = 1;
+  long long tile_step = 0;  // (pass, tile) steps enqueued: parity selects the vertex-pool buffer
+  struct FullView {
+    unsigned* ctr;
+    double *bdpt, *val, *acc, *gval, *grid_total, *grid_proxy;
+    ProxRec* prox;
+    int *pflags, *gbin, *eye_prims, *light_prims;
+  } full{};
   int light_walks = 0;
   int grid_w = 0, grid_h = 0, n_cells = 0;
   bool proxy_on = false;
@@ -571,10 +586,69 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
 //      Stage 1), into the vertex pools of buffer pass & 1;
 //   2b on stream:   connections + MIS, proxy connection, gate + film, gamma, in pass order.
 // 2a(p+1) overlaps 2b(p); 2a(p+2) waits until 2b(p) has released the buffer.
+void activate_view(pxg_ctx* c, int row0, int rows) {
+  const size_t off = static_cast<size_t>(row0 - c->row0_ctx) * c->width;
+  const int cell_off = (row0 - c->row0_ctx) / 10 * c->grid_w;
+  c->row0 = row0;
+  c->rows = rows;
+  c->n = rows * c->width;
+  c->grid_h = (rows + 9) / 10;
+  c->n_cells = c->grid_w * c->grid_h;
+  const pxg_ctx::FullView& f = c->full;
+  c->d_ctr = f.ctr + off;
+  c->d_bdpt = f.bdpt + 3 * off;
+  c->d_val = f.val + 3 * off;
+  c->d_acc = f.acc + 3 * off;
+  c->d_prox = f.prox + off;
+  c->d_pflags = f.pflags + off;
+  c->d_gbin = f.gbin + off;
+  c->d_gval = f.gval + off;
+  c->d_eye_prims = f.eye_prims + off * (c->max_depth + 1);
+  c->d_light_prims = f.light_prims + off * std::max(c->max_depth - 1, 1);
+  c->d_grid_total = f.grid_total + cell_off;
+  c->d_grid_proxy = f.grid_proxy + cell_off;
+  for (PathCache& pc : c->pcache_buf) pc.n = c->n;
+  c->pcache.n = c->n;
+}
+
+void activate_tile(pxg_ctx* c, int t) {
+  const int r0 = c->row0_ctx + t * c->tile_rows;
+  activate_view(c, r0, std::min(c->tile_rows, c->row0_ctx + c->rows_ctx - r0));
+}
+
+void activate_ctx(pxg_ctx* c) { activate_view(c, c->row0_ctx, c->rows_ctx); }
+
+void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, bool first_tile, bool last_tile);
+
+// Stage 2 of `pass` over the context's row tiles (one tile unless the image is too large for
+// one working set), then the gamma update over the whole context in pixel order.
 void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
+  for (int t = 0; t < c->ntiles; ++t) {
+    activate_tile(c, t);
+    enqueue_stage2_tile(c, pass, sl, record_prims, t == 0, t == c->ntiles - 1);
+  }
+  activate_ctx(c);
+  cudaStream_t st = c->stream;
+  if (c->proxy_on && c->gamma_learning) {
+    // record_contribution in pixel order: a stable sort by bin keeps pixel order per bin
+    CK(cub::DeviceRadixSort::SortPairs(c->d_gsort_tmp, c->gsort_bytes, c->d_gbin, c->d_gbin_sorted, c->d_gval,
+                                       c->d_gval_sorted, c->n, 0, 12, st));
+    k_gamma_update<<<blocks(kT * kS, 128), 128, 0, st>>>(c->n, c->d_gbin_sorted, c->d_gval_sorted, c->d_gamma_accum,
+                                                         c->d_gamma, 1);
+    k_gamma_rows<<<1, 32, 0, st>>>(c->d_gamma_accum, c->d_gamma);
+    c->launches += 3;
+    ++c->gamma_iter;
+    if (c->gamma_iter >= c->P.freeze_iteration) c->gamma_learning = false;
+  }
+  CK(cudaEventRecord(c->gamma_done, st));
+  CK(cudaEventRecord(c->ev[7], st));
+  CK(cudaEventRecord(sl.s2_done, st));
+}
+
+void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, bool first_tile, bool last_tile) {
   cudaStream_t st = c->stream, tt = c->stream_t;
   const int T = 128;
-  const int b = pass & 1;
+  const int b = static_cast<int>(c->tile_step++ & 1);
   c->d_eye = c->eye_buf[b];
   c->d_light = c->light_buf[b];
   c->d_neye = c->neye_buf[b];
@@ -608,9 +682,11 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
   CK(cudaEventRecord(c->ev[0], st));
   if (c->proxy_on) {
     CK(cudaStreamWaitEvent(st, sl.s1_done, 0));
-    k_fold_diag<<<blocks(kBuckets, 128), 128, 0, st>>>(sl.diag, sl.diag_touched, sl.ps, c->d_diag,
-                                                       c->d_diag_touched, c->d_kept_total);
-    ++c->launches;
+    if (first_tile) {  // the pass's Stage-1 diagnostics, once
+      k_fold_diag<<<blocks(kBuckets, 128), 128, 0, st>>>(sl.diag, sl.diag_touched, sl.ps, c->d_diag,
+                                                         c->d_diag_touched, c->d_kept_total);
+      ++c->launches;
+    }
   }
   CK(cudaStreamWaitEvent(st, c->trace_done[b], 0));
   hp.mark("trace");
@@ -665,21 +741,8 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
       c->d_grid_total, c->d_grid_proxy, c->d_gbin, c->d_gval, c->d_pflags, c->d_diag_attempt, c->d_diag_accept,
       c->d_diag_touched);
   ++c->launches;
-  if (c->proxy_on && c->gamma_learning) {
-    // record_contribution in pixel order: a stable sort by bin keeps pixel order per bin
-    CK(cub::DeviceRadixSort::SortPairs(c->d_gsort_tmp, c->gsort_bytes, c->d_gbin, c->d_gbin_sorted, c->d_gval,
-                                       c->d_gval_sorted, c->n, 0, 12, st));
-    k_gamma_update<<<blocks(kT * kS, 128), 128, 0, st>>>(c->n, c->d_gbin_sorted, c->d_gval_sorted, c->d_gamma_accum,
-                                                         c->d_gamma, 1);
-    k_gamma_rows<<<1, 32, 0, st>>>(c->d_gamma_accum, c->d_gamma);
-    c->launches += 3;
-    ++c->gamma_iter;
-    if (c->gamma_iter >= c->P.freeze_iteration) c->gamma_learning = false;
-  }
-  CK(cudaEventRecord(c->gamma_done, st));
-  CK(cudaEventRecord(c->ev[7], st));
-  CK(cudaEventRecord(sl.s2_done, st));
-  hp.mark("gate+gamma");
+  (void)last_tile;
+  hp.mark("gate");
 }
 
 void read_stage2_timing(pxg_ctx* c) {
@@ -813,7 +876,10 @@ void pxg_default_params(pxg_params* p) {
 
 int pxg_abi_version(void) { return PXG_ABI_VERSION; }
 
-int pxg_node_bytes(void) { return PXG_NODEQ ? static_cast<int>(sizeof(BvhNode4Q)) : static_cast<int>(sizeof(BvhNode4)); }
+int pxg_node_bytes(const pxg_ctx* c) {
+  if (!c) return -1;
+  return c->S.nodeq ? static_cast<int>(sizeof(BvhNode4Q)) : static_cast<int>(sizeof(BvhNode4));
+}
 
 int pxg_device_count(void) {
   int n = 0;
@@ -893,6 +959,9 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->row0 = c->shard.row_begin;
     c->rows = c->shard.row_end - c->shard.row_begin;
     c->n = c->rows * c->width;
+    c->row0_ctx = c->row0;
+    c->rows_ctx = c->rows;
+    c->n_ctx = c->n;
     bool any_spec = false;
     std::vector<Material> mats(sd->n_materials);
     for (int m = 0; m < sd->n_materials; ++m) {
@@ -915,6 +984,14 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
     if (reinterpret_cast<uintptr_t>(S.nodes4) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
     S.nodes4q = reinterpret_cast<const BvhNode4Q*>(c->upload(h.nodes4q));
+    // Quantised nodes halve the bytes per visit: a win once the node array outgrows the L1/L2
+    // working set (C4: 43 MB of 128 B nodes, +5.5%); on L2-resident scenes the decode's extra
+    // latency makes the 128 B nodes as fast or faster (C2). PXG_NODEQ=0/1 forces the choice.
+    {
+      const char* e = std::getenv("PXG_NODEQ");
+      const size_t bytes128 = h.nodes4.size() * sizeof(BvhNode4);
+      S.nodeq = PXG_NODEQ && (e ? std::atoi(e) != 0 : bytes128 > (16u << 20));
+    }
     if (reinterpret_cast<uintptr_t>(S.nodes4q) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
     S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
     S.prim_mat = c->upload(h.prim_mat);
@@ -945,8 +1022,38 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     S.max_depth = sd->max_depth;
     c->M.bmin = S.bbox_min;
     c->M.bmax = S.bbox_max;
-    // stage-2 buffers
-    const size_t n = c->n;
+    // stage-2 buffers: full-size per-pixel state, tile-size working set (see pxg_ctx::tile_rows)
+    {
+      int ms = 0;
+      for (int t = 2; t <= c->max_depth + 1; ++t) ms += 1 + std::min(c->max_depth - 1, c->max_depth + 1 - t);
+      c->max_slots = ms;
+      const double D = c->max_depth;
+      // bytes per pixel of the tile-size working set: 2 eye + 2 light vertex pools, proxy
+      // scratch, connection slots + their shadow queue, step caches, queues
+      const double per_px = 128.0 * (2 * (D + 1) + 2 * (D - 1) + kMaxLight) + ms * (40.0 + 80.0) +
+                            2.0 * 4 * kMaxPath * 8 + kMaxLight * 80.0 + 4 * 80.0 + 256.0;
+      const char* tb = std::getenv("PXG_TILE_BUDGET_GB");
+      const double budget = (tb ? std::atof(tb) : 64.0) * 1e9;
+      int tr = c->rows_ctx;
+      if (static_cast<double>(c->n_ctx) * per_px > budget)
+        tr = std::max(10, static_cast<int>(budget / per_px / c->width) / 10 * 10);
+      if (const char* e = std::getenv("PXG_TILE_ROWS")) tr = std::max(10, std::atoi(e) / 10 * 10);
+      c->tile_rows = std::min(tr, c->rows_ctx);
+      c->ntiles = (c->rows_ctx + c->tile_rows - 1) / c->tile_rows;
+      if (c->ntiles > 1 && (c->row0_ctx % 10) != 0) throw InvalidErr{"pxg_create: tiled shard must start on the gate grid"};
+    }
+    const size_t nc = c->n_ctx;
+    const size_t n = static_cast<size_t>(c->tile_rows) * c->width;  // tile-size working set
+    c->full.ctr = c->zeros<unsigned>(nc);
+    c->full.bdpt = c->zeros<double>(3 * nc);
+    c->full.val = c->zeros<double>(3 * nc);
+    c->full.acc = c->zeros<double>(3 * nc);
+    c->full.prox = c->zeros<ProxRec>(nc);
+    c->full.pflags = c->zeros<int>(nc);
+    c->full.gbin = c->zeros<int>(nc);
+    c->full.gval = c->zeros<double>(nc);
+    c->full.eye_prims = c->zeros<int>(nc * (c->max_depth + 1));
+    c->full.light_prims = c->zeros<int>(nc * std::max(c->max_depth - 1, 1));
     for (int k = 0; k < 2; ++k) {
       c->eye_buf[k] = c->alloc<PV>(n * (c->max_depth + 1));
       c->light_buf[k] = c->alloc<PV>(n * std::max(c->max_depth - 1, 1));
@@ -959,11 +1066,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_light = c->light_buf[0];
     c->d_neye = c->neye_buf[0];
     c->d_nlight = c->nlight_buf[0];
-    c->d_ctr = c->zeros<unsigned>(n);
-    c->d_bdpt = c->zeros<double>(3 * n);
-    c->d_val = c->zeros<double>(3 * n);
-    c->d_acc = c->zeros<double>(3 * n);
-    c->d_prox = c->zeros<ProxRec>(n);
     c->d_scratch = c->alloc<PV>(n * kMaxLight);
     c->pw.entry = c->zeros<int>(n);
     c->pw.tp = c->zeros<int>(n);
@@ -976,10 +1078,10 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->pw.occl = c->zeros<int>(n);
     c->pw.lv = c->d_scratch;
     for (int k = 0; k < pxg_ctx::kSnap; ++k) {
-      c->d_snap[k] = c->alloc<double>(3 * n);
+      c->d_snap[k] = c->alloc<double>(3 * nc);
       CK(cudaEventCreateWithFlags(&c->snap_ev[k], cudaEventDisableTiming));
     }
-    c->pinned_bytes = sizeof(double) * 3 * n;
+    c->pinned_bytes = sizeof(double) * 3 * nc;
     c->h_pinned = static_cast<double*>(pinned_acquire(c->pinned_bytes));
     c->h_err = static_cast<int*>(pinned_acquire(pxg_ctx::kSnap * sizeof(int)));
     for (int k = 0; k < pxg_ctx::kSnap; ++k) c->h_err[k] = 0;
@@ -987,11 +1089,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     c->d_epdf = c->zeros<double>(n);
     c->d_lbeta = c->zeros<double>(3 * n);
     c->d_lpdf = c->zeros<double>(n);
-    {
-      int ms = 0;
-      for (int t = 2; t <= c->max_depth + 1; ++t) ms += 1 + std::min(c->max_depth - 1, c->max_depth + 1 - t);
-      c->max_slots = ms;
-    }
     const size_t slots = n * static_cast<size_t>(c->max_slots);
     c->conn.count = c->zeros<int>(n + 1);
     c->conn.offset = c->zeros<int>(n + 1);
@@ -1030,6 +1127,15 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     {
       const char* eb = std::getenv("PXG_BATCH");
       c->batch = std::max(1, std::min(pxg_ctx::kBatchMax, eb ? std::atoi(eb) : pxg_ctx::kBatchDefault));
+      if (!eb && c->proxy_on && c->n_walks > 0) {
+        // a batch holds the vertex pools of all its passes' walks: cap it to a memory budget
+        // (4M walks at depth 16 take 8 GB per pass). Batch composition changes no result.
+        const double per_pass = static_cast<double>(c->n_walks) *
+                                (128.0 * std::max(c->max_depth - 1, 1) + 2 * 80.0 + 48.0 + 12.0 * c->max_depth);
+        const char* wb = std::getenv("PXG_WALK_BUDGET_GB");
+        const double budget = (wb ? std::atof(wb) : 32.0) * 1e9;
+        c->batch = std::max(1, std::min(c->batch, static_cast<int>(budget / per_pass)));
+      }
     }
     if (c->proxy_on && c->n_walks > 0) {
       const size_t w = static_cast<size_t>(c->n_walks) * c->batch;  // the walks of a whole batch
@@ -1042,24 +1148,19 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       c->d_wpdf = c->zeros<double>(w);
     }
     c->grid_w = (c->width + 9) / 10;
-    c->grid_h = (c->rows + 9) / 10;
-    c->n_cells = c->grid_w * c->grid_h;
-    c->d_grid_total = c->zeros<double>(c->n_cells);
-    c->d_grid_proxy = c->zeros<double>(c->n_cells);
-    c->d_gbin = c->zeros<int>(n);
-    c->d_gbin_sorted = c->zeros<int>(n);
-    c->d_gval = c->zeros<double>(n);
-    c->d_gval_sorted = c->zeros<double>(n);
+    c->n_cells_ctx = c->grid_w * ((c->rows_ctx + 9) / 10);
+    c->full.grid_total = c->zeros<double>(c->n_cells_ctx);
+    c->full.grid_proxy = c->zeros<double>(c->n_cells_ctx);
+    c->d_gbin_sorted = c->zeros<int>(nc);
+    c->d_gval_sorted = c->zeros<double>(nc);
     {
       size_t need = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, need, c->d_gbin, c->d_gbin_sorted, c->d_gval, c->d_gval_sorted,
-                                      static_cast<int>(n), 0, 12, c->stream);
+      cub::DeviceRadixSort::SortPairs(nullptr, need, c->full.gbin, c->d_gbin_sorted, c->full.gval, c->d_gval_sorted,
+                                      static_cast<int>(nc), 0, 12, c->stream);
       c->d_gsort_tmp = c->alloc<char>(need);
       c->gsort_bytes = need;
     }
-    c->d_pflags = c->zeros<int>(n);
-    c->d_eye_prims = c->zeros<int>(n * (c->max_depth + 1));
-    c->d_light_prims = c->zeros<int>(n * std::max(c->max_depth - 1, 1));
+    activate_ctx(c);
     // stats
     c->d_max_ratio = c->zeros<double>(kBuckets);
     c->d_sum_est = c->zeros<double>(kBuckets);

@@ -65,6 +65,7 @@ struct SceneView {
   const BvhNode* nodes;
   const BvhNode4* nodes4;
   const BvhNode4Q* nodes4q;
+  int nodeq;  // persistent kernels use nodes4q (1) or nodes4 (0), chosen per scene in pxg_create
   const PrimRec* recs;
   const int* prim_mat;       // [n_prims]
   const int* prim_emitter;   // [n_prims] emitter index or -1
@@ -276,7 +277,7 @@ template <bool kWide = false>
 __device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, const RayF& rf, float tb) {
   // the single-ray path keeps the 128 B nodes: 4 x 16 B loads of the quantised node plus its
   // decode measured 1% slower there (C4, same box)
-  if (kWide && PXG_NODEQ) return node4q_test<true>(S, node, rf, tb);
+  if (kWide && PXG_NODEQ && S.nodeq) return node4q_test<true>(S, node, rf, tb);
   const float4* __restrict__ q = reinterpret_cast<const float4*>(S.nodes4 + node);
   float4 lx, ly, lz, hx, hy, hz;
   if (kWide && PXG_NODE256) {
@@ -361,7 +362,7 @@ __device__ __forceinline__ void node4_prefetch_nearest(const SceneView& S, const
     bc = ok ? h.code[k] : bc;
   }
   if (bc != kNoChild) {
-    if (PXG_NODEQ) asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4q + bc));
+    if (PXG_NODEQ && S.nodeq) asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4q + bc));
     else asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4 + bc));
   }
 #endif

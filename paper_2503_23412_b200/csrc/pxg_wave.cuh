@@ -328,8 +328,8 @@ __global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueu
 }
 
 // Instrumented copies of the traversal kernels for the roofline measurement: the same step
-// functions on the same queue, counting node visits (pxg_node_bytes() each: 64 B quantised
-// 4-wide nodes) and primitive tests (80 B each). Launched after the timed launch; results
+// functions on the same queue, counting node visits (pxg_node_bytes(ctx) each: 64 B quantised
+// or 128 B 4-wide nodes) and primitive tests (80 B each). Launched after the timed launch; results
 // are identical and discarded.
 __global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, unsigned long long* acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;

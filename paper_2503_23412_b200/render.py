@@ -186,6 +186,10 @@ class ProxyRenderer:
         """No look-ahead Stage 1 for passes >= limit (the render's spp)."""
         self._check(self._L.pxg_set_pass_limit(self._ctx, int(limit)))
 
+    def node_bytes(self) -> int:
+        """Bytes per BVH node visit of this context's persistent traversal (pxg_node_bytes)."""
+        return int(self._L.pxg_node_bytes(self._ctx))
+
     def measure_traversal(self, n: int = 1) -> dict:
         """Render n passes with every traversal launch timed by CUDA events and its work
         counted by an instrumented copy on the same rays (roofline numerator)."""

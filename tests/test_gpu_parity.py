@@ -333,3 +333,29 @@ def test_pt_matches_reference_per_pixel(pxg, oracle, name):
     assert bad <= max(1, sc.n_px // 2000)
     chunks = render_pt(sc, spp, 11, chunks=3)  # chunk 0 is the same render, chunks 1-2 independent
     assert np.isfinite(chunks).all() and not np.array_equal(chunks, img)
+
+
+def test_stage2_row_tiles_equal_untiled(pxg, monkeypatch):
+    """Stage 2 in row tiles (the 4K / depth-16 working-set limit, pxg_ctx::tile_rows) renders
+    bitwise the same passes as one tile: per-pixel streams, gate cells and the pixel-order
+    gamma update do not see the tiling."""
+    sc = scenes.caustic_box(40)
+    pd = ProxyParams(pretrace_paths=4000, light_walks=4000)
+    runs = {}
+    for tiles in (None, "10", "30"):
+        if tiles:
+            monkeypatch.setenv("PXG_TILE_ROWS", tiles)
+        else:
+            monkeypatch.delenv("PXG_TILE_ROWS", raising=False)
+        with ProxyRenderer(sc, 4, pd) as r:
+            vals = []
+            for _ in range(4):
+                r.render_passes(1)
+                vals.append(r.dump_pass()[0])
+            runs[tiles] = (np.stack(vals), r.mean(), r.stats())
+    base = runs[None]
+    for tiles in ("10", "30"):
+        assert np.array_equal(runs[tiles][0], base[0])
+        assert np.array_equal(runs[tiles][1], base[1])
+        for a, b in zip(runs[tiles][2], base[2]):
+            assert np.array_equal(a, b)
