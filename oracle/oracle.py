@@ -110,6 +110,25 @@ def lib(variant: str = "philox"):
     return L
 
 
+def film_ref(est: np.ndarray, ref: np.ndarray, pfm_path: str, png_path: str):
+    """The reference's write_pfm / write_png of `est` and compare_images(est, ref)
+    (proj/src/image.cpp, proj/src/metrics.cpp) via oracle/_ref/film_ref; returns
+    (mape, smape, mse, epsilon)."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(REF_DIR, "film_ref")
+    if not os.path.exists(exe):
+        raise OracleUnavailable(f"{exe} missing: run `make -C oracle`")
+    h, w = est.shape[:2]
+    with tempfile.TemporaryDirectory() as d:
+        pe, pr = os.path.join(d, "e.f64"), os.path.join(d, "r.f64")
+        np.ascontiguousarray(est, np.float64).tofile(pe)
+        np.ascontiguousarray(ref, np.float64).tofile(pr)
+        out = subprocess.run([exe, str(w), str(h), pe, pr, pfm_path, png_path], capture_output=True, text=True,
+                             check=True).stdout.split()
+    return tuple(float(x) for x in out)
+
+
 def _check(L, rc):
     if rc != 0:
         raise RuntimeError(L.orc_last_error().decode())

@@ -132,6 +132,32 @@ class Scene:
         return json.dumps(doc, separators=(",", ":"))
 
 
+def save_npz(scene: Scene, path: str) -> None:
+    """Binary scene cache for large scenes: a 1M-triangle scene is
+    ~220 MB of reference JSON (~20 s through a JSON parser); the same arrays load from .npz in
+    well under a second and describe exactly the same Scene."""
+    mats = json.dumps([m.__dict__ for m in scene.materials])
+    cam, st = scene.camera, scene.settings
+    np.savez(path, shape=scene.shape, mat=scene.mat, a=scene.a, b=scene.b, c=scene.c, radius=scene.radius,
+             emitter_prim=scene.emitter_prim, emitter_radiance=scene.emitter_radiance,
+             materials=np.frombuffer(mats.encode(), np.uint8),
+             camera=np.array([*cam.position, *cam.look_at, *cam.up, cam.fov_y, cam.width, cam.height], np.float64),
+             settings=np.array([st.max_depth, st.spp, st.seed], np.int64))
+
+
+def load_npz(path: str) -> Scene:
+    z = np.load(path)
+    mats = [Material(**m) for m in json.loads(bytes(z["materials"]).decode())]
+    for m in mats:
+        m.base_color = tuple(m.base_color)
+    c = z["camera"].tolist()
+    cam = Camera(tuple(c[0:3]), tuple(c[3:6]), tuple(c[6:9]), c[9], int(c[10]), int(c[11]))
+    st = z["settings"].tolist()
+    return Scene(materials=mats, shape=z["shape"], mat=z["mat"], a=z["a"], b=z["b"], c=z["c"], radius=z["radius"],
+                 emitter_prim=z["emitter_prim"], emitter_radiance=z["emitter_radiance"], camera=cam,
+                 settings=Settings(int(st[0]), int(st[1]), int(st[2])))
+
+
 def _cross(u, v):
     return (u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0])
 

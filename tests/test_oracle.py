@@ -4,6 +4,8 @@ The oracle is checked against (1) the Random123 known-answer vectors of Philox4x
 the UNMODIFIED reference renderers compiled from /root/reference (bitwise), and (3) the
 reference's own closed-form fixtures (proj/tests/test_recip.cpp:16-18,74-152).
 """
+import json
+
 import numpy as np
 import pytest
 
@@ -175,3 +177,12 @@ def test_config_generators(oracle):
     full = scenes.procedural_c4(8, 8)
     assert 0.95e6 < full.n_prims < 1.1e6
     assert np.array_equal(full.a, scenes.procedural_c4(8, 8).a)  # seeded, deterministic
+
+
+def test_scene_npz_cache_roundtrip(tmp_path):
+    from paper_2503_23412_b200.scene import load_npz, save_npz
+    for sc in (scenes.sphere_room(8), scenes.lens_room_c3(8, cells=16, rings=4, segs=8)):
+        p = str(tmp_path / "s.npz")
+        save_npz(sc, p)
+        back = load_npz(p)
+        assert json.loads(back.to_json()) == json.loads(sc.to_json())  # 0 == 0.0: same values
