@@ -43,7 +43,36 @@ struct RayQueue {
   double* hit_t;
   int* count;
   int cap;
+  const int* order;  // optional traversal order (rays sorted by origin cell and octant), or null
 };
+
+// Sort key of ray j (PXG_RAY_SORT): direction octant above a 27-bit Morton code of the origin
+// in the scene box, so a warp's lanes fetch rays that start close together and leave in the
+// same octant. Slots past the queue's count sort last.
+__device__ __forceinline__ unsigned spread3(unsigned v) {
+  v &= 0x1ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_ray_keys(RayQueue Q, V3 bmin, V3 inv_ext, int cap, unsigned* keys, int* idx) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cap) return;
+  idx[j] = j;
+  if (j >= *Q.count) {
+    keys[j] = 0xffffffffu;
+    return;
+  }
+  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
+  auto cell = [](double x) { return static_cast<unsigned>(fmin(fmax(x, 0.0), 0.999999) * 512.0); };
+  const unsigned m = spread3(cell((r0.x - bmin.x) * inv_ext.x)) | (spread3(cell((r0.y - bmin.y) * inv_ext.y)) << 1) |
+                     (spread3(cell((r0.z - bmin.z) * inv_ext.z)) << 2);
+  const unsigned oct = (r0.w < 0.0 ? 1u : 0u) | (r1.x < 0.0 ? 2u : 0u) | (r1.y < 0.0 ? 4u : 0u);
+  keys[j] = (oct << 27) | m;
+}
 
 __device__ __forceinline__ Rng path_rng(const PathSet& P, int i) {
   Rng r;
@@ -302,7 +331,7 @@ __global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueu
       if (idle) {
         const int jj = base + __popc(m & ((1u << lane) - 1));
         if (jj < total) {
-          j = jj;
+          j = Q.order ? Q.order[jj] : jj;
           trav_init(ts, Q, j);
         }
       }
