@@ -204,14 +204,6 @@ struct pxg_ctx {
   size_t pinned_bytes = 0;
   int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
-  bool ray_sort = false;      // PXG_RAY_SORT=1: sort closest-hit queues before traversal
-  struct RaySort {
-    unsigned *keys = nullptr, *keys_out = nullptr;
-    int *idx = nullptr, *idx_out = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    V3 inv_ext{};
-  } sort1, sort2;  // stream1 (pool walks) and stream_t (sub-path traces)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
   PV* d_rw_scratch = nullptr; // candidate vertices of k_recip_eval_wave: [wave_blocks][kRW][4]
@@ -333,7 +325,6 @@ RayQueue make_queue(pxg_ctx* c, size_t cap) {
   q.hit_t = c->alloc<double>(cap);
   q.count = c->zeros<int>(1);
   q.cap = static_cast<int>(cap);
-  q.order = nullptr;
   return q;
 }
 
@@ -349,16 +340,6 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
   for (int b = 0; b + 1 < P.max_vertices; ++b) {
     int* fetch = c->d_trav_next + (st == c->stream1 ? 1 : 0);
     CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
-    in.order = nullptr;
-    if (c->ray_sort) {  // PXG_RAY_SORT: traverse the queue in (octant, origin Morton) order
-      pxg_ctx::RaySort& rs = st == c->stream1 ? c->sort1 : c->sort2;
-      const int cap = P.n;
-      k_ray_keys<<<blocks(cap, T), T, 0, st>>>(in, c->S.bbox_min, rs.inv_ext, cap, rs.keys, rs.idx);
-      CK(cub::DeviceRadixSort::SortPairs(rs.tmp, rs.tmp_bytes, rs.keys, rs.keys_out, rs.idx, rs.idx_out, cap, 0, 30,
-                                         st));
-      in.order = rs.idx_out;
-      c->launches += 2;
-    }
     if (c->measure) {
       pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 0};
       CK(cudaEventRecord(t.a, st));
@@ -681,9 +662,9 @@ void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, 
   {
     PathSet E{c->d_eye, c->d_neye, c->d_ctr, c->d_ebeta, c->d_epdf, c->seed,
               static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth + 1, 1};
-    trace_paths(c, E, c->qA, c->qB, tt);
     PathSet L{c->d_light, c->d_nlight, c->d_ctr, c->d_lbeta, c->d_lpdf, c->seed,
               static_cast<uint64_t>(c->row0) * c->width, PXG_KIND_REF, c->n, c->max_depth - 1, 0};
+    trace_paths(c, E, c->qA, c->qB, tt);
     trace_paths(c, L, c->qA, c->qB, tt);
     if (record_prims) {
       k_record_prims<<<blocks(c->n, T), T, 0, tt>>>(c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
@@ -1165,26 +1146,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       c->d_wctr = c->zeros<unsigned>(w);
       c->d_wbeta = c->zeros<double>(3 * w);
       c->d_wpdf = c->zeros<double>(w);
-    }
-    {
-      const char* e = std::getenv("PXG_RAY_SORT");
-      c->ray_sort = e && std::atoi(e) != 0;
-      if (c->ray_sort) {
-        const size_t wcap = (c->proxy_on && c->n_walks > 0) ? static_cast<size_t>(c->n_walks) * c->batch : 1;
-        for (int k = 0; k < 2; ++k) {
-          pxg_ctx::RaySort& rs = k == 0 ? c->sort1 : c->sort2;
-          const size_t cap = k == 0 ? wcap : n;
-          rs.keys = c->alloc<unsigned>(cap);
-          rs.keys_out = c->alloc<unsigned>(cap);
-          rs.idx = c->alloc<int>(cap);
-          rs.idx_out = c->alloc<int>(cap);
-          cub::DeviceRadixSort::SortPairs(nullptr, rs.tmp_bytes, rs.keys, rs.keys_out, rs.idx, rs.idx_out,
-                                          static_cast<int>(cap), 0, 30, c->stream);
-          rs.tmp = c->alloc<char>(rs.tmp_bytes);
-          const V3 ext = c->S.bbox_max - c->S.bbox_min;
-          rs.inv_ext = v3(ext.x > 0 ? 1.0 / ext.x : 0.0, ext.y > 0 ? 1.0 / ext.y : 0.0, ext.z > 0 ? 1.0 / ext.z : 0.0);
-        }
-      }
     }
     c->grid_w = (c->width + 9) / 10;
     c->n_cells_ctx = c->grid_w * ((c->rows_ctx + 9) / 10);

@@ -43,36 +43,7 @@ struct RayQueue {
   double* hit_t;
   int* count;
   int cap;
-  const int* order;  // optional traversal order (rays sorted by origin cell and octant), or null
 };
-
-// Sort key of ray j (PXG_RAY_SORT): direction octant above a 27-bit Morton code of the origin
-// in the scene box, so a warp's lanes fetch rays that start close together and leave in the
-// same octant. Slots past the queue's count sort last.
-__device__ __forceinline__ unsigned spread3(unsigned v) {
-  v &= 0x1ffu;
-  v = (v | (v << 16)) & 0x030000ffu;
-  v = (v | (v << 8)) & 0x0300f00fu;
-  v = (v | (v << 4)) & 0x030c30c3u;
-  v = (v | (v << 2)) & 0x09249249u;
-  return v;
-}
-
-__global__ void k_ray_keys(RayQueue Q, V3 bmin, V3 inv_ext, int cap, unsigned* keys, int* idx) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= cap) return;
-  idx[j] = j;
-  if (j >= *Q.count) {
-    keys[j] = 0xffffffffu;
-    return;
-  }
-  const double4 r0 = Q.ray[2 * j], r1 = Q.ray[2 * j + 1];
-  auto cell = [](double x) { return static_cast<unsigned>(fmin(fmax(x, 0.0), 0.999999) * 512.0); };
-  const unsigned m = spread3(cell((r0.x - bmin.x) * inv_ext.x)) | (spread3(cell((r0.y - bmin.y) * inv_ext.y)) << 1) |
-                     (spread3(cell((r0.z - bmin.z) * inv_ext.z)) << 2);
-  const unsigned oct = (r0.w < 0.0 ? 1u : 0u) | (r1.x < 0.0 ? 2u : 0u) | (r1.y < 0.0 ? 4u : 0u);
-  keys[j] = (oct << 27) | m;
-}
 
 __device__ __forceinline__ Rng path_rng(const PathSet& P, int i) {
   Rng r;
@@ -90,10 +61,9 @@ __device__ __forceinline__ void push_ray(const RayQueue& Q, int path, const V3& 
   Q.path[slot] = path;
 }
 
-// trace_eye_subpath start (transport.cpp:137-152): camera vertex + jittered pixel ray.
-__global__ void k_eye_start(SceneView S, PathSet P, RayQueue Q, int row0) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
+// trace_eye_subpath start (transport.cpp:137-152) of path i: camera vertex + jittered pixel
+// ray. Returns true with the first ray in (o, d) unless the sub-path ends here.
+__device__ __forceinline__ bool eye_start_one(const SceneView& S, const PathSet& P, int i, int row0, V3& o, V3& d) {
   PV z0;
   z0.p = S.cam_pos;
   z0.n = v3(0.0);
@@ -107,7 +77,7 @@ __global__ void k_eye_start(SceneView S, PathSet P, RayQueue Q, int row0) {
   z0.pad = 0.0;
   P.pool[i] = z0;
   P.nv[i] = 1;
-  if (P.max_vertices == 1) return;
+  if (P.max_vertices == 1) return false;
   Rng rng = path_rng(P, i);
   const int idx = row0 * S.width + i;
   const int x = idx % S.width, y = idx / S.width;
@@ -120,16 +90,23 @@ __global__ void k_eye_start(SceneView S, PathSet P, RayQueue Q, int row0) {
   P.beta[3 * i + 1] = 1.0;
   P.beta[3 * i + 2] = 1.0;
   P.pdf_dir[i] = 1.0;
-  push_ray(Q, i, S.cam_pos, dir, 1e30);
+  o = S.cam_pos;
+  d = dir;
+  return true;
 }
 
-// trace_light_subpath start (transport.cpp:111-135): area-sampled emitter point and a
-// cosine direction.
-__global__ void k_light_start(SceneView S, PathSet P, RayQueue Q) {
+__global__ void k_eye_start(SceneView S, PathSet P, RayQueue Q, int row0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n) return;
+  V3 o, d;
+  if (eye_start_one(S, P, i, row0, o, d)) push_ray(Q, i, o, d, 1e30);
+}
+
+// trace_light_subpath start (transport.cpp:111-135) of path i: area-sampled emitter point
+// and a cosine direction. Returns true with the first ray in (o, d).
+__device__ __forceinline__ bool light_start_one(const SceneView& S, const PathSet& P, int i, V3& o, V3& d) {
   P.nv[i] = 0;
-  if (P.max_vertices < 1) return;
+  if (P.max_vertices < 1) return false;
   Rng rng = path_rng(P, i);
   LightPoint lp = sample_light_point(S, rng);
   PV y0;
@@ -147,30 +124,33 @@ __global__ void k_light_start(SceneView S, PathSet P, RayQueue Q) {
   P.nv[i] = 1;
   if (P.max_vertices == 1) {
     P.ctr[i] = rng.r.i;
-    return;
+    return false;
   }
-  V3 d = sample_cosine_hemisphere(lp.n, rng);
+  V3 dir = sample_cosine_hemisphere(lp.n, rng);
   P.ctr[i] = rng.r.i;
-  double pdf_dir = light_direction_pdf(lp.n, d);
-  if (pdf_dir <= 0.0) return;
-  V3 beta = y0.thr * lp.radiance * (dot(d, lp.n) / pdf_dir);
+  double pdf_dir = light_direction_pdf(lp.n, dir);
+  if (pdf_dir <= 0.0) return false;
+  V3 beta = y0.thr * lp.radiance * (dot(dir, lp.n) / pdf_dir);
   P.beta[3 * i] = beta.x;
   P.beta[3 * i + 1] = beta.y;
   P.beta[3 * i + 2] = beta.z;
   P.pdf_dir[i] = pdf_dir;
-  push_ray(Q, i, lp.p, d, 1e30);
+  o = lp.p;
+  d = dir;
+  return true;
 }
 
-// One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
-__global__ void __launch_bounds__(128, 4) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= *in.count) return;
-  const int i = in.path[j];
-  const int prim = in.hit_prim[j];
-  if (prim < 0) return;  // escaped
-  const double4 r0 = in.ray[2 * j], r1 = in.ray[2 * j + 1];
-  const V3 o = v3(r0.x, r0.y, r0.z), d = v3(r0.w, r1.x, r1.y);
-  const double t = in.hit_t[j];
+__global__ void k_light_start(SceneView S, PathSet P, RayQueue Q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  V3 o, d;
+  if (light_start_one(S, P, i, o, d)) push_ray(Q, i, o, d, 1e30);
+}
+
+// One bounce of extend_walk (transport.cpp:37-56) for path i whose ray (o, d) hit `prim` at
+// t (prim >= 0): writes the vertex, samples the BSDF; true with the next ray in (no, nd).
+__device__ __forceinline__ bool shade_one(const SceneView& S, const PathSet& P, int i, const V3& o, const V3& d,
+                                          int prim, double t, V3& no, V3& nd) {
   Hit hit;
   hit.t = t;
   hit.p = o + t * d;
@@ -191,20 +171,35 @@ __global__ void __launch_bounds__(128, 4) k_shade(SceneView S, PathSet P, RayQue
   }
   P.pool[static_cast<size_t>(n) * P.n + i] = v;
   P.nv[i] = n + 1;
-  if (n + 1 >= P.max_vertices) return;
+  if (n + 1 >= P.max_vertices) return false;
   Rng rng = path_rng(P, i);
   BsdfSample bs = sample_bsdf(S.materials[v.mat], v.n, v.wi, rng);
   P.ctr[i] = rng.r.i;
-  if (!bs.valid || bs.pdf <= 0.0) return;
+  if (!bs.valid || bs.pdf <= 0.0) return false;
   beta = beta * bs.value * (fabs(dot(bs.wo, v.n)) / bs.pdf);
   // extend_walk checks the throughput after each of its own samples; the eye walk's first
   // sample (at the primary hit, transport.cpp:160-163) is not checked
-  if (!primary && near_zero(beta)) return;
+  if (!primary && near_zero(beta)) return false;
   P.beta[3 * i] = beta.x;
   P.beta[3 * i + 1] = beta.y;
   P.beta[3 * i + 2] = beta.z;
   P.pdf_dir[i] = bs.pdf;
-  push_ray(out, i, v.p, bs.wo, 1e30);
+  no = v.p;
+  nd = bs.wo;
+  return true;
+}
+
+// One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
+__global__ void __launch_bounds__(128, 4) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *in.count) return;
+  const int i = in.path[j];
+  const int prim = in.hit_prim[j];
+  if (prim < 0) return;  // escaped
+  const double4 r0 = in.ray[2 * j], r1 = in.ray[2 * j + 1];
+  V3 no, nd;
+  if (shade_one(S, P, i, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), prim, in.hit_t[j], no, nd))
+    push_ray(out, i, no, nd, 1e30);
 }
 
 // Closest hit over a queue (Scene::intersect semantics, scene.cpp:127-168).
@@ -331,7 +326,7 @@ __global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueu
       if (idle) {
         const int jj = base + __popc(m & ((1u << lane) - 1));
         if (jj < total) {
-          j = Q.order ? Q.order[jj] : jj;
+          j = jj;
           trav_init(ts, Q, j);
         }
       }
