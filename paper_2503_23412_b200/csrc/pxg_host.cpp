@@ -116,59 +116,107 @@ struct Builder {
   // Binned SAH split of [first, first+count): partitions the range, returns mid and the
   // child boxes. PXG_SAH_BINS overrides the bin count (tuning experiments).
   static constexpr int kMaxBins = 64;
+  // Bins of one range for all three axes at once: one pass over the primitives (chunks of a
+  // large range binned on worker threads and merged), the SAH sweep per axis, then one
+  // partition pass; the child boxes come from the sweep (unions of primitive boxes, exact).
+  struct Bins {
+    Box bb[3][kMaxBins];
+    int cnt[3][kMaxBins] = {};
+  };
+  static void bin_range(const BPrim* p, int count, const D3& clo, const double* scale, int nb, Bins& B) {
+    for (int i = 0; i < count; ++i) {
+      const BPrim& q = p[i];
+      const double c[3] = {q.cen.x, q.cen.y, q.cen.z};
+      const double l[3] = {clo.x, clo.y, clo.z};
+      for (int a = 0; a < 3; ++a) {
+        const int b = std::min(nb - 1, std::max(0, static_cast<int>((c[a] - l[a]) * scale[a])));
+        B.bb[a][b].grow(q.lo, q.hi);
+        ++B.cnt[a][b];
+      }
+    }
+  }
+
   void split(int first, int count, int& mid, Box& lb, Box& rb) {
-    Box cb;
-    for (int i = first; i < first + count; ++i) cb.grow(prims[i].cen, prims[i].cen);
-    mid = -1;
     static const int kBins = std::getenv("PXG_SAH_BINS") ? std::max(2, std::min(kMaxBins, std::atoi(std::getenv("PXG_SAH_BINS")))) : 16;
+    const BPrim* P = prims.data() + first;
+    Box cb;
+    for (int i = 0; i < count; ++i) cb.grow(P[i].cen, P[i].cen);
+    double scale[3];
+    bool ok[3];
+    for (int a = 0; a < 3; ++a) {
+      const double lo = comp(cb.lo, a), hi = comp(cb.hi, a);
+      ok[a] = hi > lo;
+      scale[a] = ok[a] ? kBins / (hi - lo) : 0.0;
+    }
+    Bins B;
+    constexpr int kParBin = 1 << 16;
+    if (count >= kParBin) {
+      const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+      std::vector<Bins> part(T);
+      std::vector<std::thread> th;
+      const int chunk = (count + T - 1) / T;
+      for (int t = 0; t < T; ++t) {
+        const int s0 = t * chunk, s1 = std::min(count, s0 + chunk);
+        if (s0 >= s1) break;
+        th.emplace_back([&, t, s0, s1]() { bin_range(P + s0, s1 - s0, cb.lo, scale, kBins, part[t]); });
+      }
+      for (auto& x : th) x.join();
+      for (const Bins& q : part)
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < kBins; ++b) {
+            if (q.cnt[a][b]) B.bb[a][b].grow(q.bb[a][b].lo, q.bb[a][b].hi);
+            B.cnt[a][b] += q.cnt[a][b];
+          }
+    } else {
+      bin_range(P, count, cb.lo, scale, kBins, B);
+    }
+    mid = -1;
     double best_cost = INFINITY;
     int best_axis = -1, best_bin = -1;
+    Box best_l, best_r;
     for (int axis = 0; axis < 3; ++axis) {
-      const double lo = comp(cb.lo, axis), hi = comp(cb.hi, axis);
-      if (!(hi > lo)) continue;
-      Box bb[kMaxBins];
-      int cnt[kMaxBins] = {0};
-      const double scale = kBins / (hi - lo);
-      for (int i = first; i < first + count; ++i) {
-        int b = std::min(kBins - 1, static_cast<int>((comp(prims[i].cen, axis) - lo) * scale));
-        bb[b].grow(prims[i].lo, prims[i].hi);
-        ++cnt[b];
-      }
+      if (!ok[axis]) continue;
       Box left[kMaxBins];
       int lc[kMaxBins];
       Box acc;
       int ac = 0;
       for (int b = 0; b < kBins; ++b) {
-        if (cnt[b]) acc.grow(bb[b].lo, bb[b].hi);
-        ac += cnt[b];
+        if (B.cnt[axis][b]) acc.grow(B.bb[axis][b].lo, B.bb[axis][b].hi);
+        ac += B.cnt[axis][b];
         left[b] = acc;
         lc[b] = ac;
       }
       Box racc;
       int rc = 0;
       for (int b = kBins - 1; b >= 1; --b) {
-        if (cnt[b]) racc.grow(bb[b].lo, bb[b].hi);
-        rc += cnt[b];
+        if (B.cnt[axis][b]) racc.grow(B.bb[axis][b].lo, B.bb[axis][b].hi);
+        rc += B.cnt[axis][b];
         if (lc[b - 1] == 0 || rc == 0) continue;
         double cost = left[b - 1].area() * lc[b - 1] + racc.area() * rc;
         if (cost < best_cost) {
           best_cost = cost;
           best_axis = axis;
           best_bin = b;
+          best_l = left[b - 1];
+          best_r = racc;
         }
       }
     }
     if (best_axis >= 0) {
-      const double lo = comp(cb.lo, best_axis), hi = comp(cb.hi, best_axis);
-      const double scale = kBins / (hi - lo);
+      const double lo = comp(cb.lo, best_axis), sc = scale[best_axis];
       auto it = std::partition(prims.begin() + first, prims.begin() + first + count, [&](const BPrim& p) {
-        int b = std::min(kBins - 1, static_cast<int>((comp(p.cen, best_axis) - lo) * scale));
+        int b = std::min(kBins - 1, std::max(0, static_cast<int>((comp(p.cen, best_axis) - lo) * sc)));
         return b < best_bin;
       });
       mid = static_cast<int>(it - prims.begin());
       if (mid == first || mid == first + count) mid = -1;
     }
-    if (mid < 0) mid = first + count / 2;  // degenerate centroids: split by position
+    if (mid >= 0) {
+      lb = best_l;
+      rb = best_r;
+      return;
+    }
+    mid = first + count / 2;  // degenerate centroids: split by position
     for (int i = first; i < mid; ++i) lb.grow(prims[i].lo, prims[i].hi);
     for (int i = mid; i < first + count; ++i) rb.grow(prims[i].lo, prims[i].hi);
   }
@@ -352,6 +400,7 @@ HostNode4Q quantize_node(const HostNode4& w) {
     q.origin[a] = ulo[a];
     const double ext = static_cast<double>(uhi[a]) - static_cast<double>(ulo[a]);
     int e = -126;
+    if (ext > 0.0) e = std::max(-126, std::ilogb(ext / 255.0) - 1);  // then at most a few steps up
     while (e < 127 && std::ldexp(255.0, e) < ext) ++e;
     q.exps |= static_cast<unsigned>(e + 127) << (8 * a);
     const double step = std::ldexp(1.0, e);
@@ -480,8 +529,18 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
   h.nodes4.clear();
   h.nodes4.reserve(h.nodes.size() / 2 + 2);
   Collapser{h.nodes, h.nodes4}.build(0);
-  h.nodes4q.resize(h.nodes4.size());
-  for (size_t k = 0; k < h.nodes4.size(); ++k) h.nodes4q[k] = quantize_node(h.nodes4[k]);
+  // Quantised nodes halve the bytes per visit: a win once the node array outgrows the L1/L2
+  // working set (C4: 43 MB of 128 B nodes, +5.5%); on L2-resident scenes the decode's extra
+  // latency makes the 128 B nodes as fast or faster (C2). PXG_NODEQ=0/1 forces the choice.
+  {
+    const char* e = std::getenv("PXG_NODEQ");
+    h.nodeq = e ? std::atoi(e) != 0 : h.nodes4.size() * sizeof(HostNode4) > (16u << 20);
+  }
+  h.nodes4q.clear();
+  if (h.nodeq) {
+    h.nodes4q.resize(h.nodes4.size());
+    for (size_t k = 0; k < h.nodes4.size(); ++k) h.nodes4q[k] = quantize_node(h.nodes4[k]);
+  }
   // leaf-ordered exact records
   h.recs.resize(n);
   for (int k = 0; k < n; ++k) {

@@ -61,7 +61,8 @@ struct SceneHost {
   double tan_half = 0.0, aspect = 1.0;
   std::vector<HostNode> nodes;
   std::vector<HostNode4> nodes4;
-  std::vector<HostNode4Q> nodes4q;
+  std::vector<HostNode4Q> nodes4q;  // only when nodeq
+  bool nodeq = false;               // the persistent traversal uses the quantised nodes
   std::vector<int> order;
   std::vector<HostRec> recs;
   int bvh_depth = 0;

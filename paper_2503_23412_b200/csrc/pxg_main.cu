@@ -983,15 +983,8 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
     S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
     if (reinterpret_cast<uintptr_t>(S.nodes4) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
-    S.nodes4q = reinterpret_cast<const BvhNode4Q*>(c->upload(h.nodes4q));
-    // Quantised nodes halve the bytes per visit: a win once the node array outgrows the L1/L2
-    // working set (C4: 43 MB of 128 B nodes, +5.5%); on L2-resident scenes the decode's extra
-    // latency makes the 128 B nodes as fast or faster (C2). PXG_NODEQ=0/1 forces the choice.
-    {
-      const char* e = std::getenv("PXG_NODEQ");
-      const size_t bytes128 = h.nodes4.size() * sizeof(BvhNode4);
-      S.nodeq = PXG_NODEQ && (e ? std::atoi(e) != 0 : bytes128 > (16u << 20));
-    }
+    S.nodes4q = h.nodeq ? reinterpret_cast<const BvhNode4Q*>(c->upload(h.nodes4q)) : nullptr;
+    S.nodeq = PXG_NODEQ && h.nodeq;  // chosen per scene in finalize_scene (pxg_host.cpp)
     if (reinterpret_cast<uintptr_t>(S.nodes4q) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
     S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
     S.prim_mat = c->upload(h.prim_mat);
