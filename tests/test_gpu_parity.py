@@ -164,6 +164,17 @@ PROXY_SCENES = {
     "c1_budget3000": (lambda: scenes.cornell_c1(30, max_depth=8),
                       {"pretrace_paths": 4000, "light_walks": 6000, "pool_budget": 3000}),
     "c3_small": (lambda: scenes.lens_room_c3(24, max_depth=12), {"pretrace_paths": 4000, "light_walks": 8000}),
+    # recursion cap far below the run lengths: truncated trees with split children left over
+    # (the device DFS skips them; the reference loops over them, each returning 0)
+    "caustic_cap30": (lambda: scenes.caustic_box(20), {"pretrace_paths": 4000, "light_walks": 4000,
+                                                       "recursion_cap": 30}),
+    # gamma frozen after one pass, a gate that never reopens, one reciprocal run per entry
+    "glass_freeze1": (lambda: scenes.glass_slab(20), {"pretrace_paths": 4000, "light_walks": 4000,
+                                                      "freeze_iteration": 1, "gate_low": 0.0,
+                                                      "gate_threshold": 0.5, "recip_repeats": 1}),
+    # the deepest supported paths (C5's depth) and the shallowest
+    "c1_depth16": (lambda: scenes.cornell_c1(20, max_depth=16), {"pretrace_paths": 4000, "light_walks": 8000}),
+    "c1_depth2": (lambda: scenes.cornell_c1(20, max_depth=2), {"pretrace_paths": 4000, "light_walks": 8000}),
     "c4_small": (lambda: scenes.procedural_c4(40, 24, max_depth=12), {"pretrace_paths": 4000, "light_walks": 8000}),
 }
 
@@ -293,6 +304,24 @@ def test_diagnostics_match_oracle(pxg, oracle):
     # recip counters are exact; retrace attempts/accepts follow the gated trajectory
     assert np.array_equal(got[:, 2:], run.diag[:, 2:])
     assert np.abs(got[:, :2] - run.diag[:, :2]).sum() <= 2
+
+
+def test_truncated_recip_diagnostics_match_oracle(pxg, oracle):
+    """recursion_cap 30: run counts, truncations and failed estimates per bucket equal the
+    restated reference loop exactly (the DFS's post-cap shortcut keeps the flag)."""
+    sc = scenes.caustic_box(16)
+    pd = {"pretrace_paths": 3000, "light_walks": 3000, "recursion_cap": 30}
+    o = oracle.OracleScene(sc.to_json())
+    _, run = o.render(3, 4, params=pd, threads=8, trace=True)
+    d = pxg.ProxyDiagnostics()
+    pxg.render_proxy_bdpt(sc, 3, 4, ProxyParams(**pd), diagnostics=d)
+    from paper_2503_23412_b200.render import index_of
+    got = np.zeros((4000, 5), np.int64)
+    for (u, c, s), row in d.rows.items():
+        got[index_of(u, c, s)] = [row.retrace_attempts, row.retrace_accepts, row.recip_runs, row.recip_truncated,
+                                  row.estimates_failed]
+    assert run.diag[:, 3].sum() > 0  # the cap is reached
+    assert np.array_equal(got[:, 2:], run.diag[:, 2:])
 
 
 def test_full_size_c2_pass_is_deterministic_and_finite(pxg):
