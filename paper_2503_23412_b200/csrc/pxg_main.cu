@@ -204,6 +204,7 @@ struct pxg_ctx {
   size_t pinned_bytes = 0;
   int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
+  int gs_blocks = 0;          // grid of the grid-stride slot kernels (SMs x 256 blocks of 128; 16 / 64 measured slower)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
   PV* d_rw_scratch = nullptr; // candidate vertices of k_recip_eval_wave: [wave_blocks][kRW][4]
@@ -368,7 +369,8 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
   CK(cudaMemsetAsync(C.n_live, 0, sizeof(int), st));
   const long long slots = static_cast<long long>(n) * c->max_slots;
-  k_conn_eval<<<blocks(slots, T), T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
+  const int gs = static_cast<int>(std::min<long long>(c->gs_blocks, blocks(slots, T)));
+  k_conn_eval<<<gs, T, 0, st>>>(c->S, c->d_eye, c->d_light, n, C, c->qS);
   int* fetch = c->d_trav_next + 2;
   CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
   if (c->measure) {
@@ -381,8 +383,8 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   } else {
     k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
   }
-  k_conn_visibility<<<blocks(slots, T), T, 0, st>>>(c->qS, C);
-  k_conn_mis<<<blocks(slots, T), T, 0, st>>>(c->S, c->M,
+  k_conn_visibility<<<gs, T, 0, st>>>(c->qS, C);
+  k_conn_mis<<<gs, T, 0, st>>>(c->S, c->M,
                                              StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
                                              use_stats ? 1 : 0, c->d_eye, c->d_light, n, C, c->pcache);
   k_conn_sum<<<blocks(n, T), T, 0, st>>>(n, C, c->d_bdpt);
@@ -1239,6 +1241,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
+      c->gs_blocks = sms * (std::getenv("PXG_GS_PER_SM") ? std::atoi(std::getenv("PXG_GS_PER_SM")) : 256);
       int pe = 0, pd = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe, k_recip_eval, 64, 0));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, k_recip_dfs_warp<128>, 128, 0));

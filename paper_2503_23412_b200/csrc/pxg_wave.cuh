@@ -190,7 +190,10 @@ __device__ __forceinline__ bool shade_one(const SceneView& S, const PathSet& P, 
 }
 
 // One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
-__global__ void __launch_bounds__(128, 4) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
+#ifndef PXG_SHADE_MINB
+#define PXG_SHADE_MINB 4
+#endif
+__global__ void __launch_bounds__(128, PXG_SHADE_MINB) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *in.count) return;
   const int i = in.path[j];
@@ -422,9 +425,8 @@ __global__ void k_conn_enum(const int* n_eye, const int* n_light, int n, int max
 }
 
 // Unoccluded value of every slot; connections that need a shadow ray are queued.
-__global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, ConnBuf C, RayQueue shadow) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= *C.total) return;
+__device__ __forceinline__ void conn_eval_one(const SceneView& S, const PV* eye, const PV* light, int n,
+                                              const ConnBuf& C, const RayQueue& shadow, int g) {
   const int2 dsc = C.desc[g];
   const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
   const size_t st = static_cast<size_t>(n);
@@ -493,13 +495,22 @@ __global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, 
   if (state == 1) C.live[atomicAdd(C.n_live, 1)] = g;
 }
 
+// Grid-stride over the enumerated slots (a fixed grid instead of one thread per possible slot:
+// most of the n x max_slots threads would only read the count and exit).
+__global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, ConnBuf C, RayQueue shadow) {
+  const int total = *C.total;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x)
+    conn_eval_one(S, eye, light, n, C, shadow, g);
+}
+
 __global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= *shadow.count) return;
-  const int g = shadow.path[q];
-  const int vis = shadow.hit_prim[q] ? 0 : 1;  // occluded -> no contribution
-  C.state[g] = vis;
-  if (vis) C.live[atomicAdd(C.n_live, 1)] = g;
+  const int count = *shadow.count;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) {
+    const int g = shadow.path[q];
+    const int vis = shadow.hit_prim[q] ? 0 : 1;  // occluded -> no contribution
+    C.state[g] = vis;
+    if (vis) C.live[atomicAdd(C.n_live, 1)] = g;
+  }
 }
 
 // Per-pixel sub-path step densities (PathCache), evaluated once per pixel and pass.
@@ -652,8 +663,8 @@ __global__ void __launch_bounds__(32 * kConnWarps) k_conn_pixel(SceneView S, Map
 // reciprocal_mis_weight of every live slot; value <- value * w.
 __global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
                            int n, ConnBuf C, PathCache PC) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= *C.n_live) return;
+  const int n_live = *C.n_live;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_live; q += gridDim.x * blockDim.x) {
   const int g = C.live[q];
   const int2 dsc = C.desc[g];
   const int i = dsc.x, t = dsc.y >> 8, s = dsc.y & 255;
@@ -666,6 +677,7 @@ __global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, c
   C.value[3 * g] = C.value[3 * g] * w;
   C.value[3 * g + 1] = C.value[3 * g + 1] * w;
   C.value[3 * g + 2] = C.value[3 * g + 2] * w;
+  }
 }
 
 // weighted_bdpt_value's accumulation (proxy.cpp:627-641) in slot order.
