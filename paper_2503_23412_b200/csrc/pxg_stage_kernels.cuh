@@ -112,17 +112,32 @@ __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L,
   vals += static_cast<size_t>(b) * cap;
   count += b;
   const int n = wnv[i];
-  int flag[kMaxLight], emitter[kMaxLight];
-  double pdf[kMaxLight];
+  // dropout_eligible of every prefix end in one forward pass, in registers: the trailing
+  // specular run length u, the running pdf product (the same left-to-right product the
+  // reference forms for each end) and sliding windows of the last prefix products and
+  // emitter ids, enough for u <= 4 (proxy.cpp:59-94).
+  double P = 1.0, Pw[5] = {1.0, 1.0, 1.0, 1.0, 1.0};  // Pw[m] = product of pdf[0 .. k-m-1]
+  int Ew[6] = {-1, -1, -1, -1, -1, -1};                 // Ew[m] = emitter[k-m]
+  int flag0 = -1, run = 0;
   for (int k = 0; k < n; ++k) {
     const PV& v = wpool[static_cast<size_t>(k) * total + i];
-    flag[k] = v.flag;
-    emitter[k] = v.emitter;
-    pdf[k] = v.pdf_fwd;
-  }
-  for (int end = 2; end <= n; ++end) {
-    if (flag[end - 1] != kSpecular) continue;
-    if (!dropout_eligible(flag, emitter, pdf, end)) continue;
+    const int fk = v.flag;
+#pragma unroll
+    for (int m = 4; m > 0; --m) Pw[m] = Pw[m - 1];
+    Pw[0] = P;
+#pragma unroll
+    for (int m = 5; m > 0; --m) Ew[m] = Ew[m - 1];
+    Ew[0] = v.emitter;
+    if (k == 0) flag0 = fk;
+    run = fk == kSpecular ? run + 1 : 0;
+    P *= v.pdf_fwd;
+    const int end = k + 1;
+    if (end < 2 || fk != kSpecular || run > 4 || run >= end) continue;
+    const int u = run, terminal = k - u;
+    const int em = u == 1 ? Ew[2] : u == 2 ? Ew[3] : u == 3 ? Ew[4] : Ew[5];  // emitter[terminal - 1]
+    const double pp = u == 1 ? Pw[1] : u == 2 ? Pw[2] : u == 3 ? Pw[3] : Pw[4];  // product of pdf[0 .. terminal-1]
+    if (terminal > 0 ? em < 0 : flag0 != kLight) continue;
+    if (!(pp > 0.0)) continue;
     Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
     unsigned long long hi = pxg_next_u32(&kr.r);
     unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
