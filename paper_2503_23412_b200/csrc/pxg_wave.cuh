@@ -309,7 +309,10 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* 
 constexpr int kRefill = 4;  // refill a warp's idle lanes once at least this many are idle
 
 template <bool kAny>
-__global__ void __launch_bounds__(128, 7) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
+#ifndef PXG_TRAV_MINB
+#define PXG_TRAV_MINB 7
+#endif
+__global__ void __launch_bounds__(128, PXG_TRAV_MINB) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int total = *Q.count;
