@@ -204,6 +204,7 @@ struct pxg_ctx {
   size_t pinned_bytes = 0;
   int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
+  int trav_minb = 6;          // resident blocks per SM of the traversal variant (6 or 8)
   int gs_blocks = 0;          // grid of the grid-stride slot kernels (SMs x 256 blocks of 128; 16 / 64 measured slower)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
@@ -318,6 +319,15 @@ struct HostProbe {
   }
 };
 
+// Persistent traversal of queue q (closest hit or any hit) with the context's occupancy variant.
+template <bool kAny>
+void launch_trav(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
+  if (c->trav_minb == 8)
+    k_trav_persistent<kAny, 8><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+  else
+    k_trav_persistent<kAny, 6><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+}
+
 RayQueue make_queue(pxg_ctx* c, size_t cap) {
   RayQueue q;
   q.ray = c->alloc<double4>(2 * cap);
@@ -344,12 +354,12 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
     if (c->measure) {
       pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 0};
       CK(cudaEventRecord(t.a, st));
-      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
+      launch_trav<false>(c, in, fetch, st);
       CK(cudaEventRecord(t.b, st));
       k_closest_count<<<blocks(P.n, T), T, 0, st>>>(c->S, in, c->d_tcnt);
       c->tl.push_back(t);
     } else {
-      k_trav_persistent<false><<<c->trav_blocks, 128, 0, st>>>(c->S, in, fetch);
+      launch_trav<false>(c, in, fetch, st);
     }
     CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
     k_shade<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, out);
@@ -376,12 +386,12 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   if (c->measure) {
     pxg_ctx::TimedLaunch t{c->take_event(), c->take_event(), 1};
     CK(cudaEventRecord(t.a, st));
-    k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
+    launch_trav<true>(c, c->qS, fetch, st);
     CK(cudaEventRecord(t.b, st));
     k_anyhit_count<<<blocks(slots, T), T, 0, st>>>(c->S, c->qS, c->d_tcnt + 3);
     c->tl.push_back(t);
   } else {
-    k_trav_persistent<true><<<c->trav_blocks, 128, 0, st>>>(c->S, c->qS, fetch);
+    launch_trav<true>(c, c->qS, fetch, st);
   }
   k_conn_visibility<<<gs, T, 0, st>>>(c->qS, C);
   k_conn_mis<<<gs, T, 0, st>>>(c->S, c->M,
@@ -715,7 +725,7 @@ void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, 
     for (int step = 0; step < 4; ++step) {
       int* fetch = c->d_trav_next + 3;
       CK(cudaMemsetAsync(fetch, 0, sizeof(int), sp));
-      k_trav_persistent<false><<<c->trav_blocks, 128, 0, sp>>>(c->S, in, fetch);
+      launch_trav<false>(c, in, fetch, sp);
       CK(cudaMemsetAsync(out.count, 0, sizeof(int), sp));
       k_pxw_retrace<<<blocks(c->n, T), T, 0, sp>>>(C, W, pass, c->n_px_total, in, out);
       std::swap(in, out);
@@ -725,7 +735,7 @@ void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, 
     {
       int* fetch = c->d_trav_next + 4;
       CK(cudaMemsetAsync(fetch, 0, sizeof(int), sp));
-      k_trav_persistent<true><<<c->trav_blocks, 128, 0, sp>>>(c->S, c->qPS, fetch);
+      launch_trav<true>(c, c->qPS, fetch, sp);
     }
     k_pxw_occlusion<<<blocks(static_cast<long long>(c->n) * kMaxLight, T), T, 0, sp>>>(W, c->qPS);
     k_pxw_mis<<<blocks(c->n, T), T, 0, sp>>>(C, W, c->d_prox);
@@ -1239,7 +1249,12 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     {
       int sms = 0, per_sm = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false>, 128, 0));
+      c->trav_minb = c->S.nodeq ? 8 : 6;
+      if (const char* e = std::getenv("PXG_TRAV_MINB")) c->trav_minb = std::atoi(e) == 8 ? 8 : 6;
+      if (c->trav_minb == 8)
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 8>, 128, 0));
+      else
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
       c->gs_blocks = sms * (std::getenv("PXG_GS_PER_SM") ? std::atoi(std::getenv("PXG_GS_PER_SM")) : 256);
       int pe = 0, pd = 0;
