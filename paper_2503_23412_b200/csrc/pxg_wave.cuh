@@ -517,18 +517,33 @@ __global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
 }
 
 // Per-pixel sub-path step densities (PathCache), evaluated once per pixel and pass.
+// One thread per (pixel, family): 4 n threads (LF, LR, EF, ER) so the fp64 step loops of a
+// pixel run side by side; the LF thread also writes the light-direction density.
 __global__ void k_path_factors(SceneView S, const PV* eye, const int* n_eye, const PV* light, const int* n_light,
                                int n, PathCache C) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= 4ll * n) return;
+  const int i = static_cast<int>(tid % n), fam = static_cast<int>(tid / n);
   const size_t st = static_cast<size_t>(n);
-  const int nl = n_light[i], ne = n_eye[i];
   const PV* y = light + i;
   const PV* e = eye + i;
+  if (fam == 1) {
+    const int nl = n_light[i];
+    for (int j = 0; j <= nl - 3; ++j) C.LR[j * st + i] = bsdf_step_v(S, y[(j + 1) * st], y[(j + 2) * st], y[j * st]);
+    return;
+  }
+  if (fam == 2) {
+    const int ne = n_eye[i];
+    for (int m = 0; m <= ne - 3; ++m) C.EF[m * st + i] = bsdf_step_v(S, e[(m + 1) * st], e[(m + 2) * st], e[m * st]);
+    return;
+  }
+  if (fam == 3) {
+    const int ne = n_eye[i];
+    for (int m = 2; m <= ne - 1; ++m) C.ER[m * st + i] = bsdf_step_v(S, e[(m - 1) * st], e[(m - 2) * st], e[m * st]);
+    return;
+  }
+  const int nl = n_light[i];
   for (int k = 2; k <= nl - 1; ++k) C.LF[k * st + i] = bsdf_step_v(S, y[(k - 1) * st], y[(k - 2) * st], y[k * st]);
-  for (int j = 0; j <= nl - 3; ++j) C.LR[j * st + i] = bsdf_step_v(S, y[(j + 1) * st], y[(j + 2) * st], y[j * st]);
-  for (int m = 0; m <= ne - 3; ++m) C.EF[m * st + i] = bsdf_step_v(S, e[(m + 1) * st], e[(m + 2) * st], e[m * st]);
-  for (int m = 2; m <= ne - 1; ++m) C.ER[m * st + i] = bsdf_step_v(S, e[(m - 1) * st], e[(m - 2) * st], e[m * st]);
   int ok = 0;
   double area = 0.0;
   if (nl >= 2) {
