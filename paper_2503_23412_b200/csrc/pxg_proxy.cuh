@@ -106,24 +106,6 @@ __device__ __forceinline__ bool dropout(const Mapper& M, const PV* v, int n, Inc
   return true;
 }
 
-// Light-walk eligibility only (no labels): used by the pool-walk kernel to count and key
-// candidates without materialising them.
-__device__ __forceinline__ bool dropout_eligible(const int* flag, const int* emitter, const double* pdf, int n) {
-  if (n < 2 || flag[n - 1] != kSpecular) return false;
-  int u = 0;
-  while (u < n && flag[n - 1 - u] == kSpecular) ++u;
-  if (u < 1 || u > 4) return false;
-  const int terminal = n - 1 - u;
-  if (terminal > 0) {
-    if (emitter[terminal - 1] < 0) return false;
-  } else if (flag[terminal] != kLight) {
-    return false;
-  }
-  double pp = 1.0;
-  for (int i = 0; i < terminal; ++i) pp *= pdf[i];
-  return pp > 0.0;
-}
-
 __device__ __forceinline__ PV vertex_from_hit(const SceneView& S, const Hit& hit, const V3& wi) {
   return surface_vertex(S, hit, wi);
 }

@@ -344,30 +344,6 @@ __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* s
   return c[0];
 }
 
-#ifndef PXG_PREFETCH
-#define PXG_PREFETCH 0  // measured: -1% on C2 and C4
-#endif
-
-// The nearest hit inner child of h (kNoChild if none), before the leaf tests of the step
-// tighten t_best: its node is prefetched into L1 so the fetch latency overlaps the fp64
-// primitive tests (the visit order itself is decided after them, as before).
-__device__ __forceinline__ void node4_prefetch_nearest(const SceneView& S, const Node4Hits& h) {
-#if PXG_PREFETCH
-  float bt = __int_as_float(0x7f800000);
-  int bc = kNoChild;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const bool ok = (h.hit >> k & 1u) && h.code[k] >= 0 && h.tn[k] < bt;
-    bt = ok ? h.tn[k] : bt;
-    bc = ok ? h.code[k] : bc;
-  }
-  if (bc != kNoChild) {
-    if (PXG_NODEQ && S.nodeq) asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4q + bc));
-    else asm volatile("prefetch.global.L1 [%0];" ::"l"(S.nodes4 + bc));
-  }
-#endif
-}
-
 // Hit leaf children of a visited node (bit k of the result: child k is a hit leaf).
 __device__ __forceinline__ unsigned node4_leaves(const Node4Hits& h) {
   unsigned leaves = 0u;

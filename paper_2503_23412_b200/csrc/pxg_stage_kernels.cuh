@@ -112,7 +112,7 @@ __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L,
   vals += static_cast<size_t>(b) * cap;
   count += b;
   const int n = wnv[i];
-  // dropout_eligible of every prefix end in one forward pass, in registers: the trailing
+  // dropout eligibility (proxy.cpp:59-94) of every prefix end in one forward pass, in registers: the trailing
   // specular run length u, the running pdf product (the same left-to-right product the
   // reference forms for each end) and sliding windows of the last prefix products and
   // emitter ids, enough for u <= 4 (proxy.cpp:59-94).

@@ -256,9 +256,7 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
   // inner children are ordered nearest-first (the next node, then the stack)
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tbound_f(ts.t_best));
   if (kCount) cnt->nodes += 1;
-  const unsigned leaves0 = node4_leaves(h);
-  if (leaves0) node4_prefetch_nearest(S, h);
-  for (unsigned leaves = leaves0; leaves; leaves &= leaves - 1) {
+  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     if (kCount) cnt->prims += count;
@@ -286,9 +284,7 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* 
   const float tb = tbound_f(ts.t_best);
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
   if (kCount) cnt->nodes += 1;
-  const unsigned leaves0 = node4_leaves(h);
-  if (leaves0) node4_prefetch_nearest(S, h);
-  for (unsigned leaves = leaves0; leaves; leaves &= leaves - 1) {
+  for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
     const int first = code >> 4, count = code & 15;
     for (int i = 0; i < count; ++i) {
