@@ -129,10 +129,11 @@ struct VisDirect {
   __device__ __forceinline__ bool operator()(int, const V3& a, const V3& b) const { return visible(*S, a, b); }
 };
 
-// support_pdf (proxy.cpp:153-209)
+// The two terms of support_pdf (proxy.cpp:153-209): q_fs (the from-specular strand) and
+// q_other (light-area or from-control strand; only for u == 1).
 template <class Vis>
-__device__ __forceinline__ double support_pdf_v(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g,
-                                                const Vis& vis) {
+__device__ __forceinline__ void support_terms_v(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g,
+                                                const Vis& vis, double& q_fs_out, double& q_other_out) {
   const int u = h.u;
   const PV* hc = inc_control(h, prefix);
   const PV& y = h.spec_end;
@@ -160,7 +161,9 @@ __device__ __forceinline__ double support_pdf_v(const SceneView& S, const IncHdr
       prev = &nxt;
     }
   }
-  if (u > 1) return q_fs;
+  q_fs_out = q_fs;
+  q_other_out = 0.0;
+  if (u > 1) return;
   double q_other = 0.0;
   if (hc == nullptr) {
     if (g[0].emitter >= 0) q_other = 1.0 / S.total_emitter_area;
@@ -174,7 +177,20 @@ __device__ __forceinline__ double support_pdf_v(const SceneView& S, const IncHdr
       if (pdf_w > 0.0 && vis(4, hc->p, g[0].p)) q_other = to_area_density(pdf_w, hc->p, g[0].p, g[0].n);
     }
   }
-  return 0.5 * (q_other + q_fs);
+  q_other_out = q_other;
+}
+
+// support_pdf from its terms, in the reference's operation order.
+__device__ __forceinline__ double support_combine(int u, double q_fs, double q_other) {
+  return u > 1 ? q_fs : 0.5 * (q_other + q_fs);
+}
+
+template <class Vis>
+__device__ __forceinline__ double support_pdf_v(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g,
+                                                const Vis& vis) {
+  double q_fs, q_other;
+  support_terms_v(S, h, prefix, g, vis, q_fs, q_other);
+  return support_combine(h.u, q_fs, q_other);
 }
 
 __device__ __forceinline__ double support_pdf(const SceneView& S, const IncHdr& h, const PV* prefix, const PV* g) {

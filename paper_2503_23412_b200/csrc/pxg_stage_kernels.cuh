@@ -475,8 +475,9 @@ __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride
 // every node's glue code runs on its own thread, but each ray phase traces only the rays that
 // exist, compacted onto the first threads of the block: (1) sampling chain, <= 4 rounds of
 // compacted closest-hit rays; (2) the visibility segments of every node (the density code run
-// with a functor that records them and their endpoints, VisDirect's segment ids) as one
-// compacted any-hit list; (3) the density code run again with the traced results. Candidate
+// with a functor that records them and their endpoints, VisDirect's segment ids, and answers
+// "visible") as one compacted any-hit list; (3) the recorded density terms, each zeroed when
+// one of its segments is hidden (exactly what the reference's early exits produce). Candidate
 // vertices and segment endpoints live in a global scratch slot per (block, node).
 // Scene::intersect / visible through the persistent kernels' step functions (quantised
 // nodes, 32-byte loads), inlined: same hits as intersect() / visible() (closest hit with the
@@ -534,10 +535,6 @@ struct VisRecord {  // phase 2a: record every segment the density code asks for,
     e[0] = a.x, e[1] = a.y, e[2] = a.z, e[3] = b.x, e[4] = b.y, e[5] = b.z;
     return true;
   }
-};
-struct VisReplay {  // phase 2c: answer from the traced results
-  unsigned vis;
-  __device__ __forceinline__ bool operator()(int seg, const V3&, const V3&) const { return (vis >> seg) & 1u; }
 };
 __global__ void __launch_bounds__(kRW) k_recip_eval_wave(SceneView S, uint64_t seed, int repeats, int stride,
                                                           long long cap, const __grid_constant__ BatchSet bs,
@@ -677,14 +674,24 @@ __global__ void __launch_bounds__(kRW) k_recip_eval_wave(SceneView S, uint64_t s
     if (t == 0) s_nseg = 0;
     __syncthreads();
     unsigned need = 0;
+    // the densities assuming every segment visible; a hidden segment only zeroes its term
+    // (support q_fs: segments 0-3, q_other: 4, target: 5-9), which (2c) applies without
+    // evaluating the fp64 densities again
+    double qfs_all = 0.0, qoth_all = 0.0, f_all = 0.0;
+    int u_node = 0;
     if (k >= 0 && state == kRWSampled) {
       const BatchPass& P = bs.p[j / stride];
       const int e = (j % stride) / repeats;
       const IncHdr& h = P.inc[e];
       const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
       const VisRecord rec{&need, ends_block + t * 60};
-      const double q = support_pdf_v(S, h, pre, gv, rec);
-      if (q > 0.0) target_density_v(S, h, pre, gv, rec);
+      support_terms_v(S, h, pre, gv, rec, qfs_all, qoth_all);
+      u_node = h.u;
+      if (support_combine(u_node, qfs_all, qoth_all) > 0.0) {
+        unsigned tneed = 0;
+        f_all = target_density_v(S, h, pre, gv, VisRecord{&tneed, ends_block + t * 60});
+        need |= tneed;
+      }
       for (unsigned m = need; m; m &= m - 1)
         s_seg[atomicAdd(&s_nseg, 1)] = static_cast<unsigned short>(t * 16 + (__ffs(m) - 1));
     }
@@ -709,10 +716,12 @@ __global__ void __launch_bounds__(kRW) k_recip_eval_wave(SceneView S, uint64_t s
       const double B = P.bound[e];
       double qx = 1.0, fx = 0.0;
       if (state == kRWSampled) {
-        const VisReplay vr{s_vis[t]};
-        qx = support_pdf_v(S, h, pre, gv, vr);
+        const unsigned hidden = need & ~s_vis[t];
+        const double q_fs = (hidden & 0xfu) ? 0.0 : qfs_all;
+        const double q_other = (hidden & 0x10u) ? 0.0 : qoth_all;
+        qx = support_combine(u_node, q_fs, q_other);
         if (!(qx > 0.0)) qx = 1.0;  // escaped (support_sample's q <= 0 branch)
-        else fx = target_density_v(S, h, pre, gv, vr);
+        else fx = (hidden & 0x3e0u) ? 0.0 : f_all;
       }
       int err = 0;
       if (!isfinite(fx) || fx < 0.0) err = kErrIntegrand;
