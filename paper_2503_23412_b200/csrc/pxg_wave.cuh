@@ -675,7 +675,15 @@ __global__ void __launch_bounds__(32 * kConnWarps) k_conn_pixel(SceneView S, Map
 }
 
 // reciprocal_mis_weight of every live slot; value <- value * w.
-__global__ void k_conn_mis(SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
+#ifndef PXG_MIS_MINB
+#define PXG_MIS_MINB 0
+#endif
+#if PXG_MIS_MINB
+__global__ void __launch_bounds__(128, PXG_MIS_MINB) k_conn_mis(
+#else
+__global__ void k_conn_mis(
+#endif
+  SceneView S, Mapper M, StatsView st, int use_stats, const PV* eye, const PV* light,
                            int n, ConnBuf C, PathCache PC) {
   const int n_live = *C.n_live;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_live; q += gridDim.x * blockDim.x) {
