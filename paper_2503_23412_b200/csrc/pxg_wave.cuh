@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(32 * kConnWarps) k_conn_pixel(SceneView S, Map
 
 // reciprocal_mis_weight of every live slot; value <- value * w.
 #ifndef PXG_MIS_MINB
-#define PXG_MIS_MINB 0
+#define PXG_MIS_MINB 8
 #endif
 #if PXG_MIS_MINB
 __global__ void __launch_bounds__(128, PXG_MIS_MINB) k_conn_mis(

@@ -1,7 +1,7 @@
 # Round evidence (run under gpurun, one GPU): tests, smoke, bench lines for every config, launch
 # lists and ncu --set full captures exported to CSV. Each ncu run only after the same command
 # exited 0 without ncu.
-O=gpurun_out/final3; mkdir -p $O
+O=gpurun_out/final4; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -1 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?"; tail -1 $O/smoke.log
 timeout 900 python bench.py > $O/bench_C2.log 2>&1; echo "bench C2 exit $?"; tail -1 $O/bench_C2.log > $O/bench_C2.json
