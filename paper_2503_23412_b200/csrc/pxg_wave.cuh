@@ -191,7 +191,7 @@ __device__ __forceinline__ bool shade_one(const SceneView& S, const PathSet& P, 
 
 // One bounce of extend_walk (transport.cpp:37-56) for the rays of queue `in`.
 #ifndef PXG_SHADE_MINB
-#define PXG_SHADE_MINB 4
+#define PXG_SHADE_MINB 5
 #endif
 __global__ void __launch_bounds__(128, PXG_SHADE_MINB) k_shade(SceneView S, PathSet P, RayQueue in, RayQueue out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -496,7 +496,10 @@ __device__ __forceinline__ void conn_eval_one(const SceneView& S, const PV* eye,
 
 // Grid-stride over the enumerated slots (a fixed grid instead of one thread per possible slot:
 // most of the n x max_slots threads would only read the count and exit).
-__global__ void k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, ConnBuf C, RayQueue shadow) {
+#ifndef PXG_EVAL_MINB
+#define PXG_EVAL_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PXG_EVAL_MINB) k_conn_eval(SceneView S, const PV* eye, const PV* light, int n, ConnBuf C, RayQueue shadow) {
   const int total = *C.total;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x)
     conn_eval_one(S, eye, light, n, C, shadow, g);
@@ -515,7 +518,10 @@ __global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
 // Per-pixel sub-path step densities (PathCache), evaluated once per pixel and pass.
 // One thread per (pixel, family): 4 n threads (LF, LR, EF, ER) so the fp64 step loops of a
 // pixel run side by side; the LF thread also writes the light-direction density.
-__global__ void k_path_factors(SceneView S, const PV* eye, const int* n_eye, const PV* light, const int* n_light,
+#ifndef PXG_PF_MINB
+#define PXG_PF_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PXG_PF_MINB) k_path_factors(SceneView S, const PV* eye, const int* n_eye, const PV* light, const int* n_light,
                                int n, PathCache C) {
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= 4ll * n) return;
