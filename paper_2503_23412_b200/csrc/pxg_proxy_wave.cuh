@@ -75,7 +75,17 @@ __device__ __forceinline__ Rng prox_rng(const ProxCtx& C, const ProxWave& W, int
 }
 
 // Selection (proxy.cpp:747-798) and the first retrace sample (proxy.cpp:280-288).
-__global__ void k_pxw_select(ProxCtx C, ProxWave W, int pass, int n_px_total, ProxRec* out, RayQueue Q) {
+// resident 128-thread blocks per SM of the proxy-wavefront kernels (0: no launch bounds)
+#ifndef PXG_PXW_MINB
+#define PXG_PXW_MINB 0
+#endif
+#if PXG_PXW_MINB
+#define PXW_BOUNDS __launch_bounds__(128, PXG_PXW_MINB)
+#else
+#define PXW_BOUNDS
+#endif
+
+__global__ void PXW_BOUNDS k_pxw_select(ProxCtx C, ProxWave W, int pass, int n_px_total, ProxRec* out, RayQueue Q) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C.n) return;
   ProxRec o;
@@ -167,7 +177,7 @@ __global__ void k_pxw_select(ProxCtx C, ProxWave W, int pass, int n_px_total, Pr
 }
 
 // One retrace step (proxy.cpp:285-306) for every ray of the queue.
-__global__ void k_pxw_retrace(ProxCtx C, ProxWave W, int pass, int n_px_total, RayQueue in, RayQueue out) {
+__global__ void PXW_BOUNDS k_pxw_retrace(ProxCtx C, ProxWave W, int pass, int n_px_total, RayQueue in, RayQueue out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *in.count) return;
   const int i = in.path[j];
@@ -232,7 +242,7 @@ __global__ void k_pxw_retrace(ProxCtx C, ProxWave W, int pass, int n_px_total, R
 }
 
 // Repair, value without visibility, and one shadow ray per segment (proxy.cpp:562-592).
-__global__ void k_pxw_value(ProxCtx C, ProxWave W, RayQueue shadow) {
+__global__ void PXW_BOUNDS k_pxw_value(ProxCtx C, ProxWave W, RayQueue shadow) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C.n) return;
   W.occl[i] = 0;
@@ -308,7 +318,7 @@ __global__ void k_pxw_occlusion(ProxWave W, RayQueue shadow) {
 }
 
 // reciprocal_mis_weight of the proxy strategy and the final contribution (proxy.cpp:594-602).
-__global__ void k_pxw_mis(ProxCtx C, ProxWave W, ProxRec* out) {
+__global__ void PXW_BOUNDS k_pxw_mis(ProxCtx C, ProxWave W, ProxRec* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C.n) return;
   if (W.state[i] != kPxShadow || W.occl[i]) return;
