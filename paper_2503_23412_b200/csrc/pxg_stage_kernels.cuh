@@ -536,7 +536,15 @@ struct VisRecord {  // phase 2a: record every segment the density code asks for,
     return true;
   }
 };
-__global__ void __launch_bounds__(kRW) k_recip_eval_wave(SceneView S, uint64_t seed, int repeats, int stride,
+#ifndef PXG_RW_MINB
+#define PXG_RW_MINB 0  // resident blocks per SM (A/B; 0: none); the grid follows the occupancy query
+#endif
+#if PXG_RW_MINB
+__global__ void __launch_bounds__(kRW, PXG_RW_MINB) k_recip_eval_wave(
+#else
+__global__ void __launch_bounds__(kRW) k_recip_eval_wave(
+#endif
+SceneView S, uint64_t seed, int repeats, int stride,
                                                           long long cap, const __grid_constant__ BatchSet bs,
                                                           const int* active, const int* n_active, int chunk,
                                                           const RunState* st, double* g, long long* nsplit,
