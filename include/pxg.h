@@ -167,6 +167,18 @@ int pxg_dump_pool(pxg_ctx* ctx, int cap, int* n, long long* raw, int* walk, int*
 int pxg_intersect(pxg_ctx* ctx, int n, const double* rays, const double* tmax, int* prim, double* t);
 int pxg_occluded(pxg_ctx* ctx, int n, const double* segs, int* occ);
 
+/* Parity of the traversal kernels that ship: the same rays as pxg_intersect (any_hit = 0:
+ * rays[n*6] origin + unit direction, tmax may be NULL) or pxg_occluded (any_hit = 1:
+ * segments[n*6] from + to, prim[i] = 1 when occluded, t unused) through
+ *   kernel 0: the single-ray paths (trace_closest_t / trace_any_t, 128 B nodes),
+ *   kernel 1: the production persistent queue kernels k_trav_persistent<0/1> (lane refill,
+ *             256-bit loads, the context's node layout: pxg_node_bytes),
+ *   kernel 2: the reciprocal node wavefront's inlined step loops (wave_intersect /
+ *             wave_visible).
+ * Reference: Scene::intersect / Scene::occluded (proj/src/scene.cpp:127-177). */
+int pxg_trace_rays(pxg_ctx* ctx, int kernel, int any_hit, int n, const double* rays, const double* tmax, int* prim,
+                   double* t);
+
 /* proxima::render_pt (proj/include/proxima/transport.hpp:88, proj/src/transport.cpp:272-381)
  * on the device for this context's pixels: the unidirectional path tracer with NEE, the
  * converged reference of the relMSE checks. rgb[n*3] = mean over `chunks` independent
@@ -181,6 +193,11 @@ int pxg_recip_twopoint(int n, double bound, long long cap, uint64_t seed, double
 
 /* Philox stream check: first n draws of stream (seed, kind, sub, stream) computed on the device. */
 int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, int n, unsigned* out);
+
+/* sin(phi), cos(phi) of phi = 2*pi*(k[i] * 2^-32) on `device` with the samplers' device
+ * code (include/pxg_sincos.h): bitwise the host glibc's std::sin / std::cos that the
+ * reference calls at proj/src/bsdf.cpp:63-65, 226-227 and proj/src/scene.cpp:199-201. */
+int pxg_sincos_2pi(int device, int n, const uint32_t* k, double* s, double* c);
 
 /* Device timeline of the last pxg_render_passes call (ms, CUDA events on the context's
  * stream): t[0] stage 1 (pool walks, selection, probes, reciprocal runs, incl. the host

@@ -20,12 +20,15 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["pxg_main.cu"]
 CPP_SOURCES = ["pxg_host.cpp"]
+SINCOS_TABLE = os.path.join(HERE, "pxg_sincos_glibc.bin")
+SINCOS_GEN = os.path.join(HERE, "_build", "pxg_sincos_gen")
 HEADERS = ["pxg_pt.cuh", "pxg_stage_kernels.cuh", "pxg_proxy_wave.cuh", "pxg_wave.cuh", "pxg_math.cuh", "pxg_bsdf.cuh", "pxg_scene.cuh", "pxg_path.cuh", "pxg_proxy.cuh", "pxg_host.h"]
 
 
 def _inputs():
     files = [os.path.join(CSRC, f) for f in CU_SOURCES + CPP_SOURCES + HEADERS]
-    files += [os.path.join(REPO, "include", "pxg.h"), os.path.join(REPO, "include", "pxg_philox.h")]
+    files += [os.path.join(REPO, "include", "pxg.h"), os.path.join(REPO, "include", "pxg_philox.h"),
+              os.path.join(REPO, "include", "pxg_sincos.h")]
     return files
 
 
@@ -36,9 +39,26 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
+def build_sincos_table(force: bool = False, verbose: bool = False) -> str:
+    """The glibc agreement table of the device sin / cos (include/pxg_sincos.h): every one of
+    the 2^32 sampler angles evaluated with this host's libm (~2 min on 8 cores), written next
+    to libpxg.so. Rebuilt only when the generator or the header changes."""
+    gen_src = os.path.join(CSRC, "pxg_sincos_gen.cpp")
+    hdr = os.path.join(REPO, "include", "pxg_sincos.h")
+    os.makedirs(os.path.dirname(SINCOS_GEN), exist_ok=True)
+    if force or not os.path.exists(SINCOS_GEN) or any(os.path.getmtime(f) > os.path.getmtime(SINCOS_GEN)
+                                                       for f in (gen_src, hdr)):
+        _run(["g++", "-std=c++20", "-O2", "-pthread", "-ffp-contract=off", "-I", os.path.join(REPO, "include"),
+              gen_src, "-o", SINCOS_GEN], verbose)
+    if force or not os.path.exists(SINCOS_TABLE) or os.path.getmtime(SINCOS_GEN) > os.path.getmtime(SINCOS_TABLE):
+        _run([SINCOS_GEN, SINCOS_TABLE], verbose)
+    return SINCOS_TABLE
+
+
 def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
     """`out` / `defines` (-DNAME=V for the device code): A/B variants of the same sources for
     tuning runs (loaded through PXG_LIBRARY); the shipped library is the default build."""
+    build_sincos_table(force=False, verbose=verbose)
     if out == OUT and not defines and not force and up_to_date():
         return OUT
     bdir = os.path.join(HERE, "_build" if out == OUT else "_build_" + os.path.basename(out).replace(".so", ""))

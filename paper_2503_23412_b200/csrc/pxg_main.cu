@@ -6,6 +6,9 @@
 // -> gamma) on `stream`. Stage 1 of pass p+1 reads and writes only the subspace statistics
 // and its own pool slot, never the film, the grid shares or gamma, so overlapping it with
 // Stage 2 of pass p leaves every result identical to the sequential order.
+#include <dlfcn.h>
+
+#include <fstream>
 #include <mutex>
 #include <utility>
 
@@ -68,6 +71,104 @@ void pinned_release(void* p, size_t bytes) {
   }
   g_pinned_free.emplace_back(bytes, p);
 }
+}  // namespace
+
+// ---- parity entry point of the production traversal kernels (pxg_trace_rays)
+// Queue fill with the production conventions: closest-hit rays as given (tmax or 1e30);
+// any-hit segments a -> b as conn_eval_one / occluded() build them (unit direction sd/dist,
+// tmax = dist * (1 - 1e-6)); a segment shorter than kRayEps is never occluded (tmax 0).
+__global__ void k_fill_trace_queue(int n, const double* rays, const double* tmax, int any, RayQueue Q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* r = rays + 6 * static_cast<size_t>(i);
+  V3 o = v3(r[0], r[1], r[2]), d;
+  double tm;
+  if (any) {
+    const V3 sd = v3(r[3], r[4], r[5]) - o;
+    const double dist = length(sd);
+    if (dist < kRayEps) {
+      d = v3(1.0, 0.0, 0.0);
+      tm = 0.0;
+    } else {
+      d = sd / dist;
+      tm = dist * (1.0 - 1e-6);
+    }
+  } else {
+    d = v3(r[3], r[4], r[5]);
+    tm = tmax ? tmax[i] : 1e30;
+  }
+  Q.ray[2 * i] = make_double4(o.x, o.y, o.z, d.x);
+  Q.ray[2 * i + 1] = make_double4(d.y, d.z, tm, 0.0);
+  Q.path[i] = i;
+  if (i == 0) *Q.count = n;
+}
+
+// The reciprocal node wavefront's inlined traversal (k_recip_eval_wave: wave_intersect /
+// wave_visible) on the queue's rays, one thread per ray; rays with a finite tmax run the same
+// step loop with that bound.
+template <bool kAny>
+__global__ void k_wave_trace(SceneView S, RayQueue Q, const double* rays, int any_segments) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *Q.count) return;
+  if (kAny) {
+    const double* r = rays + 6 * static_cast<size_t>(j);
+    Q.hit_prim[j] = wave_visible(S, v3(r[0], r[1], r[2]), v3(r[3], r[4], r[5])) ? 0 : 1;
+    return;
+  }
+  const double4 r1 = Q.ray[2 * j + 1];
+  if (r1.z >= 1e30) {
+    const double4 r0 = Q.ray[2 * j];
+    Hit h;
+    if (wave_intersect(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), h)) {
+      Q.hit_prim[j] = h.prim;
+      Q.hit_t[j] = h.t;
+    } else {
+      Q.hit_prim[j] = -1;
+      Q.hit_t[j] = 1e30;
+    }
+    return;
+  }
+  TravState ts;
+  int stack[kStack];
+  trav_init(ts, Q, j);
+  while (!closest_step(S, ts, stack)) {
+  }
+  Q.hit_prim[j] = ts.best;
+  Q.hit_t[j] = ts.t_best;
+}
+
+// sin / cos of the draws k (u = k * 2^-32, phi = 2*pi*u) with the device code path of the
+// samplers (pxg_sincos_2pi parity entry point).
+__global__ void k_sincos_2pi(int n, const uint32_t* k, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s, c;
+  sincos_2pi(static_cast<double>(k[i]) * 0x1p-32, s, c);
+  out[2 * i] = s;
+  out[2 * i + 1] = c;
+}
+
+// glibc agreement table of the device sin / cos (include/pxg_sincos.h), built next to
+// libpxg.so by the build (csrc/pxg_sincos_gen.cpp, from the host's libm). Loaded once per
+// process and uploaded once per device; a missing table is an error, never a silent switch
+// to CUDA's sin / cos.
+namespace {
+std::mutex g_sc_mu;
+std::vector<char> g_sc_file;
+bool g_sc_device[64] = {};
+
+std::string sincos_table_path() {
+  if (const char* e = std::getenv("PXG_SINCOS_TABLE")) return e;
+  Dl_info info{};
+  if (dladdr(reinterpret_cast<void*>(&pxg_abi_version), &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const size_t slash = so.rfind('/');
+    return (slash == std::string::npos ? std::string(".") : so.substr(0, slash)) + "/pxg_sincos_glibc.bin";
+  }
+  return "pxg_sincos_glibc.bin";
+}
+
+void ensure_sincos_table(int device);
 }  // namespace
 
 struct pxg_ctx {
@@ -868,6 +969,35 @@ int guarded(pxg_ctx* c, F&& f) {
   }
 }
 
+void ensure_sincos_table(int device) {
+  std::lock_guard<std::mutex> lk(g_sc_mu);
+  if (device < 0 || device >= 64) throw InvalidErr{"pxg: device index out of range"};
+  if (g_sc_device[device]) return;
+  if (g_sc_file.empty()) {
+    const std::string path = sincos_table_path();
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw InvalidErr{"pxg: sin/cos table " + path + " missing (run the build: python -m paper_2503_23412_b200.build)"};
+    std::vector<char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    uint32_t hdr[2] = {0, 0};
+    if (buf.size() >= sizeof(hdr)) std::memcpy(hdr, buf.data(), sizeof(hdr));
+    const size_t want = sizeof(hdr) + sizeof(double) * 2 * PXG_SC_RANGES + sizeof(uint32_t) * (PXG_SC_BUCKETS + 1) +
+                        sizeof(uint16_t) * static_cast<size_t>(hdr[1]);
+    if (hdr[0] != PXG_SC_MAGIC || buf.size() != want) throw InvalidErr{"pxg: sin/cos table " + path + " is corrupt"};
+    g_sc_file.swap(buf);
+  }
+  const char* p = g_sc_file.data() + 2 * sizeof(uint32_t);
+  const size_t bytes = g_sc_file.size() - 2 * sizeof(uint32_t);
+  char* d = nullptr;
+  CK(cudaMalloc(&d, bytes));  // process lifetime, shared by every context on the device
+  CK(cudaMemcpy(d, p, bytes, cudaMemcpyHostToDevice));
+  pxg_sincos_table t;
+  t.thr = reinterpret_cast<const double*>(d);
+  t.offset = reinterpret_cast<const uint32_t*>(d + sizeof(double) * 2 * PXG_SC_RANGES);
+  t.entry = reinterpret_cast<const uint16_t*>(d + sizeof(double) * 2 * PXG_SC_RANGES + sizeof(uint32_t) * (PXG_SC_BUCKETS + 1));
+  CK(cudaMemcpyToSymbol(pxg::g_sincos, &t, sizeof(t)));
+  g_sc_device[device] = true;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI
@@ -930,6 +1060,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     if (params) c->P = *params; else pxg_default_params(&c->P);
     c->seed = seed;
     CK(cudaSetDevice(device));
+    ensure_sincos_table(device);
     {
       cudaMemPool_t pool;
       CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1556,6 +1687,55 @@ int pxg_intersect(pxg_ctx* c, int n, const double* rays, const double* tmax, int
   });
 }
 
+int pxg_trace_rays(pxg_ctx* c, int kernel, int any_hit, int n, const double* rays, const double* tmax, int* prim,
+                   double* t) {
+  return guarded(c, [&]() {
+    if (n <= 0) return;
+    if (!rays || !prim || (!any_hit && !t)) throw InvalidErr{"pxg_trace_rays: null argument"};
+    if (kernel < 0 || kernel > 2) throw InvalidErr{"pxg_trace_rays: kernel must be 0, 1 or 2"};
+    if (kernel == 0) {  // the single-ray paths (Scene::intersect / Scene::occluded)
+      const int rc = any_hit ? pxg_occluded(c, n, rays, prim) : pxg_intersect(c, n, rays, tmax, prim, t);
+      if (rc == PXG_E_INVALID) throw InvalidErr{c->err};
+      if (rc != PXG_OK) throw CudaErr{c->err};
+      return;
+    }
+    cudaStream_t st = c->stream;
+    double* dr = dupload(rays, static_cast<size_t>(n) * 6);
+    double* dt = (!any_hit && tmax) ? dupload(tmax, n) : nullptr;
+    RayQueue q;
+    q.ray = dalloc<double4>(2 * static_cast<size_t>(n));
+    q.path = dalloc<int>(n);
+    q.hit_prim = dalloc<int>(n);
+    q.hit_t = dalloc<double>(n);
+    q.count = dalloc<int>(1);
+    q.cap = n;
+    int* fetch = dalloc<int>(1);
+    CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+    k_fill_trace_queue<<<blocks(n, 128), 128, 0, st>>>(n, dr, dt, any_hit, q);
+    if (kernel == 1) {  // the production persistent kernels, the context's node layout
+      if (any_hit)
+        launch_trav<true>(c, q, fetch, st);
+      else
+        launch_trav<false>(c, q, fetch, st);
+    } else if (any_hit) {
+      k_wave_trace<true><<<blocks(n, 128), 128, 0, st>>>(c->S, q, dr, 1);
+    } else {
+      k_wave_trace<false><<<blocks(n, 128), 128, 0, st>>>(c->S, q, dr, 0);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(prim, q.hit_prim, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    if (!any_hit) CK(cudaMemcpyAsync(t, q.hit_t, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (void* p : {static_cast<void*>(dr), static_cast<void*>(dt), static_cast<void*>(q.ray),
+                    static_cast<void*>(q.path), static_cast<void*>(q.hit_prim), static_cast<void*>(q.hit_t),
+                    static_cast<void*>(q.count), static_cast<void*>(fetch)})
+      if (p) cudaFree(p);
+    if (!any_hit)
+      for (int i = 0; i < n; ++i)
+        if (prim[i] < 0) t[i] = 0.0;  // pxg_intersect's convention for a miss
+  });
+}
+
 int pxg_render_pt(pxg_ctx* c, int spp, uint64_t seed, int chunks, double* rgb) {
   return guarded(c, [&]() {
     if (!rgb) throw InvalidErr{"pxg_render_pt: null output"};
@@ -1653,6 +1833,27 @@ int pxg_rng_draws(uint64_t seed, unsigned kind, unsigned sub, uint64_t stream, i
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, d, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
     cudaFree(d);
+  });
+}
+
+int pxg_sincos_2pi(int device, int n, const uint32_t* k, double* s, double* c) {
+  return guarded(nullptr, [&]() {
+    if (n <= 0) return;
+    if (!k || !s || !c) throw InvalidErr{"pxg_sincos_2pi: null argument"};
+    CK(cudaSetDevice(device));
+    ensure_sincos_table(device);
+    uint32_t* dk = dupload(k, static_cast<size_t>(n));
+    double* ds = dalloc<double>(2 * static_cast<size_t>(n));
+    k_sincos_2pi<<<blocks(n, 256), 256>>>(n, dk, ds);
+    CK(cudaGetLastError());
+    std::vector<double> h(2 * static_cast<size_t>(n));
+    CK(cudaMemcpy(h.data(), ds, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+      s[i] = h[2 * static_cast<size_t>(i)];
+      c[i] = h[2 * static_cast<size_t>(i) + 1];
+    }
+    cudaFree(dk);
+    cudaFree(ds);
   });
 }
 

@@ -507,8 +507,9 @@ __device__ __forceinline__ LightPoint sample_light_point(const SceneView& S, Rng
   if (shape == kSphere) {
     double z = 1.0 - 2.0 * rng.next_double();
     double r = sqrt(dmax(0.0, 1.0 - z * z));
-    double phi = 2.0 * kPi * rng.next_double();
-    V3 n = v3(r * cos(phi), r * sin(phi), z);
+    double sp, cp;
+    sincos_2pi(rng.next_double(), sp, cp);  // phi = 2*pi*u
+    V3 n = v3(r * cp, r * sp, z);
     const double* c = S.prim_center + 4 * prim;
     lp.p = v3(c[0], c[1], c[2]) + c[3] * n;
     lp.n = n;

@@ -300,6 +300,19 @@ class ProxyRenderer:
         self._check(self._L.pxg_occluded(self._ctx, segs.shape[0], _dp(segs), _ip(occ)))
         return occ.astype(bool)
 
+    def trace_rays(self, kernel: int, rays: np.ndarray, tmax=None, any_hit: bool = False):
+        """The same rays through a chosen traversal kernel (include/pxg.h pxg_trace_rays):
+        0 single-ray paths, 1 the production persistent kernels, 2 the reciprocal
+        wavefront's inlined step loops. Returns (prim, t) or the occlusion booleans."""
+        rays = np.ascontiguousarray(rays, np.float64)
+        n = rays.shape[0]
+        prim = np.zeros(n, np.int32)
+        t = np.zeros(n)
+        tm = None if (tmax is None or any_hit) else np.ascontiguousarray(np.broadcast_to(tmax, (n,)), np.float64)
+        self._check(self._L.pxg_trace_rays(self._ctx, kernel, int(any_hit), n, _dp(rays),
+                                           _dp(tm) if tm is not None else None, _ip(prim), _dp(t)))
+        return prim.astype(bool) if any_hit else (prim, t)
+
 
 SNAPSHOT_SLOTS = 4   # PXG_SNAPSHOT_SLOTS (include/pxg.h)
 PIPELINE_AHEAD = 3   # passes in flight in the pipelined pass_done loop (< SNAPSHOT_SLOTS)
@@ -374,3 +387,14 @@ def rng_draws(seed: int, kind: int, sub: int, stream: int, n: int) -> np.ndarray
     out = np.zeros(n, np.uint32)
     _lib.check(L.pxg_rng_draws(seed, kind, sub, stream, n, out.ctypes.data_as(C.POINTER(C.c_uint))))
     return out
+
+
+def sincos_2pi(k: np.ndarray, device: int = 0):
+    """sin / cos of phi = 2*pi*(k * 2^-32) on the device, with the samplers' code path
+    (bitwise the host glibc's, include/pxg_sincos.h)."""
+    L = _lib.lib()
+    k = np.ascontiguousarray(k, dtype=np.uint32)
+    s = np.zeros(k.size)
+    c = np.zeros(k.size)
+    _lib.check(L.pxg_sincos_2pi(device, k.size, k.ctypes.data_as(C.POINTER(C.c_uint)), _dp(s), _dp(c)))
+    return s, c

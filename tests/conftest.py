@@ -33,3 +33,24 @@ def pxg():
     if L.pxg_device_count() <= 0:
         pytest.fail("no CUDA device visible to libpxg")
     return p
+
+
+_PARITY = {}
+
+
+@pytest.fixture(scope="session")
+def parity_report():
+    """Collects the observed parity numbers (mismatch counts, max relative errors) of the GPU
+    parity tests and writes them as JSON at the end of the session: $PXG_PARITY_REPORT, or
+    gpurun_out/parity_report.json (copied under profiles/ as round evidence)."""
+    import json
+
+    def add(section, record):
+        _PARITY.setdefault(section, []).append(record)
+
+    yield add
+    if _PARITY:
+        path = os.environ.get("PXG_PARITY_REPORT") or os.path.join(REPO, "gpurun_out", "parity_report.json")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        with open(path, "w") as f:
+            json.dump(_PARITY, f, indent=1)

@@ -73,39 +73,61 @@ TRAVERSAL_SCENES = {
 }
 
 
+def _segments(o, sc, n, rng):
+    """Shadow segments between surface points (hit points of camera rays and of secondary
+    rays), the connection / visibility queries of the path."""
+    sec = _secondary_rays(o, _camera_rays(sc, n, rng), rng)
+    a = sec[:, :3]
+    b = a[rng.permutation(a.shape[0])]
+    return np.concatenate([a, b], axis=1)
+
+
+KERNELS = {0: "single-ray trace_closest_t/trace_any_t", 1: "production k_trav_persistent<0/1>",
+           2: "reciprocal wavefront wave_intersect/wave_visible"}
+
+
 @pytest.mark.parametrize("name", list(TRAVERSAL_SCENES))
-def test_traversal_prim_ids_bit_exact(pxg, oracle, name):
+def test_traversal_prim_ids_bit_exact(pxg, oracle, name, monkeypatch, parity_report):
+    """Scene::intersect / Scene::occluded (proj/src/scene.cpp:127-177, pinned by the
+    reference's own proj/tests/test_scene.cpp:111-148) against every traversal kernel that
+    ships, with both node layouts: 1.6 M closest-hit rays (camera rays and rays leaving
+    surface points with no origin offset, as extend_walk shoots them), 0.8 M of them again
+    with a finite tmax, and 0.4 M shadow segments. Prim ids and fp64 t bitwise equal, 0
+    mismatches allowed."""
     sc = TRAVERSAL_SCENES[name]()
     o = oracle_scene(oracle, "geom_" + name, sc)
     rng = np.random.default_rng(1)
-    prim_rays = _camera_rays(sc, 200000, rng)
+    prim_rays = _camera_rays(sc, 800000, rng)
     sec = _secondary_rays(o, prim_rays, rng)
     rays = np.concatenate([prim_rays, sec])
-    with ProxyRenderer(sc, 0, ProxyParams(enabled=False)) as r:
-        gp, gt = r.intersect(rays)
-        tm = rng.uniform(0.05, 2.0, size=sec.shape[0])
-        gp2, _ = r.intersect(sec, tm)
-    op, ot = o.intersect(rays)
-    op2, _ = o.intersect(sec, tm)
-    mism = np.count_nonzero(gp != op)
-    print(f"{name}: {rays.shape[0]} rays, {mism} prim-id mismatches; tmax rays {np.count_nonzero(gp2 != op2)}")
-    assert mism == 0
-    assert np.count_nonzero(gp2 != op2) == 0
-    same = gp == op
-    assert np.array_equal(gt[same], ot[same])  # identical fp64 t
-
-
-def test_occlusion_matches(pxg, oracle):
-    sc = scenes.cornell_c2(32)
-    o = oracle.OracleScene(sc.to_json())
-    rng = np.random.default_rng(2)
-    sec = _secondary_rays(o, _camera_rays(sc, 50000, rng), rng)
-    a = sec[:, :3]
-    b = a[rng.permutation(a.shape[0])]
-    segs = np.concatenate([a, b], axis=1)
-    with ProxyRenderer(sc, 0, ProxyParams(enabled=False)) as r:
-        g = r.occluded(segs)
-    assert np.array_equal(g, o.occluded(segs))
+    tm = rng.uniform(0.05, 2.0, size=sec.shape[0])
+    segs = _segments(o, sc, 400000, rng)
+    op, ot = o.intersect(rays, threads=16)
+    op2, ot2 = o.intersect(sec, tm, threads=16)
+    oocc = o.occluded(segs, threads=16)
+    for nodeq in (0, 1):
+        monkeypatch.setenv("PXG_NODEQ", str(nodeq))
+        with ProxyRenderer(sc, 0, ProxyParams(enabled=False)) as r:
+            layout = f"{r.node_bytes()} B nodes"
+            for kernel in (0, 1, 2):
+                gp, gt = r.trace_rays(kernel, rays)
+                gp2, gt2 = r.trace_rays(kernel, sec, tm)
+                gocc = r.trace_rays(kernel, segs, any_hit=True)
+                m1 = int(np.count_nonzero(gp != op))
+                m2 = int(np.count_nonzero(gp2 != op2))
+                m3 = int(np.count_nonzero(gocc != oocc))
+                same = (gp == op) & (op >= 0)
+                tbits = int(np.count_nonzero(gt[same].view(np.uint64) != ot[same].view(np.uint64)))
+                same2 = (gp2 == op2) & (op2 >= 0)
+                tbits += int(np.count_nonzero(gt2[same2].view(np.uint64) != ot2[same2].view(np.uint64)))
+                rec = {"scene": name, "layout": layout, "kernel": KERNELS[kernel], "rays": int(rays.shape[0]),
+                       "tmax_rays": int(sec.shape[0]), "segments": int(segs.shape[0]),
+                       "prim_mismatch": m1, "tmax_prim_mismatch": m2, "occlusion_mismatch": m3,
+                       "t_bit_mismatch": tbits, "hits": int(np.count_nonzero(op >= 0)),
+                       "occluded": int(np.count_nonzero(oocc))}
+                parity_report("traversal", rec)
+                print(rec)
+                assert m1 == 0 and m2 == 0 and m3 == 0 and tbits == 0, rec
 
 
 BDPT_SCENES = {
@@ -120,7 +142,7 @@ BDPT_SCENES = {
 
 
 @pytest.mark.parametrize("name", list(BDPT_SCENES))
-def test_bdpt_matches_reference_per_pixel(pxg, oracle, name):
+def test_bdpt_matches_reference_per_pixel(pxg, oracle, name, parity_report):
     """Proxy off: every pixel-sample equals the UNMODIFIED reference render_bdpt (same
     pixel streams) within 1e-4 relative; primitive-id trajectories are identical."""
     sc = BDPT_SCENES[name]()
@@ -141,14 +163,19 @@ def test_bdpt_matches_reference_per_pixel(pxg, oracle, name):
     n_px = sc.n_px
     eye_ok = np.all(eye == run.eye_prims, axis=1)
     light_ok = np.all(light == run.light_prims[:, :light.shape[1]], axis=1)
-    print(f"{name}: eye trajectories equal {eye_ok.mean():.6f}, light {light_ok.mean():.6f}")
-    assert eye_ok.mean() >= 0.999 and light_ok.mean() >= 0.999
+    rec = {"scene": name, "pixels": n_px, "passes": spp, "eye_trajectories_differ": int(np.count_nonzero(~eye_ok)),
+           "light_trajectories_differ": int(np.count_nonzero(~light_ok)), "pixels_over_tol": [], "max_rel_err": []}
     for p in range(spp):
         e = rel_err(vals[p], run.pass_val[p])
-        both = eye_ok & light_ok if p == spp - 1 else np.ones(n_px, bool)
-        bad = np.count_nonzero((e > REL_TOL).any(axis=1) & both)
-        print(f"  pass {p}: max rel err {e.max():.3e}, pixels over tol {bad}")
-        assert bad <= max(1, n_px // 2000)
+        rec["pixels_over_tol"].append(int(np.count_nonzero((e > REL_TOL).any(axis=1))))
+        rec["max_rel_err"].append(float(e.max()))
+    rec["image_max_rel_err_vs_unmodified_render_bdpt"] = float(rel_err(img, ref).max())
+    parity_report("bdpt_per_pixel", rec)
+    print(rec)
+    assert eye_ok.all() and light_ok.all()
+    assert sum(rec["pixels_over_tol"]) == 0
+    # observed: every pixel-sample bitwise equal (round 2 report); the north-star bar is 1e-4
+    assert max(rec["max_rel_err"]) == 0.0
     assert np.allclose(img, ref, rtol=1e-6, atol=1e-12)
 
 
@@ -179,48 +206,87 @@ PROXY_SCENES = {
 }
 
 
-@pytest.mark.parametrize("name", list(PROXY_SCENES))
-def test_proxy_render_matches_oracle(pxg, oracle, name):
-    """Proxy on: pool selection, reciprocal estimates, per-pixel proxy connections and the
-    gated per-pass values equal the restated reference loop."""
-    make, pd = PROXY_SCENES[name]
-    sc = make()
-    o = oracle_scene(oracle, name, sc)
-    spp = 3
-    img_o, run = o.render(spp, 9, params=pd, threads=8, trace=True, pool_cap=max(400, pd.get("pool_budget", 400)))
-    params = ProxyParams(**pd)
-    with ProxyRenderer(sc, 9, params) as r:
+def compare_proxy_render(o, sc, pd, spp, seed, name, parity_report, threads=16, section="proxy_per_pass"):
+    """GPU passes vs the restated reference loop on identical Philox streams, with no failure
+    budget: pool (raw, kept, walk, end, bucket) exact, bounds B within 1e-12, inverse_p and
+    every pixel-sample within 1e-4 relative (north star), gate / proxy flags exact, subspace
+    counts exact. The observed maxima go to the parity report."""
+    img_o, run = o.render(spp, seed, params=pd, threads=threads, trace=True,
+                          pool_cap=max(400, pd.get("pool_budget", 400)))
+    rec = {"scene": name, "pixels": sc.n_px, "passes": spp, "params": pd, "pool_raw": [], "pool_kept": [],
+           "bound_max_rel": [], "inv_p_max_rel": [], "inv_p_over_tol": [], "c_over_tol": [], "val_over_tol": [],
+           "val_max_rel": [], "flags_differ": [], "contributing": []}
+    with ProxyRenderer(sc, seed, ProxyParams(**pd)) as r:
         for p in range(spp):
             r.render_passes(1)
             pool = r.dump_pool()
             val, bd, c, fl = r.dump_pass()
-            n = run.pool_n[p]
-            print(f"{name} pass {p}: raw {pool['raw']} vs {run.pool_raw[p]}, kept {pool['n']} vs {n}")
-            assert pool["raw"] == run.pool_raw[p]
-            assert pool["n"] == n
+            n = int(run.pool_n[p])
+            assert pool["raw"] == run.pool_raw[p] and pool["n"] == n, (pool["raw"], run.pool_raw[p], pool["n"], n)
             assert np.array_equal(pool["walk"], run.pool_walk[p, :n])
             assert np.array_equal(pool["end"], run.pool_end[p, :n])
             assert np.array_equal(pool["key"], run.pool_key[p, :n])
             eb = rel_err(pool["bound"], run.pool_bound[p, :n])
             ei = rel_err(pool["inv_p"], run.pool_inv_p[p, :n])
-            print(f"   bound max rel {eb.max() if n else 0:.2e}, inverse_p max rel {ei.max() if n else 0:.2e}")
-            assert (eb <= 1e-12).all()
-            assert np.count_nonzero(ei > REL_TOL) <= max(1, n // 100)
             ec = rel_err(c, run.pass_c[p])
             ev = rel_err(val, run.pass_val[p])
-            flag_eq = np.mean(fl == run.pass_flags[p])
-            print(f"   proxy c over tol {np.count_nonzero((ec > REL_TOL).any(1))}, val over tol "
-                  f"{np.count_nonzero((ev > REL_TOL).any(1))}, flags equal {flag_eq:.5f}, "
-                  f"contributing {np.count_nonzero(fl & 8)}")
-            assert np.count_nonzero((ev > REL_TOL).any(1)) <= max(2, sc.n_px // 500)
-            assert flag_eq >= 0.998
+            rec["pool_raw"].append(int(pool["raw"]))
+            rec["pool_kept"].append(n)
+            rec["bound_max_rel"].append(float(eb.max()) if n else 0.0)
+            rec["inv_p_max_rel"].append(float(ei.max()) if n else 0.0)
+            rec["inv_p_over_tol"].append(int(np.count_nonzero(ei > REL_TOL)))
+            rec["c_over_tol"].append(int(np.count_nonzero((ec > REL_TOL).any(1))))
+            rec["val_over_tol"].append(int(np.count_nonzero((ev > REL_TOL).any(1))))
+            rec["val_max_rel"].append(float(ev.max()))
+            rec["flags_differ"].append(int(np.count_nonzero(fl != run.pass_flags[p])))
+            rec["contributing"].append(int(np.count_nonzero(fl & 8)))
         s3, c2, g = r.stats()
         img = r.mean()
-    assert np.array_equal(c2, run.stats_cnt)
+    rec["stats_counts_differ"] = int(np.count_nonzero(c2 != run.stats_cnt))
+    rec["stats_sums_max_rel"] = float(rel_err(s3, run.stats).max())
+    rec["gamma_max_abs"] = float(np.abs(g - run.gamma_rows).max())
+    rec["image_max_rel"] = float(rel_err(img, img_o).max())
+    parity_report(section, rec)
+    print(rec)
+    assert max(rec["bound_max_rel"]) <= 1e-12
+    assert sum(rec["inv_p_over_tol"]) == 0
+    assert sum(rec["c_over_tol"]) == 0 and sum(rec["val_over_tol"]) == 0
+    assert sum(rec["flags_differ"]) == 0
+    assert rec["stats_counts_differ"] == 0
     assert np.allclose(s3, run.stats, rtol=1e-6, atol=0)
     assert np.allclose(g, run.gamma_rows, rtol=1e-6, atol=1e-12)
-    assert np.allclose(img, img_o, rtol=1e-4, atol=1e-10) or \
-        np.count_nonzero(~np.isclose(img, img_o, rtol=1e-4, atol=1e-10)) <= 3 * max(2, sc.n_px // 500)
+    assert np.allclose(img, img_o, rtol=1e-4, atol=1e-10)
+    # observed: bitwise equal (bit-exact trajectories, the same fp64 op order and sum orders)
+    assert max(rec["val_max_rel"]) == 0.0 and max(rec["inv_p_max_rel"]) == 0.0 and rec["image_max_rel"] == 0.0
+    return rec
+
+
+@pytest.mark.parametrize("name", list(PROXY_SCENES))
+def test_proxy_render_matches_oracle(pxg, oracle, name, parity_report):
+    """Proxy on: pool selection, reciprocal estimates, per-pixel proxy connections and the
+    gated per-pass values equal the restated reference loop."""
+    make, pd = PROXY_SCENES[name]
+    sc = make()
+    compare_proxy_render(oracle_scene(oracle, name, sc), sc, pd, 3, 9, name, parity_report)
+
+
+FULL_SIZE = {
+    # BASELINE.json configs[1] at full size: 512^2, depth 10, 262,144 pool walks, 2 passes
+    "C2": (lambda: scenes.cornell_c2(512), {"light_walks": 262144}, 2),
+    # configs[3] (the north star's 1M-triangle scene) at full size: 1920x1080, depth 12,
+    # 2,073,600 pool walks (one per pixel), 1 pass
+    "C4": (lambda: scenes.procedural_c4(1920, 1080, max_depth=12), {"light_walks": 0}, 1),
+}
+
+
+@pytest.mark.parametrize("cfg", list(FULL_SIZE))
+def test_full_size_matches_oracle(pxg, oracle, cfg, parity_report):
+    """The bench workloads at their full size against the restated reference loop
+    (proj/src/proxy.cpp:684-819) on 16 host threads, with the same bars as the small scenes."""
+    make, pd, spp = FULL_SIZE[cfg]
+    sc = make()
+    o = oracle_scene(oracle, "full_" + cfg, sc)
+    compare_proxy_render(o, sc, pd, spp, 0, cfg, parity_report, threads=16, section="full_size")
 
 
 def test_pool_budget_edges(pxg, oracle):
@@ -252,8 +318,8 @@ def test_pretrace_matches_oracle(pxg, oracle):
     with ProxyRenderer(sc, 3, ProxyParams(pretrace_paths=20000, light_walks=100)) as r:
         s3, c2, _ = r.stats()
     assert np.array_equal(c2[:, 0], run.pretrace_cnt)
-    # maxima agree to rounding (sin/cos of CUDA vs glibc differ by <= 2 ulp)
-    assert np.allclose(s3[:, 0], run.pretrace_max, rtol=1e-9, atol=0)
+    # maxima bitwise (the device sin / cos are glibc's, include/pxg_sincos.h)
+    assert np.array_equal(s3[:, 0], run.pretrace_max)
 
 
 def test_recip_two_point_on_device(pxg, oracle):
@@ -301,9 +367,8 @@ def test_diagnostics_match_oracle(pxg, oracle):
     for (u, c, s), row in d.rows.items():
         got[index_of(u, c, s)] = [row.retrace_attempts, row.retrace_accepts, row.recip_runs, row.recip_truncated,
                                   row.estimates_failed]
-    # recip counters are exact; retrace attempts/accepts follow the gated trajectory
-    assert np.array_equal(got[:, 2:], run.diag[:, 2:])
-    assert np.abs(got[:, :2] - run.diag[:, :2]).sum() <= 2
+    # every counter exact, retrace attempts / accepts included (bit-exact trajectories)
+    assert np.array_equal(got, run.diag)
 
 
 def test_truncated_recip_diagnostics_match_oracle(pxg, oracle):
@@ -359,7 +424,7 @@ def test_pt_matches_reference_per_pixel(pxg, oracle, name):
     e = rel_err(img, ref)
     bad = np.count_nonzero((e > REL_TOL).any(axis=-1))
     print(f"{name}: max rel err {e.max():.3e}, pixels over tol {bad} of {sc.n_px}")
-    assert bad <= max(1, sc.n_px // 2000)
+    assert bad == 0
     chunks = render_pt(sc, spp, 11, chunks=3)  # chunk 0 is the same render, chunks 1-2 independent
     assert np.isfinite(chunks).all() and not np.array_equal(chunks, img)
 
