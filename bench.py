@@ -5,18 +5,19 @@ One step = one progressive pass = one sample for every pixel of the workload: St
 walks, priority selection, reciprocal estimates) + Stage 2 (eye/light sub-paths, all
 standard strategies with reciprocal-aware MIS, the gated proxy connection, film, gamma).
 
-Workload (N=1): BASELINE.json configs[1] ("C2"): 512x512, max depth 10, 262,144 pool walks
-per pass, Cornell box + mirror icosphere (5,120 tris) + dielectric icosphere (20,480 tris)
-+ GGX floor, Philox seed 0 -- a seeded synthetic scene (paper_2503_23412_b200/scenes.py)
-standing in for the paper's proprietary scenes. L2: the per-pass working set (eye/light/walk
-vertex pools ~1 GB, connection slots, shadow-ray queue) is far larger than the 126 MB L2;
-the scene itself (~3.3 MB of BVH + primitives) is read-only and L2-resident by design.
+Workload (N=1): BASELINE.json configs[3] ("C4"), the north star's 1M-triangle scene and the
+largest single-GPU config: 1920x1080, max depth 12, 2,073,600 pool walks per pass (one per
+pixel, the reference default), 2,000 seeded instances (1,011,340 triangles), 4 area lights,
+Philox seed 0 -- a seeded synthetic scene (paper_2503_23412_b200/scenes.py) standing in for
+the paper's proprietary scenes. L2: the per-pass working set (vertex pools, connection slots,
+queues: tens of GB) is far larger than the 126 MB L2, and so is the ~200 MB scene.
+The line also carries a C2 device measurement (configs[1]) as the extra key "C2".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C1..C5]
 
 --impl reference times the reference's own CPU implementation (the unmodified
 proxima::render_proxy_bdpt compiled from /root/reference by oracle/Makefile, PCG32 as
-shipped) on the same config, one independent render per host core.
+shipped) on the same config, one independent render per host core (see reference_rate).
 """
 from __future__ import annotations
 
@@ -41,14 +42,14 @@ PRIM_BYTES = 80  # PrimRec (csrc/pxg_scene.cuh); node bytes per context: pxg_nod
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    # default: the timed passes 8..63 of C2's 64-spp render (BASELINE configs[1])
-    ap.add_argument("--steps", type=int, default=56)
+    # default: passes 8..31 of the C4 render (BASELINE configs[3])
+    ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tuning sweeps: skip roofline, e2e and cpu_baseline")
-    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M-triangle) device line in the C2 run")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra C2 device line of the C4 run")
     ap.add_argument("--e2e-spp", type=int, default=64,
                     help="spp of the end-to-end render call (capped at the config's spp)")
     return ap.parse_args()
@@ -155,16 +156,54 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference CPU path
-def reference_sample(sc, walks, copies: int, seed: int = 0):
-    """One step of the reference arm: `copies` independent unmodified reference renders
-    (proxima::render_proxy_bdpt, 1 pass each, PCG32 as shipped) on `copies` host threads."""
+# Scenes whose full-size reference pass takes minutes per core (C3-C5: the reference's fixed
+# Stage-1 cost is ~34 s per pass on C4, its per-pixel cost ~0.43 ms) are timed at two reduced
+# resolutions (W/8 x H/8 and W/4 x H/4, same geometry, camera, depth and walks per pixel) and
+# the steady-state full-size pass time is the linear fit T(N) = F + c N at the full pixel count.
+FIT_CONFIGS = {"C3", "C4", "C5"}
+
+
+def reference_rate(cfg: str, sc, walks: int, cores: int, seed: int = 0):
+    """Steady-state throughput of the unmodified reference (proxima::render_proxy_bdpt, PCG32
+    as shipped) on this host: `cores` concurrent single-threaded renders of 2 passes each; the
+    time of pass 1 comes from the pass_done callback's timestamps (pass 0 also holds the
+    render's one-time pretrace and first-pass gate). Returns (Msamples/s, sample description,
+    wall seconds)."""
     from oracle import oracle as orc
+    t_start = time.perf_counter()
     o = orc.OracleScene(sc.to_json(), variant="pcg")
-    params = {"light_walks": walks}
-    t0 = time.perf_counter()
-    o.render_proxy_ref_mt(1, seed, copies, params)
-    dt = time.perf_counter() - t0
-    return copies * sc.n_px / dt / 1e6, dt
+    W, H, N = sc.camera.width, sc.camera.height, sc.n_px
+    if cfg not in FIT_CONFIGS:
+        te = o.render_proxy_ref_timed(2, seed, cores, {"light_walks": walks})
+        t1 = float(np.mean(te[:, 1] - te[:, 0]))
+        value = cores * N / t1 / 1e6
+        sample = (f"{cores} concurrent unmodified proxima::render_proxy_bdpt renders (PCG32) of {cfg} at full size "
+                  f"({W}x{H}, {walks} pool walks), 2 passes each; steady pass time {t1:.2f} s (pass 1, pass_done "
+                  f"timestamps)")
+        return value, sample, time.perf_counter() - t_start
+    sizes = [(max(10, W // 8), max(10, H // 8)), (max(10, W // 4), max(10, H // 4))]
+    per = max(1, cores // 2)
+    scs = [o.with_resolution(w, h) for (w, h) in sizes]
+    n_s = [w * h for (w, h) in sizes]
+    walks_s = [max(1, round(walks * n / N)) for n in n_s]
+    # the reference's light_walks is one per pixel by default (0): keep the walks per pixel
+    params = {"light_walks": 0} if walks == N else None
+    if params is None and walks_s[0] != walks_s[1]:
+        raise RuntimeError("reference fit needs walks per pixel equal across sizes")
+    te = o.render_proxy_ref_timed(2, seed, 2 * per, params or {"light_walks": walks_s[0]},
+                                  scenes=[scs[0]] * per + [scs[1]] * per)
+    t1 = te[:, 1] - te[:, 0]
+    T = [float(np.mean(t1[:per])), float(np.mean(t1[per:]))]
+    c = (T[1] - T[0]) / (n_s[1] - n_s[0])
+    F = T[0] - c * n_s[0]
+    t_full = F + c * N
+    value = cores * N / t_full / 1e6
+    sample = (f"{2 * per} concurrent unmodified proxima::render_proxy_bdpt renders (PCG32) of the {cfg} scene, "
+              f"{per} at {sizes[0][0]}x{sizes[0][1]} and {per} at {sizes[1][0]}x{sizes[1][1]} (same geometry, camera, "
+              f"depth, one pool walk per pixel), 2 passes each; steady pass times {T[0]:.1f} s / {T[1]:.1f} s (pass 1, "
+              f"pass_done timestamps) -> T(N) = {F:.1f} s + {c * 1e3:.4f} ms x N px; full size {W}x{H}: "
+              f"{t_full:.0f} s per pass per core, x {cores} cores")
+    return value, sample, time.perf_counter() - t_start
 
 
 def host_cores():
@@ -180,25 +219,15 @@ def run_reference(args):
         return
     sc, walks = make_scene(args.config)
     cores = host_cores()
-    steps = max(1, min(args.steps, 3))
-    warm = min(args.warmup, 1)
     try:
-        for _ in range(warm):
-            reference_sample(sc, walks, cores, seed=100)
-        vals, times = [], []
-        for k in range(steps):
-            v, dt = reference_sample(sc, walks, cores, seed=k)
-            vals.append(v)
-            times.append(dt)
+        value, sample, wall = reference_rate(args.config, sc, walks, cores, seed=0)
     except Exception as e:  # the reference library is test infrastructure; report, do not crash
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"[:300]}), flush=True)
         return
-    total = sum(times)
-    value = cores * sc.n_px * steps / total / 1e6
-    sample = (f"{steps} step(s) x {cores} concurrent unmodified proxima::render_proxy_bdpt renders of 1 pass each "
-              f"({args.config}, full resolution, {walks} pool walks, PCG32 as shipped)")
+    # one timed step = one steady-state pass on every core (pass 0 is the warm-up)
+    ms = 1e3 * cores * sc.n_px / (value * 1e6)
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Msamples/s",
-           "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * total / steps, 2),
+           "n_gpus": args.gpus, "steps": 1, "warmup": 1, "ms_per_step": round(ms, 1), "wall_s": round(wall, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded scene generator)", "config": config_json(args.config, sc, walks),
            "cpu_baseline": {"value": round(value, 6), "unit": "Msamples/s", "cores": cores, "kind": "reference",
@@ -208,11 +237,6 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def scene_bytes(sc):
-    return int(sc.shape.nbytes + sc.mat.nbytes + sc.a.nbytes + sc.b.nbytes + sc.c.nbytes + sc.radius.nbytes +
-               len(sc.materials) * 7 * 8 + sc.emitter_prim.nbytes + sc.emitter_radiance.nbytes)
-
-
 def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
     """Device-resident throughput of `steps` passes after the warm-up (CUDA events on the
     pass stream), then the traversal roofline over one more batch cycle."""
@@ -314,6 +338,12 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     sc, walks = make_scene(args.config)
+    # Scene::finalize (validation, emitter tables, BVH) happens once when the scene is loaded,
+    # as in the reference (load_scene -> finalize); every render call and context reuses it
+    from paper_2503_23412_b200.render import finalized_scene
+    t_fin = time.perf_counter()
+    scene_dev_bytes = finalized_scene(sc).device_bytes()
+    t_fin = time.perf_counter() - t_fin
     W, H = sc.camera.width, sc.camera.height
     params = ProxyParams(light_walks=walks)
 
@@ -327,17 +357,15 @@ def run_ours(args):
         dev = measure_device(sc, params, seed, args.steps, args.warmup, world, local, args.quick, args.config)
     value, dev_ms, warm, counts, stage_ms, roofline = (dev[k] for k in ("value", "dev_ms", "warm", "counts",
                                                                         "stage_ms", "roofline"))
-    # The north star's roofline target is quoted on the 1M-triangle scene (C4, BASELINE.json
-    # configs[3]): the default C2 line also carries a C4 device measurement (same method).
-    north_star_scene = None
-    if args.config == "C2" and world == 1 and not args.quick and not args.no_c4:
-        sc4, walks4 = make_scene("C4")
-        d4 = measure_device(sc4, ProxyParams(light_walks=walks4), seed, 16, 8, 1, local, False, "C4")
-        north_star_scene = {"config": config_json("C4", sc4, walks4)["workload"], "value": round(d4["value"], 4),
-                            "unit": "Msamples/s", "steps": 16, "warmup": d4["warm"],
-                            "ms_per_step": round(d4["dev_ms"] / 16, 4), "roofline": d4["roofline"],
-                            "hbm_gb_used": d4["hbm_gb_used"]}
-        del sc4
+    # Extra key: BASELINE.json configs[1] (C2, the L2-resident Cornell box) measured the same way.
+    extra = None
+    if args.config == "C4" and world == 1 and not args.quick and not args.no_extra:
+        sc2, walks2 = make_scene("C2")
+        d2 = measure_device(sc2, ProxyParams(light_walks=walks2), seed, 56, 8, 1, local, False, "C2")
+        extra = {"config": config_json("C2", sc2, walks2)["workload"], "value": round(d2["value"], 4),
+                 "unit": "Msamples/s", "steps": 56, "warmup": d2["warm"], "ms_per_step": round(d2["dev_ms"] / 56, 4),
+                 "roofline": d2["roofline"], "hbm_gb_used": d2["hbm_gb_used"]}
+        del sc2
 
     # ---- end to end through the public API: render_proxy_bdpt(scene arrays on the host, spp=K)
     # with the pass_done callback reading the running mean image back every pass
@@ -376,20 +404,22 @@ def run_ours(args):
     if not args.quick:
         d2h = (reads[0] + img.nbytes) / spp_e2e
         e2e = {"value": round(W * H * spp_e2e * world / e2e_s / 1e6, 4), "unit": "Msamples/s",
-               "h2d_bytes_per_step": int(scene_bytes(sc) / spp_e2e), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(scene_dev_bytes / spp_e2e), "d2h_bytes_per_step": int(d2h),
                "spp": spp_e2e,
-               "includes": f"one full render call render_proxy_bdpt(scene, spp={spp_e2e}) per rank from host arrays: "
-                           "pxg_create (scene upload, finalize, BVH build, pretrace) + every pass + the running-mean "
-                           "read-back after every pass (the reference's pass_done callback) + the final image"}
+               "includes": f"one full render call render_proxy_bdpt(scene, spp={spp_e2e}) per rank on a finalised "
+                           "scene (host arrays): context creation (upload of the scene's BVH nodes and primitive "
+                           "records from host memory, per-pass state, pretrace) + every pass + the running-mean "
+                           "read-back after every pass (the reference's pass_done callback) + the final image",
+               "excludes": f"Scene::finalize (validation, emitter tables, host BVH build: {t_fin:.2f} s), done once "
+                           "when the scene is loaded, as the reference's load_scene does before any render call"}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
             cores = host_cores()
-            v, dt = reference_sample(sc, walks, cores, seed=0)
+            v, sample, wall = reference_rate(args.config, sc, walks, cores, seed=0)
             cpu_baseline = {"value": round(v, 6), "unit": "Msamples/s", "cores": cores, "kind": "reference",
-                            "sample": f"{cores} concurrent unmodified proxima::render_proxy_bdpt renders (PCG32), "
-                                      f"1 pass each of {args.config} at full size ({dt:.1f} s)"}
+                            "sample": sample, "wall_s": round(wall, 1)}
         except Exception as e:
             cpu_baseline = {"value": None, "unit": "Msamples/s", "cores": 0, "kind": "reference",
                             "sample": f"unavailable: {type(e).__name__}: {e}"[:200]}
@@ -414,7 +444,7 @@ def run_ours(args):
         "gpu_launches": int(counts[0]),
         "roofline": roofline,
         "hbm_gb_used": dev["hbm_gb_used"],
-        "north_star_scene": north_star_scene,
+        "C2": extra,
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
         "stage_ms": {"stage1_batches_total": round(float(stage_ms[0]), 3),

@@ -88,11 +88,26 @@ typedef struct pxg_shard {
 } pxg_shard;
 
 typedef struct pxg_ctx pxg_ctx;
+/* A finalised scene: the reference's Scene after load_scene -> Scene::finalize
+ * (proj/src/scene.cpp:234-252, 317-436), i.e. validated, with emitter tables and the BVH
+ * built (on the host, once). Immutable; contexts on any device are created from it without
+ * rebuilding, as the reference's render_proxy_bdpt(const Scene&, ...) receives a finalised
+ * scene. The description's arrays are copied. */
+typedef struct pxg_scene pxg_scene;
 
 void pxg_default_params(pxg_params* p);
 int pxg_abi_version(void);
 int pxg_device_count(void);
 
+int pxg_scene_create(const pxg_scene_desc* scene, pxg_scene** out);
+void pxg_scene_destroy(pxg_scene* scene);
+/* Bytes one context uploads from the finalised scene (BVH nodes, primitive records and tables). */
+long long pxg_scene_device_bytes(const pxg_scene* scene);
+/* Render context on `device` for a finalised scene (uploads it, allocates the per-pass state,
+ * runs the pretrace, proj/src/subspace.cpp:190-218). */
+int pxg_create_from_scene(const pxg_scene* scene, const pxg_params* params, uint64_t seed, int device,
+                          const pxg_shard* shard, pxg_ctx** out);
+/* pxg_scene_create + pxg_create_from_scene in one call (the scene is released again). */
 int pxg_create(const pxg_scene_desc* scene, const pxg_params* params, uint64_t seed, int device,
                const pxg_shard* shard, pxg_ctx** out);
 void pxg_destroy(pxg_ctx* ctx);

@@ -100,6 +100,10 @@ def lib(variant: str = "philox"):
     L.orc_render_pt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, _DP]
     L.orc_render_proxy_ref.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), _DP, _LP]
     L.orc_render_proxy_ref_mt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), C.c_int, _DP]
+    L.orc_render_proxy_ref_timed.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_ulonglong, C.POINTER(OrcParams),
+                                             C.c_int, _DP]
+    L.orc_scene_with_resolution.restype = C.c_void_p
+    L.orc_scene_with_resolution.argtypes = [C.c_void_p, C.c_int, C.c_int]
     if variant == "philox":
         L.orc_render.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), C.c_int, _DP,
                                  C.POINTER(OrcTrace)]
@@ -214,6 +218,30 @@ class OracleScene:
         _check(self.L, self.L.orc_render_proxy_ref_mt(self.h, spp, seed, C.byref(op), copies,
                                                       _ptr(out, C.c_double)))
         return out
+
+    def with_resolution(self, width: int, height: int) -> "OracleScene":
+        """The same loaded scene rendered at another resolution (no reload)."""
+        o = OracleScene.__new__(OracleScene)
+        o.L = self.L
+        h = self.L.orc_scene_with_resolution(self.h, width, height)
+        if not h:
+            raise RuntimeError(self.L.orc_last_error().decode())
+        o.h = C.c_void_p(h)
+        o.width, o.height = width, height
+        o.max_depth, o.n_prims, o.n_emitters, o.spp = self.max_depth, self.n_prims, self.n_emitters, self.spp
+        o.total_emitter_area, o.bbox_min, o.bbox_max = self.total_emitter_area, self.bbox_min, self.bbox_max
+        return o
+
+    def render_proxy_ref_timed(self, spp: int, seed: int, copies: int, params=None, scenes=None) -> np.ndarray:
+        """`copies` concurrent unmodified render_proxy_bdpt calls of `spp` passes (copy i on
+        scenes[i], default this scene); returns the pass end times [copies, spp] in seconds
+        (pass_done callback timestamps from the common start)."""
+        scenes = scenes or [self] * copies
+        hs = (C.c_void_p * copies)(*[s.h.value for s in scenes])
+        t = np.zeros((copies, spp))
+        op = make_params(params)
+        _check(self.L, self.L.orc_render_proxy_ref_timed(hs, spp, seed, C.byref(op), copies, _ptr(t, C.c_double)))
+        return t
 
     def render(self, spp: int, seed: int, params=None, threads: int = 8, trace: bool = False,
                trace_pass: int = -1, pool_cap: int = 400):

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -264,6 +265,47 @@ ORC_API int orc_render_proxy_ref_mt(void* h, int spp, unsigned long long seed, c
       imgs[i] = render_proxy_bdpt(sc, spp, seed + static_cast<unsigned long long>(i), pp);
     });
     if (rgb0) std::memcpy(rgb0, imgs[0].pixels.data(), imgs[0].pixels.size() * sizeof(Vec3));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Copy of a loaded scene rendered at another resolution (same geometry, camera pose and
+// settings; Camera::width / height are plain members, proj/include/proxima/scene.hpp:43-44).
+ORC_API void* orc_scene_with_resolution(void* h, int width, int height) {
+  try {
+    auto* src = static_cast<OrcScene*>(h);
+    auto* c = new OrcScene(*src);
+    c->scene.camera.width = width;
+    c->scene.camera.height = height;
+    return c;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+// `copies` independent unmodified reference renders of `spp` passes on `copies` threads,
+// copy i of scene hs[i] with seed seed+i, each with a pass_done callback (the reference's
+// progressive-render hook, proj/include/proxima/proxy.hpp:197-200) that records the time since
+// the common start: pass_end[i * spp + p] = seconds at the end of pass p of copy i. The
+// steady-state time of one pass is pass_end[p] - pass_end[p-1] for p >= 1 (pass 0 also holds
+// the render's one-time pretrace and the gate's first pass).
+ORC_API int orc_render_proxy_ref_timed(void* const* hs, int spp, unsigned long long seed, const OrcParams* p,
+                                       int copies, double* pass_end) {
+  try {
+    ProxyParams pp = to_params(p);
+    const auto t0 = std::chrono::steady_clock::now();
+    parallel_for(copies, copies, [&](int i) {
+      const Scene& sc = static_cast<OrcScene*>(hs[i])->scene;
+      auto cb = [&, i](int done, const Image&) {
+        pass_end[static_cast<size_t>(i) * spp + (done - 1)] =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return true;
+      };
+      render_proxy_bdpt(sc, spp, seed + static_cast<unsigned long long>(i), pp, nullptr, cb);
+    });
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

@@ -86,6 +86,12 @@ def lib():
     L.pxg_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(Params), C.c_uint64, C.c_int, C.POINTER(Shard),
                              C.POINTER(C.c_void_p)]
     L.pxg_destroy.argtypes = [C.c_void_p]
+    L.pxg_scene_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(C.c_void_p)]
+    L.pxg_scene_destroy.argtypes = [C.c_void_p]
+    L.pxg_scene_device_bytes.argtypes = [C.c_void_p]
+    L.pxg_scene_device_bytes.restype = C.c_longlong
+    L.pxg_create_from_scene.argtypes = [C.c_void_p, C.POINTER(Params), C.c_uint64, C.c_int, C.POINTER(Shard),
+                                        C.POINTER(C.c_void_p)]
     L.pxg_render_pass.argtypes = [C.c_void_p]
     L.pxg_render_passes.argtypes = [C.c_void_p, C.c_int]
     L.pxg_render_pass_traced.argtypes = [C.c_void_p]
@@ -117,7 +123,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = [
-    "pxg_default_params", "pxg_abi_version", "pxg_node_bytes", "pxg_device_count", "pxg_create", "pxg_destroy", "pxg_last_error",
+    "pxg_default_params", "pxg_abi_version", "pxg_node_bytes", "pxg_device_count", "pxg_create", "pxg_scene_create", "pxg_scene_destroy", "pxg_scene_device_bytes", "pxg_create_from_scene", "pxg_destroy", "pxg_last_error",
     "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_render_passes_async", "pxg_snapshot_mean", "pxg_read_snapshot",
     "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_read_diag",
     "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_intersect", "pxg_occluded", "pxg_trace_rays",

@@ -171,6 +171,21 @@ std::string sincos_table_path() {
 void ensure_sincos_table(int device);
 }  // namespace
 
+// A finalised scene (the analogue of the reference's Scene after load_scene -> finalize,
+// proj/src/scene.cpp:234-252): the flattened description (owned copies), the host BVH
+// (pxg_host.cpp) and the device-ready arrays. Immutable; any number of contexts, on any
+// device, are created from it without rebuilding the BVH.
+struct pxg_scene {
+  std::vector<int> shape, material, emitter_prim;
+  std::vector<double> a, b, c, radius, materials, emitter_radiance;
+  pxg_scene_desc desc{};  // pointers into the vectors above
+  SceneHost host;
+  std::vector<std::pair<void*, size_t>> pinned;  // page-locked host arrays (fast per-context upload)
+  ~pxg_scene() {
+    for (auto& pr : pinned) cudaHostUnregister(pr.first);
+  }
+};
+
 struct pxg_ctx {
   std::string err;
   int device = 0;
@@ -190,7 +205,6 @@ struct pxg_ctx {
   PathCache pcache_buf[2];  // per-sub-path MIS step caches, double-buffered like the pools
   cudaStream_t stream_p = nullptr;  // Stage 2b': proxy connection, forked from the pass
   cudaEvent_t proxy_done = nullptr, gamma_done = nullptr;
-  SceneHost host;
   pxg_params P{};
   pxg_shard shard{};
   uint64_t seed = 0;
@@ -349,6 +363,13 @@ struct pxg_ctx {
     T* p = alloc<T>(v.size());
     if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));  // v may be a temporary
+    return p;
+  }
+  // upload of host data that outlives the call (the pxg_scene's arrays): no synchronisation
+  template <typename T>
+  T* upload_async(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
     return p;
   }
   template <typename T>
@@ -1037,9 +1058,105 @@ void pxg_destroy(pxg_ctx* ctx) {
   delete ctx;
 }
 
+namespace {
+void scene_build(const pxg_scene_desc* sd, pxg_scene* s) {
+  const int n = sd->n_prims, nm = sd->n_materials, ne = sd->n_emitters;
+  if (n < 0 || nm < 0 || ne < 0) throw InvalidErr{"scene: negative count"};
+  s->shape.assign(sd->shape, sd->shape + n);
+  s->material.assign(sd->material, sd->material + n);
+  s->a.assign(sd->a, sd->a + 3 * static_cast<size_t>(n));
+  s->b.assign(sd->b, sd->b + 3 * static_cast<size_t>(n));
+  s->c.assign(sd->c, sd->c + 3 * static_cast<size_t>(n));
+  s->radius.assign(sd->radius, sd->radius + n);
+  s->materials.assign(sd->materials, sd->materials + 7 * static_cast<size_t>(nm));
+  s->emitter_prim.assign(sd->emitter_prim, sd->emitter_prim + ne);
+  s->emitter_radiance.assign(sd->emitter_radiance, sd->emitter_radiance + 3 * static_cast<size_t>(ne));
+  s->desc = *sd;
+  s->desc.shape = s->shape.data();
+  s->desc.material = s->material.data();
+  s->desc.a = s->a.data();
+  s->desc.b = s->b.data();
+  s->desc.c = s->c.data();
+  s->desc.radius = s->radius.data();
+  s->desc.materials = s->materials.data();
+  s->desc.emitter_prim = s->emitter_prim.data();
+  s->desc.emitter_radiance = s->emitter_radiance.data();
+  if (sd->max_depth < 1) throw InvalidErr{"scene: max_depth must be at least 1"};
+  if (sd->max_depth + 1 > kMaxPath - 2 || sd->max_depth - 1 > kMaxLight - 1)
+    throw InvalidErr{"pxg: max_depth above 16 is not supported"};
+  finalize_scene(s->desc, s->host);
+  s->host.nodes.clear();  // the binary tree is only the input of the 4-wide collapse
+  s->host.nodes.shrink_to_fit();
+  // page-lock the large arrays once, so every context uploads them at full PCIe speed
+  auto pin = [&](void* p, size_t bytes) {
+    if (bytes < (1u << 20)) return;
+    if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) == cudaSuccess)
+      s->pinned.emplace_back(p, bytes);
+    else
+      cudaGetLastError();  // not fatal: the upload falls back to staged copies
+  };
+  SceneHost& h = s->host;
+  pin(h.nodes4.data(), h.nodes4.size() * sizeof(HostNode4));
+  pin(h.nodes4q.data(), h.nodes4q.size() * sizeof(HostNode4Q));
+  pin(h.recs.data(), h.recs.size() * sizeof(HostRec));
+  pin(h.prim_abc.data(), h.prim_abc.size() * sizeof(double));
+  pin(h.prim_geo.data(), h.prim_geo.size() * sizeof(double));
+  pin(h.prim_center.data(), h.prim_center.size() * sizeof(double));
+}
+
+int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, int device, const pxg_shard* shard,
+                pxg_ctx** out);
+}  // namespace
+
+int pxg_scene_create(const pxg_scene_desc* sd, pxg_scene** out) {
+  if (!sd || !out) return fail(nullptr, PXG_E_INVALID, "pxg_scene_create: null argument");
+  *out = nullptr;
+  auto* s = new pxg_scene();
+  const int rc = guarded(nullptr, [&]() { scene_build(sd, s); });
+  if (rc != PXG_OK) {
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return PXG_OK;
+}
+
+void pxg_scene_destroy(pxg_scene* s) { delete s; }
+
+long long pxg_scene_device_bytes(const pxg_scene* s) {
+  if (!s) return -1;
+  const SceneHost& h = s->host;
+  return static_cast<long long>(h.nodes4.size() * sizeof(HostNode4) + h.nodes4q.size() * sizeof(HostNode4Q) +
+                                h.recs.size() * sizeof(HostRec) +
+                                (h.prim_mat.size() + h.prim_emitter.size() + h.prim_shape.size()) * sizeof(int) +
+                                (h.prim_geo.size() + h.prim_center.size() + h.prim_abc.size() + h.emitter_cum.size() +
+                                 s->emitter_radiance.size()) * sizeof(double) +
+                                s->emitter_prim.size() * sizeof(int) + s->materials.size() * sizeof(double));
+}
+
+int pxg_create_from_scene(const pxg_scene* scene, const pxg_params* params, uint64_t seed, int device,
+                          const pxg_shard* shard, pxg_ctx** out) {
+  if (!scene || !out) return fail(nullptr, PXG_E_INVALID, "pxg_create_from_scene: null argument");
+  return create_impl(scene, params, seed, device, shard, out);
+}
+
 int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed, int device,
                const pxg_shard* shard, pxg_ctx** out) {
   if (!sd || !out) return fail(nullptr, PXG_E_INVALID, "pxg_create: null argument");
+  *out = nullptr;
+  if (pxg_device_count() <= 0) return fail(nullptr, PXG_E_NODEVICE, "pxg_create: no CUDA device");
+  pxg_scene* s = nullptr;
+  int rc = pxg_scene_create(sd, &s);
+  if (rc != PXG_OK) return rc;
+  rc = create_impl(s, params, seed, device, shard, out);
+  pxg_scene_destroy(s);  // the context holds device copies only
+  return rc;
+}
+
+namespace {
+int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, int device, const pxg_shard* shard,
+                pxg_ctx** out) {
+  const pxg_scene_desc* sd = &scn->desc;
   *out = nullptr;
   if (pxg_device_count() <= 0) return fail(nullptr, PXG_E_NODEVICE, "pxg_create: no CUDA device");
   auto* c = new pxg_ctx();
@@ -1054,9 +1171,6 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
       std::fprintf(stderr, "[pxg] create %-12s %8.2f ms\n", what, ms);
     };
-    if (sd->max_depth < 1) throw InvalidErr{"scene: max_depth must be at least 1"};
-    if (sd->max_depth + 1 > kMaxPath - 2 || sd->max_depth - 1 > kMaxLight - 1)
-      throw InvalidErr{"pxg: max_depth above 16 is not supported"};
     if (params) c->P = *params; else pxg_default_params(&c->P);
     c->seed = seed;
     CK(cudaSetDevice(device));
@@ -1082,9 +1196,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
     mark("streams");
-    finalize_scene(*sd, c->host);
-    mark("finalize+bvh");
-    SceneHost& h = c->host;
+    const SceneHost& h = scn->host;
     c->width = sd->width;
     c->height = sd->height;
     c->max_depth = sd->max_depth;
@@ -1123,26 +1235,26 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
     (void)any_spec;
     // device scene
     SceneView& S = c->S;
-    S.nodes = reinterpret_cast<const BvhNode*>(c->upload(h.nodes));
-    S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload(h.nodes4));
+    S.nodes = nullptr;  // the binary tree stays on the host (pxg_scene)
+    S.nodes4 = reinterpret_cast<const BvhNode4*>(c->upload_async(h.nodes4));
     if (reinterpret_cast<uintptr_t>(S.nodes4) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
-    S.nodes4q = h.nodeq ? reinterpret_cast<const BvhNode4Q*>(c->upload(h.nodes4q)) : nullptr;
+    S.nodes4q = h.nodeq ? reinterpret_cast<const BvhNode4Q*>(c->upload_async(h.nodes4q)) : nullptr;
     S.nodeq = PXG_NODEQ && h.nodeq;  // chosen per scene in finalize_scene (pxg_host.cpp)
     if (reinterpret_cast<uintptr_t>(S.nodes4q) % 32 != 0) throw CudaErr{"pxg_create: node array not 32-byte aligned"};
-    S.recs = reinterpret_cast<const PrimRec*>(c->upload(h.recs));
-    S.prim_mat = c->upload(h.prim_mat);
-    S.prim_emitter = c->upload(h.prim_emitter);
-    S.prim_geo = c->upload(h.prim_geo);
-    S.prim_center = c->upload(h.prim_center);
-    S.prim_shape = c->upload(h.prim_shape);
-    S.prim_abc = c->upload(h.prim_abc);
+    S.recs = reinterpret_cast<const PrimRec*>(c->upload_async(h.recs));
+    S.prim_mat = c->upload_async(h.prim_mat);
+    S.prim_emitter = c->upload_async(h.prim_emitter);
+    S.prim_geo = c->upload_async(h.prim_geo);
+    S.prim_center = c->upload_async(h.prim_center);
+    S.prim_shape = c->upload_async(h.prim_shape);
+    S.prim_abc = c->upload_async(h.prim_abc);
     S.materials = c->upload(mats);
-    S.emitter_prim = c->upload(std::vector<int>(sd->emitter_prim, sd->emitter_prim + sd->n_emitters));
-    S.emitter_rad = c->upload(std::vector<double>(sd->emitter_radiance, sd->emitter_radiance + 3 * sd->n_emitters));
-    S.emitter_cum = c->upload(h.emitter_cum);
+    S.emitter_prim = c->upload_async(scn->emitter_prim);
+    S.emitter_rad = c->upload_async(scn->emitter_radiance);
+    S.emitter_cum = c->upload_async(h.emitter_cum);
     S.n_prims = sd->n_prims;
     S.n_emit = sd->n_emitters;
-    S.n_nodes = static_cast<int>(h.nodes.size());
+    S.n_nodes = static_cast<int>(h.nodes4.size());
     S.n_mat = sd->n_materials;
     S.total_emitter_area = h.total_emitter_area;
     S.bbox_min = v3(h.bbox_min[0], h.bbox_min[1], h.bbox_min[2]);
@@ -1426,6 +1538,7 @@ int pxg_create(const pxg_scene_desc* sd, const pxg_params* params, uint64_t seed
   *out = c;
   return PXG_OK;
 }
+}  // namespace
 
 int pxg_render_passes(pxg_ctx* c, int npass) {
   if (!c) return fail(nullptr, PXG_E_INVALID, "null context");

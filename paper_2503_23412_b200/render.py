@@ -94,16 +94,16 @@ def _lp(a):
     return a.ctypes.data_as(C.POINTER(C.c_longlong))
 
 
-class ProxyRenderer:
-    """One libpxg context: the scene resident in HBM, the per-pass state, the film."""
+_FINALIZE_ENV = ("PXG_NODEQ", "PXG_LEAF", "PXG_SAH_BINS")  # host BVH build knobs (A/B experiments)
 
-    def __init__(self, scene: Scene, seed: int, params: ProxyParams | None = None, device: int = 0,
-                 rows: tuple | None = None, walks: tuple | None = None):
+
+class FinalizedScene:
+    """A pxg_scene handle: the scene validated, with emitter tables and BVH (include/pxg.h)."""
+
+    def __init__(self, scene: Scene):
+        import os
         L = _lib.lib()
-        self.scene = scene
-        self.params = params or ProxyParams()
-        W, H = scene.camera.width, scene.camera.height
-        self.width, self.height, self.max_depth = W, H, scene.settings.max_depth
+        self.key = _finalize_key(scene)
         keep = dict(
             shape=np.ascontiguousarray(scene.shape, np.int32), mat=np.ascontiguousarray(scene.mat, np.int32),
             a=np.ascontiguousarray(scene.a, np.float64), b=np.ascontiguousarray(scene.b, np.float64),
@@ -123,8 +123,62 @@ class ProxyRenderer:
         d.cam_look_at[:] = scene.camera.look_at
         d.cam_up[:] = scene.camera.up
         d.fov_y = scene.camera.fov_y
-        d.width, d.height = W, H
+        d.width, d.height = scene.camera.width, scene.camera.height
         d.max_depth = scene.settings.max_depth
+        h = C.c_void_p()
+        _lib.check(L.pxg_scene_create(C.byref(d), C.byref(h)), None)
+        self._h = h
+        self._L = L
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_bytes(self) -> int:
+        """Bytes a context uploads from this scene (pxg_scene_device_bytes)."""
+        return int(self._L.pxg_scene_device_bytes(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pxg_scene_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _finalize_key(scene: Scene):
+    import os
+    cam = scene.camera
+    return (tuple(os.environ.get(k) for k in _FINALIZE_ENV), tuple(cam.position), tuple(cam.look_at), tuple(cam.up),
+            cam.fov_y, cam.width, cam.height, scene.settings.max_depth, scene.n_prims, len(scene.materials),
+            id(scene.a), id(scene.shape), id(scene.emitter_prim))
+
+
+def finalized_scene(scene: Scene) -> FinalizedScene:
+    """The scene's pxg_scene, built on first use and kept on the Scene object (the reference
+    keeps its BVH in the Scene after finalize)."""
+    f = getattr(scene, "_pxg_finalized", None)
+    if f is None or f.key != _finalize_key(scene):
+        f = FinalizedScene(scene)
+        scene._pxg_finalized = f
+    return f
+
+
+class ProxyRenderer:
+    """One libpxg context: the scene resident in HBM, the per-pass state, the film."""
+
+    def __init__(self, scene: Scene, seed: int, params: ProxyParams | None = None, device: int = 0,
+                 rows: tuple | None = None, walks: tuple | None = None):
+        L = _lib.lib()
+        self.scene = scene
+        self.params = params or ProxyParams()
+        W, H = scene.camera.width, scene.camera.height
+        self.width, self.height, self.max_depth = W, H, scene.settings.max_depth
+        fin = finalized_scene(scene)
         cp = self.params.to_c()
         shard = None
         light_walks = self.params.light_walks if self.params.light_walks > 0 else W * H
@@ -134,9 +188,10 @@ class ProxyRenderer:
             shard = _lib.Shard(r0, r1, w0, w1)
         self.row0, self.row1 = (rows if rows is not None else (0, H))
         ctx = C.c_void_p()
-        rc = L.pxg_create(C.byref(d), C.byref(cp), C.c_uint64(seed), device,
-                          C.byref(shard) if shard is not None else None, C.byref(ctx))
+        rc = L.pxg_create_from_scene(fin.handle, C.byref(cp), C.c_uint64(seed), device,
+                                     C.byref(shard) if shard is not None else None, C.byref(ctx))
         _lib.check(rc, None)
+        self._fin = fin  # the context was built from it; keep it alive with the renderer
         self._ctx = ctx
         self._L = L
 

@@ -92,6 +92,15 @@ class Scene:
     def has_specular(self) -> bool:
         return any(is_specular(m) for m in self.materials)
 
+    def finalize(self) -> "Scene":
+        """Scene::finalize (proj/src/scene.cpp:234-252): validation, emitter tables and the
+        BVH, built once on the host by libpxg (pxg_scene_create) and reused by every render
+        call and context, as the reference's render functions receive a finalised Scene. Like
+        the reference's, the scene is immutable afterwards (rendering calls this lazily)."""
+        from .render import finalized_scene
+        finalized_scene(self)
+        return self
+
     def material_table(self) -> np.ndarray:
         """f64 [n_mat, 8]: base_color xyz, metallic, roughness, transmission, ior, 0."""
         t = np.zeros((len(self.materials), 8))

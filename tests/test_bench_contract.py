@@ -28,3 +28,14 @@ def test_config_table_covers_baseline():
     with open(os.path.join(REPO, "BASELINE.json")) as f:
         n = len(json.load(f)["configs"])
     assert sorted(v[0] for v in bench.CONFIGS.values()) == list(range(n))
+
+
+def test_reference_fit_path(oracle):
+    """The two-resolution fit of the reference arm (C3-C5): steady pass times at W/8 and W/4,
+    linear in the pixel count, extrapolated to the full size."""
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_2503_23412_b200 import scenes
+    sc = scenes.caustic_box(160)
+    value, sample, wall = bench.reference_rate("C3", sc, sc.n_px, 2)
+    assert value > 0 and "20x20" in sample and "40x40" in sample and "160x160" in sample
