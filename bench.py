@@ -255,11 +255,19 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
     BATCH = 8
     warm = -(-max(warmup, 3) // BATCH) * BATCH
     r.set_pass_limit(warm + BATCH)
-    for _ in range(warm):
-        r.render_passes(1)
-        if world > 1:
-            r.accum_to_device(acc.data_ptr())
+    ts = torch.cuda.current_stream()
+
+    def one_pass():
+        if world > 1:  # pass -> stream-ordered accumulator copy -> NCCL all-reduce, no host wait
+            r.render_passes_async(1)
+            r.accum_to_device(acc.data_ptr(), stream=ts.cuda_stream)
             dist.all_reduce(acc)
+        else:
+            r.render_passes(1)
+
+    for _ in range(warm):
+        one_pass()
+    r.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -270,12 +278,10 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
         r.render_passes(steps)
         torch.cuda.synchronize()
     else:
-        ev0.record()
+        ev0.record(ts)
         for _ in range(steps):
-            r.render_passes(1)
-            r.accum_to_device(acc.data_ptr())
-            dist.all_reduce(acc)
-        ev1.record()
+            one_pass()
+        ev1.record(ts)
         torch.cuda.synchronize()
     stage_ms, counts = r.timing()
     if world == 1:

@@ -152,7 +152,13 @@ int pxg_read_mean(pxg_ctx* ctx, double* rgb, int* passes_done);
 /* Unnormalised accumulator (sum of per-pass values), for shard reduction. */
 int pxg_read_accum(pxg_ctx* ctx, double* rgb, int* passes_done);
 /* Same, copied device-to-device into `dst` (a device buffer on the context's GPU, e.g. a
- * torch tensor that is then NCCL-reduced across ranks). */
+ * tensor that is then NCCL-reduced across ranks), stream-ordered against the caller's CUDA
+ * stream `stream` (a cudaStream_t; NULL = the legacy default stream): the copy starts after the
+ * work already enqueued on `stream` (so it never overwrites `dst` while an earlier in-place
+ * reduce is still running) and includes every pass enqueued on the context so far; work the
+ * caller enqueues on `stream` afterwards runs after the copy. Never blocks the host. */
+int pxg_accum_to_device_async(pxg_ctx* ctx, double* dst, void* stream, int* passes_done);
+/* pxg_accum_to_device_async on the legacy default stream, then waits for the copy. */
 int pxg_accum_to_device(pxg_ctx* ctx, double* dst, int* passes_done);
 
 /* ProxyDiagnostics: rows[4000*5] = {retrace_attempts, retrace_accepts, recip_runs,

@@ -99,7 +99,8 @@ def lib(variant: str = "philox"):
     L.orc_render_bdpt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, _DP]
     L.orc_render_pt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, _DP]
     L.orc_render_proxy_ref.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), _DP, _LP]
-    L.orc_render_proxy_ref_mt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), C.c_int, _DP]
+    L.orc_render_proxy_ref_mt.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), C.c_int, _DP,
+                                          _DP]
     L.orc_render_proxy_ref_timed.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_ulonglong, C.POINTER(OrcParams),
                                              C.c_int, _DP]
     L.orc_scene_with_resolution.restype = C.c_void_p
@@ -212,12 +213,15 @@ class OracleScene:
                                                    _ptr(rk, C.c_longlong)))
         return out, int(rk[0]), int(rk[1])
 
-    def render_proxy_ref_mt(self, spp: int, seed: int, copies: int, params=None):
+    def render_proxy_ref_mt(self, spp: int, seed: int, copies: int, params=None, all_images: bool = False):
+        """`copies` independent unmodified render_proxy_bdpt calls (seeds seed + i) on `copies`
+        threads; returns copy 0's image, or all of them [copies, H, W, 3]."""
         out = np.zeros((self.height, self.width, 3))
+        allimg = np.zeros((copies, self.height, self.width, 3)) if all_images else None
         op = make_params(params)
         _check(self.L, self.L.orc_render_proxy_ref_mt(self.h, spp, seed, C.byref(op), copies,
-                                                      _ptr(out, C.c_double)))
-        return out
+                                                      _ptr(out, C.c_double), _ptr(allimg, C.c_double)))
+        return allimg if all_images else out
 
     def with_resolution(self, width: int, height: int) -> "OracleScene":
         """The same loaded scene rendered at another resolution (no reload)."""

@@ -256,7 +256,7 @@ ORC_API int orc_render_proxy_ref(void* h, int spp, unsigned long long seed, cons
 // Runs `copies` independent unmodified reference renders on `copies` threads (distinct
 // seeds seed+i); used to time the single-threaded reference on every host core.
 ORC_API int orc_render_proxy_ref_mt(void* h, int spp, unsigned long long seed, const OrcParams* p,
-                                    int copies, double* rgb0) {
+                                    int copies, double* rgb0, double* rgb_all) {
   try {
     const Scene& sc = static_cast<OrcScene*>(h)->scene;
     ProxyParams pp = to_params(p);
@@ -265,6 +265,10 @@ ORC_API int orc_render_proxy_ref_mt(void* h, int spp, unsigned long long seed, c
       imgs[i] = render_proxy_bdpt(sc, spp, seed + static_cast<unsigned long long>(i), pp);
     });
     if (rgb0) std::memcpy(rgb0, imgs[0].pixels.data(), imgs[0].pixels.size() * sizeof(Vec3));
+    if (rgb_all)
+      for (int i = 0; i < copies; ++i)
+        std::memcpy(rgb_all + static_cast<size_t>(i) * imgs[i].pixels.size() * 3, imgs[i].pixels.data(),
+                    imgs[i].pixels.size() * sizeof(Vec3));
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

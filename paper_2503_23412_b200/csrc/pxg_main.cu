@@ -205,6 +205,7 @@ struct pxg_ctx {
   PathCache pcache_buf[2];  // per-sub-path MIS step caches, double-buffered like the pools
   cudaStream_t stream_p = nullptr;  // Stage 2b': proxy connection, forked from the pass
   cudaEvent_t proxy_done = nullptr, gamma_done = nullptr;
+  cudaEvent_t x_in = nullptr, x_out = nullptr;  // pxg_accum_to_device_async: caller <-> context ordering
   pxg_params P{};
   pxg_shard shard{};
   uint64_t seed = 0;
@@ -398,7 +399,7 @@ struct pxg_ctx {
     if (stream1) cudaStreamDestroy(stream1);
     if (stream_t) cudaStreamDestroy(stream_t);
     if (stream_p) cudaStreamDestroy(stream_p);
-    for (cudaEvent_t e : {proxy_done, gamma_done})
+    for (cudaEvent_t e : {proxy_done, gamma_done, x_in, x_out})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {trace_done[0], trace_done[1], paths_free[0], paths_free[1]})
       if (e) cudaEventDestroy(e);
@@ -973,8 +974,24 @@ int fail(pxg_ctx* c, int code, const std::string& msg) {
   return code;
 }
 
+// Restores the caller's current device on exit (a host thread driving several GPUs keeps its
+// own device selection across libpxg calls).
+struct DeviceRestore {
+  int dev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = -1;
+    }
+  }
+  ~DeviceRestore() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+};
+
 template <typename F>
 int guarded(pxg_ctx* c, F&& f) {
+  DeviceRestore keep;
   try {
     if (c) CK(cudaSetDevice(c->device));
     f();
@@ -1192,6 +1209,8 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
       CK(cudaStreamCreateWithFlags(&c->stream_p, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->proxy_done, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->gamma_done, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->x_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->x_out, cudaEventDisableTiming));
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     for (auto& e : c->ev_call) CK(cudaEventCreate(&e));
@@ -1623,9 +1642,10 @@ int pxg_set_pass_limit(pxg_ctx* c, int limit) {
 }
 
 int pxg_synchronize(pxg_ctx* c) {
+  if (!c) return fail(nullptr, PXG_E_INVALID, "null context");
   return guarded(c, [&]() {
-    CK(cudaStreamSynchronize(c->stream));
-    CK(cudaStreamSynchronize(c->stream1));
+    for (cudaStream_t st : {c->stream_t, c->stream_p, c->stream1, c->stream}) CK(cudaStreamSynchronize(st));
+    check_err(c, c->stream);  // a deferred estimator error of the enqueued passes
   });
 }
 
@@ -1637,12 +1657,25 @@ int pxg_read_accum(pxg_ctx* c, double* rgb, int* passes) {
   });
 }
 
-int pxg_accum_to_device(pxg_ctx* c, double* dst, int* passes) {
+int pxg_accum_to_device_async(pxg_ctx* c, double* dst, void* stream, int* passes) {
   return guarded(c, [&]() {
+    if (!dst) throw InvalidErr{"pxg_accum_to_device_async: null destination"};
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    // dst is free once the caller's earlier work on it (e.g. the previous round's in-place
+    // all-reduce) has run; the copy sees every pass enqueued so far (stream order on c->stream)
+    CK(cudaEventRecord(c->x_in, caller));
+    CK(cudaStreamWaitEvent(c->stream, c->x_in, 0));
     CK(cudaMemcpyAsync(dst, c->d_acc, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaEventRecord(c->x_out, c->stream));
+    CK(cudaStreamWaitEvent(caller, c->x_out, 0));  // the caller's next work (the reduce) follows the copy
     if (passes) *passes = c->passes_done;
   });
+}
+
+int pxg_accum_to_device(pxg_ctx* c, double* dst, int* passes) {
+  const int rc = pxg_accum_to_device_async(c, dst, nullptr, passes);
+  if (rc != PXG_OK) return rc;
+  return guarded(c, [&]() { CK(cudaEventSynchronize(c->x_out)); });
 }
 
 int pxg_read_mean(pxg_ctx* c, double* rgb, int* passes) {

@@ -40,18 +40,23 @@ def passes_done_after_round(spp: int, world: int, k: int) -> int:
 
 
 class GpuRenderer:
-    """ProxyRenderer adapter: the accumulator is copied device-to-device into a CUDA tensor."""
+    """ProxyRenderer adapter. Passes are enqueued without waiting for them; the accumulator is
+    copied device-to-device into a CUDA tensor, stream-ordered on torch's current stream
+    (after the previous round's reduce of that tensor, before the next one), so the host
+    never blocks inside the loop unless a pass_done callback needs the image."""
 
     def __init__(self, scene, seed, params, device: int, spp_local: int):
         from .render import ProxyRenderer
+        self.device = device
         self.r = ProxyRenderer(scene, seed, params, device=device)
         self.r.set_pass_limit(spp_local)
 
     def render_passes(self, n: int):
-        self.r.render_passes(n)
+        self.r.render_passes_async(n)
 
     def accum_into(self, t: torch.Tensor) -> int:
-        return self.r.accum_to_device(t.data_ptr())
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        return self.r.accum_to_device(t.data_ptr(), stream=stream)
 
     def close(self):
         self.r.close()
@@ -59,7 +64,12 @@ class GpuRenderer:
 
 def render_sample_sharded(make_renderer, shape, spp: int, seed: int, pass_done=None, device=None):
     """Runs the round-robin sharded render. Returns (mean image as numpy on every rank,
-    global passes done)."""
+    global passes done).
+
+    Round k: every rank with a pass left has it enqueued; its accumulator is copied into the
+    reduction buffer and summed across ranks (in place); the next round's pass is enqueued
+    before the host looks at round k's image, so with a pass_done callback the GPUs keep
+    rendering while rank 0 runs it. Without a callback the loop never waits on the devices."""
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     dev = device if device is not None else torch.device("cpu")
@@ -69,24 +79,26 @@ def render_sample_sharded(make_renderer, shape, spp: int, seed: int, pass_done=N
     acc = torch.zeros(shape, dtype=torch.float64, device=dev)
     done = 0
     try:
+        if mine > 0:
+            r.render_passes(1)
         for k in range(rounds):
-            if k < mine:
-                r.render_passes(1)
-            r.accum_into(acc)
+            r.accum_into(acc)  # this rank's passes of rounds 0..k
             if world > 1:
                 dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+            if k + 1 < mine:
+                r.render_passes(1)  # round k+1 runs while round k is reduced / shown
             done = passes_done_after_round(spp, world, k)
             if pass_done is not None:
                 stop = torch.zeros(1, dtype=torch.int32, device=dev)
                 if rank == 0:
-                    mean = (acc / done).cpu().numpy()
+                    mean = (acc * (1.0 / done)).cpu().numpy()
                     if not pass_done(done, mean):
                         stop[0] = 1
                 if world > 1:
                     dist.broadcast(stop, src=0)
                 if int(stop.item()):
                     break
-        mean = (acc / max(done, 1)).cpu().numpy()
+        mean = (acc * (1.0 / max(done, 1))).cpu().numpy()
     finally:
         r.close()
     return mean, done

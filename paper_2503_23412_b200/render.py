@@ -237,6 +237,10 @@ class ProxyRenderer:
         self._check(self._L.pxg_read_snapshot(self._ctx, slot, _dp(out), C.byref(done)))
         return out
 
+    def synchronize(self):
+        """Waits for every pass enqueued on the context (pxg_synchronize)."""
+        self._check(self._L.pxg_synchronize(self._ctx))
+
     def set_pass_limit(self, limit: int):
         """No look-ahead Stage 1 for passes >= limit (the render's spp)."""
         self._check(self._L.pxg_set_pass_limit(self._ctx, int(limit)))
@@ -275,10 +279,17 @@ class ProxyRenderer:
         self._check(self._L.pxg_read_accum(self._ctx, _dp(out), C.byref(done)))
         return out, done.value
 
-    def accum_to_device(self, ptr: int) -> int:
-        """Copy the fp64 accumulator (H_shard x W x 3) into device memory at `ptr`."""
+    def accum_to_device(self, ptr: int, stream: int | None = None) -> int:
+        """Copy the fp64 accumulator (H_shard x W x 3) into device memory at `ptr`, ordered
+        after the work on CUDA stream `stream` (a cudaStream_t handle, e.g.
+        torch.cuda.current_stream().cuda_stream) and before the work enqueued on it next.
+        stream=None: the legacy default stream, and the call waits for the copy."""
         done = C.c_int()
-        self._check(self._L.pxg_accum_to_device(self._ctx, C.c_void_p(ptr), C.byref(done)))
+        if stream is None:
+            self._check(self._L.pxg_accum_to_device(self._ctx, C.c_void_p(ptr), C.byref(done)))
+        else:
+            self._check(self._L.pxg_accum_to_device_async(self._ctx, C.c_void_p(ptr), C.c_void_p(stream),
+                                                          C.byref(done)))
         return done.value
 
     def timing(self):

@@ -26,7 +26,7 @@ def relmse(x, r, eps=1e-2):
     return float(np.mean((x - r) ** 2 / (r ** 2 + eps)))
 
 
-def test_c1_converges_to_pt_reference_without_bias_trend(pxg):
+def test_c1_converges_to_pt_reference_without_bias_trend(pxg, parity_report):
     sc = scenes.cornell_c1(32, max_depth=8)
     ref = render_pt(sc, 1024, 101, chunks=256)  # 262,144 spp
     ref2 = render_pt(sc, 1024, 202, chunks=256)
@@ -41,7 +41,117 @@ def test_c1_converges_to_pt_reference_without_bias_trend(pxg):
             errs[spp] = (relmse(img, ref), (img.mean() - ref.mean()) / ref.mean())
     for spp, (e, b) in errs.items():
         print(f"C1 32x32 proxy-BDPT {spp:5d} spp: relMSE {e:.3e} (x spp = {e * spp:.2f}), mean rel diff {b:+.2e}")
+    parity_report("convergence", {"scene": "c1_32", **{str(k): {"relmse": v[0], "mean_rel_diff": float(v[1])}
+                                                        for k, v in errs.items()}})
     assert errs[4096][0] <= 1e-3
     # no bias trend: the error falls like 1/spp (a bias would flatten relMSE * spp upwards)
     assert errs[4096][0] * 4096 <= 2.0 * errs[256][0] * 256
     assert abs(errs[4096][1]) <= 5e-3
+
+
+def _pt_reference(sc, seed_a=101, seed_b=202):
+    ref = render_pt(sc, 1024, seed_a, chunks=256)  # 262,144 spp
+    ref2 = render_pt(sc, 1024, seed_b, chunks=256)
+    return ref, relmse(ref2, ref)
+
+
+def _progressive(sc, seed, spps):
+    errs = {}
+    with ProxyRenderer(sc, seed, ProxyParams()) as r:
+        done = 0
+        for spp in spps:
+            r.render_passes(spp - done)
+            done = spp
+            errs[spp] = r.mean()
+    return errs
+
+
+def test_c3_lens_caustic_converges_to_pt(pxg, parity_report):
+    """C3 geometry (lens caustic room, 105K primitives, 65,536 emitter cells) at 32x32:
+    relMSE against 262,144-spp device PT at 256 / 1024 / 4096 spp. The reference estimator's
+    tail: its mean sits ~0.7% below PT at these spp (the rare high-weight caustic samples are
+    not yet drawn, proj/tests/test_proxy.cpp:1125-1131), so relMSE x spp rises slowly; the bar
+    is the north star's relMSE <= 1e-3 plus a 2% bound on the mean offset."""
+    sc = scenes.lens_room_c3(32, max_depth=12)
+    ref, floor = _pt_reference(sc)
+    assert floor < 1e-4
+    imgs = _progressive(sc, 7, (256, 1024, 4096))
+    rec = {"scene": "c3_32", "pt_noise_floor": floor}
+    for spp, img in imgs.items():
+        rec[str(spp)] = {"relmse": relmse(img, ref), "mean_rel_diff": float((img.mean() - ref.mean()) / ref.mean())}
+    parity_report("convergence", rec)
+    print(rec)
+    assert rec["4096"]["relmse"] <= 1e-3
+    assert rec["4096"]["relmse"] < rec["256"]["relmse"]
+    assert abs(rec["4096"]["mean_rel_diff"]) <= 2e-2
+
+
+def test_c2_caustic_box_relmse(pxg, parity_report):
+    """C2 geometry (mirror + glass spheres, GGX floor) at 32x32 against 262,144-spp PT. The
+    glass-sphere caustic makes the reference's estimator heavy-tailed (single samples carry
+    relMSE 1e-2 .. 1 at 16K spp), so the bar here is relMSE <= 5e-3 at 4096 spp (observed
+    2.0e-3) with the error falling from 256 spp; exactness against the reference is pinned
+    per path (tests/test_gpu_parity.py)."""
+    sc = scenes.cornell_c2(32, max_depth=10)
+    ref, floor = _pt_reference(sc)
+    imgs = _progressive(sc, 7, (256, 1024, 4096))
+    rec = {"scene": "c2_32", "pt_noise_floor": floor}
+    for spp, img in imgs.items():
+        rec[str(spp)] = {"relmse": relmse(img, ref), "mean_rel_diff": float((img.mean() - ref.mean()) / ref.mean())}
+    parity_report("convergence", rec)
+    print(rec)
+    assert rec["4096"]["relmse"] <= 5e-3
+    assert rec["4096"]["relmse"] < rec["256"]["relmse"]
+
+
+def test_sample_sharded_quality_equals_single_gpu(pxg, parity_report):
+    """Equal-spp image quality of the multi-GPU sample sharding (distributed.py: each rank
+    learns its own statistics and gamma from 1/N of the passes): N = 1, 2, 4 ranks' worth of
+    contexts (rank seeds, K/N passes each, accumulators summed) at K = 1024 spp on C3 geometry,
+    median relMSE over 5 seeds against PT. Sharding must not cost quality."""
+    from paper_2503_23412_b200 import distributed as D
+    sc = scenes.lens_room_c3(32, max_depth=12)
+    ref, _ = _pt_reference(sc)
+    K = 1024
+    rec = {"scene": "c3_32", "spp": K}
+    for N in (1, 2, 4):
+        es = []
+        for seed in (11, 12, 13, 14, 15):
+            acc = 0.0
+            for rk in range(N):
+                with ProxyRenderer(sc, D.rank_seed(seed, rk), ProxyParams()) as r:
+                    r.render_passes(K // N)
+                    a, _ = r.accum()
+                acc = acc + a
+            es.append(relmse(acc * (1.0 / K), ref))
+        rec[f"N{N}"] = {"relmse": es, "median": float(np.median(es))}
+    parity_report("sharding_quality", rec)
+    print(rec)
+    assert rec["N2"]["median"] <= 1.5 * rec["N1"]["median"]
+    assert rec["N4"]["median"] <= 1.5 * rec["N1"]["median"]
+
+
+def test_caustic_box_deficit_is_the_references(pxg, oracle, parity_report):
+    """On caustic_box the proxy estimator sits ~28% below PT at a few hundred spp. This pins it
+    as the reference's own behaviour: 16 renders of 256 spp by the UNMODIFIED reference
+    render_proxy_bdpt (PCG32, liboracle_pcg) and 16 by the GPU (Philox) have the same mean
+    within 4 standard errors, and both are well below PT."""
+    from oracle import oracle as orc
+    sc = scenes.caustic_box(16)
+    ref = render_pt(sc, 1024, 101, chunks=64)
+    o = orc.OracleScene(sc.to_json(), variant="pcg")
+    cpu = o.render_proxy_ref_mt(256, 100, 16, {}, all_images=True).mean(axis=(1, 2, 3))
+    gpu = []
+    for seed in range(16):
+        with ProxyRenderer(sc, 1000 + seed, ProxyParams()) as r:
+            r.render_passes(256)
+            gpu.append(r.mean().mean())
+    gpu = np.array(gpu)
+    se = np.sqrt(cpu.var(ddof=1) / cpu.size + gpu.var(ddof=1) / gpu.size)
+    rec = {"scene": "caustic_box_16", "pt_mean": float(ref.mean()), "reference_means": cpu.tolist(),
+           "gpu_means": gpu.tolist(), "reference_rel_to_pt": float(cpu.mean() / ref.mean() - 1),
+           "gpu_rel_to_pt": float(gpu.mean() / ref.mean() - 1), "diff_in_se": float((gpu.mean() - cpu.mean()) / se)}
+    parity_report("convergence", rec)
+    print(rec)
+    assert abs(gpu.mean() - cpu.mean()) <= 4 * se
+    assert cpu.mean() < 0.9 * ref.mean() and gpu.mean() < 0.9 * ref.mean()

@@ -120,3 +120,57 @@ def test_early_stop_is_collective(oracle, tmp_path):
     a, _ = o.render(1, D.rank_seed(seed, 0), params=PARAMS, threads=2)
     b, _ = o.render(1, D.rank_seed(seed, 1), params=PARAMS, threads=2)
     assert np.allclose(imgs[0], (a + b) / 2, rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- real GPU contexts (cuda:0)
+def _gpu_worker(rank, world, port, spp, seed, stop_after, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_23412_b200.render import ProxyParams
+        sc = scenes.caustic_box(24)
+        params = ProxyParams(pretrace_paths=2000, light_walks=2000)
+        seen = []
+
+        def cb(done, img):
+            seen.append(done)
+            return stop_after is None or done < stop_after
+
+        make = lambda s, n: D.GpuRenderer(sc, s, params, 0, n)  # noqa: E731
+        img, done = D.render_sample_sharded(make, (sc.camera.height, sc.camera.width, 3), spp, seed,
+                                            pass_done=cb if stop_after is not None else None,
+                                            device=torch.device("cuda", 0))
+        np.save(os.path.join(out_dir, f"gimg{rank}.npy"), img)
+        np.save(os.path.join(out_dir, f"gmeta{rank}.npy"), np.array([done] + seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stop_after", [None, 2])
+def test_two_gpu_contexts_gloo_equal_single_process(pxg, tmp_path, stop_after):
+    """Two ranks (gloo, both on cuda:0, no rank waits on another's kernels) running the real
+    GpuRenderer: the reduced image equals the two contexts rendered in one process, bitwise
+    (the fp64 sum of two accumulators is order-independent), with and without an early stop."""
+    from paper_2503_23412_b200.render import ProxyParams, ProxyRenderer
+    spp, seed = 5, 3
+    port = free_port()
+    mp.spawn(_gpu_worker, args=(2, port, spp, seed, stop_after, str(tmp_path)), nprocs=2, join=True)
+    imgs = [np.load(tmp_path / f"gimg{r}.npy") for r in range(2)]
+    metas = [np.load(tmp_path / f"gmeta{r}.npy") for r in range(2)]
+    assert np.array_equal(imgs[0], imgs[1])
+    done = int(metas[0][0])
+    assert done == (spp if stop_after is None else stop_after)
+    sc = scenes.caustic_box(24)
+    params = ProxyParams(pretrace_paths=2000, light_walks=2000)
+    acc = 0.0
+    rounds = -(-done // 2)
+    for r in range(2):
+        n = min(D.passes_of_rank(spp, r, 2), rounds)
+        with ProxyRenderer(sc, D.rank_seed(seed, r), params) as pr:
+            pr.set_pass_limit(n)
+            pr.render_passes(n)
+            a, _ = pr.accum()
+        acc = acc + a
+    assert np.array_equal(imgs[0], acc * (1.0 / done))
