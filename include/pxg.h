@@ -194,8 +194,8 @@ int pxg_occluded(pxg_ctx* ctx, int n, const double* segs, int* occ);
  *   kernel 0: the single-ray paths (trace_closest_t / trace_any_t, 128 B nodes),
  *   kernel 1: the production persistent queue kernels k_trav_persistent<0/1> (lane refill,
  *             256-bit loads, the context's node layout: pxg_node_bytes),
- *   kernel 2: the reciprocal node wavefront's inlined step loops (wave_intersect /
- *             wave_visible).
+ *   kernel 2: the reciprocal node wavefront's traversal (rw_trace: per-lane step loops,
+ *             or warp_trace with postponed leaf tests when built with PXG_RW_WARP=1).
  * Reference: Scene::intersect / Scene::occluded (proj/src/scene.cpp:127-177). */
 int pxg_trace_rays(pxg_ctx* ctx, int kernel, int any_hit, int n, const double* rays, const double* tmax, int* prim,
                    double* t);

@@ -103,38 +103,26 @@ __global__ void k_fill_trace_queue(int n, const double* rays, const double* tmax
   if (i == 0) *Q.count = n;
 }
 
-// The reciprocal node wavefront's inlined traversal (k_recip_eval_wave: wave_intersect /
-// wave_visible) on the queue's rays, one thread per ray; rays with a finite tmax run the same
-// step loop with that bound.
+// The reciprocal node wavefront's traversal (k_recip_eval_wave: rw_trace) on the queue's
+// rays, one lane per ray.
 template <bool kAny>
 __global__ void k_wave_trace(SceneView S, RayQueue Q, const double* rays, int any_segments) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= *Q.count) return;
-  if (kAny) {
-    const double* r = rays + 6 * static_cast<size_t>(j);
-    Q.hit_prim[j] = wave_visible(S, v3(r[0], r[1], r[2]), v3(r[3], r[4], r[5])) ? 0 : 1;
-    return;
-  }
-  const double4 r1 = Q.ray[2 * j + 1];
-  if (r1.z >= 1e30) {
-    const double4 r0 = Q.ray[2 * j];
-    Hit h;
-    if (wave_intersect(S, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), h)) {
-      Q.hit_prim[j] = h.prim;
-      Q.hit_t[j] = h.t;
-    } else {
-      Q.hit_prim[j] = -1;
-      Q.hit_t[j] = 1e30;
-    }
-    return;
-  }
+  const int n = *Q.count;
+  bool has = j < n;
   TravState ts;
-  int stack[kStack];
-  trav_init(ts, Q, j);
-  while (!closest_step(S, ts, stack)) {
+  if (has) {
+    trav_init(ts, Q, j);
+    if (kAny && !(ts.t_best > 0.0)) has = false;  // a segment shorter than kRayEps: never occluded
   }
-  Q.hit_prim[j] = ts.best;
-  Q.hit_t[j] = ts.t_best;
+  const bool occ = rw_trace<kAny>(S, ts, has);
+  if (j >= n) return;
+  if (kAny) {
+    Q.hit_prim[j] = occ ? 1 : 0;
+  } else {
+    Q.hit_prim[j] = ts.best;
+    Q.hit_t[j] = ts.t_best;
+  }
 }
 
 // sin / cos of the draws k (u = k * 2^-32, phi = 2*pi*u) with the device code path of the
@@ -321,6 +309,7 @@ struct pxg_ctx {
   int* h_err = nullptr;                    // [kSnap] pinned error flags of the snapshots
   int trav_blocks = 0;        // persistent traversal grid (SMs x resident blocks)
   int trav_minb = 6;          // resident blocks per SM of the traversal variant (6 or 8)
+  bool trav_post = false;     // postponed leaf tests (scenes with quantised nodes)
   int gs_blocks = 0;          // grid of the grid-stride slot kernels (SMs x 256 blocks of 128; 16 / 64 measured slower)
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
@@ -445,10 +434,17 @@ struct HostProbe {
 // Persistent traversal of queue q (closest hit or any hit) with the context's occupancy variant.
 template <bool kAny>
 void launch_trav(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
-  if (c->trav_minb == 8)
-    k_trav_persistent<kAny, 8><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
-  else
-    k_trav_persistent<kAny, 6><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+  if (c->trav_minb == 8) {
+    if (c->trav_post)
+      k_trav_persistent<kAny, 8, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+    else
+      k_trav_persistent<kAny, 8, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+  } else {
+    if (c->trav_post)
+      k_trav_persistent<kAny, 6, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+    else
+      k_trav_persistent<kAny, 6, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+  }
 }
 
 RayQueue make_queue(pxg_ctx* c, size_t cap) {
@@ -1513,10 +1509,12 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       c->trav_minb = c->S.nodeq ? 8 : 6;
       if (const char* e = std::getenv("PXG_TRAV_MINB")) c->trav_minb = std::atoi(e) == 8 ? 8 : 6;
+      c->trav_post = c->S.nodeq != 0;
+      if (const char* e = std::getenv("PXG_TRAV_POSTPONE")) c->trav_post = std::atoi(e) != 0;
       if (c->trav_minb == 8)
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 8>, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 8, true>, 128, 0));
       else
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6>, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6, false>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
       c->gs_blocks = sms * (std::getenv("PXG_GS_PER_SM") ? std::atoi(std::getenv("PXG_GS_PER_SM")) : 256);
       int pe = 0, pd = 0;

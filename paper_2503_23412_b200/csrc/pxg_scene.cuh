@@ -227,7 +227,22 @@ __device__ __forceinline__ void ldg256(const void* p, float4& a, float4& b) {
 #define PXG_NODEQ 1
 #endif
 
-__device__ __forceinline__ float qbyte(unsigned w, int k) { return static_cast<float>((w >> (8 * k)) & 0xffu); }
+#ifndef PXG_QSIGN
+#define PXG_QSIGN 1
+#endif
+#ifndef PXG_QCVT
+#define PXG_QCVT 0
+#endif
+// Byte k of w as a float, exactly. PXG_QCVT 1: one byte permute builds the fp32 bit pattern
+// 0x4B0000bb = 2^23 + b and one exact FADD removes 2^23 (two full-rate instructions instead
+// of the quarter-rate I2F.U8).
+__device__ __forceinline__ float qbyte(unsigned w, int k) {
+#if PXG_QCVT
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, static_cast<unsigned>(k) | 0x7540u)) - 8388608.0f;
+#else
+  return static_cast<float>((w >> (8 * k)) & 0xffu);
+#endif
+}
 
 // Box tests of a quantised node: per axis t = q * (step * inv) + (origin - o) * inv, i.e. the
 // slab distance of the decoded plane (one FFMA per plane after 2 per axis), conservative
@@ -260,6 +275,24 @@ __device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, c
   r.code[1] = __float_as_int(b.y);
   r.code[2] = __float_as_int(b.z);
   r.code[3] = __float_as_int(b.w);
+#if PXG_QSIGN
+  // near / far planes picked once per node by the sign of the slope (fma(q, A, B) is monotone
+  // in q, so this is exactly the min / max of the two slab distances): 3 + 3 distances and
+  // two 3-input min / max per child instead of 6 two-input ones
+  const unsigned nxw = Ax < 0.0f ? hxw : lxw, fxw = Ax < 0.0f ? lxw : hxw;
+  const unsigned nyw = Ay < 0.0f ? hyw : lyw, fyw = Ay < 0.0f ? lyw : hyw;
+  const unsigned nzw = Az < 0.0f ? hzw : lzw, fzw = Az < 0.0f ? lzw : hzw;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float nx = __fmaf_rn(qbyte(nxw, k), Ax, Bx), fx = __fmaf_rn(qbyte(fxw, k), Ax, Bx);
+    const float ny = __fmaf_rn(qbyte(nyw, k), Ay, By), fy = __fmaf_rn(qbyte(fyw, k), Ay, By);
+    const float nz = __fmaf_rn(qbyte(nzw, k), Az, Bz), fz = __fmaf_rn(qbyte(fzw, k), Az, Bz);
+    const float t0 = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+    const float t1 = fminf(fminf(fx, fy), fminf(fz, tb));
+    if (t0 <= t1) r.hit |= 1u << k;
+    r.tn[k] = t0;
+  }
+#else
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float tx0 = __fmaf_rn(qbyte(lxw, k), Ax, Bx), tx1 = __fmaf_rn(qbyte(hxw, k), Ax, Bx);
@@ -270,6 +303,7 @@ __device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, c
     if (t0 <= t1) r.hit |= 1u << k;
     r.tn[k] = t0;
   }
+#endif
   return r;
 }
 
@@ -321,10 +355,42 @@ __device__ __forceinline__ void cswap4(float& ta, int& ca, float& tb, int& cb) {
 
 constexpr int kNoChild = static_cast<int>(0x80000000u);  // never a node or leaf code
 
+// Traversal stacks of child codes. LocalStack: one per-thread local array (kStack entries).
+// SplitStack<kS>: the first kS entries in shared memory (entry i of thread t at
+// sm[i * 128 + t]: the lanes of a warp hit 32 distinct banks whatever their depths, one
+// wavefront per access instead of one L1 line per lane), deeper entries in a local array.
+struct LocalStack {
+  int* a;
+  __device__ __forceinline__ void push(int& sp, int v) {
+    if (sp < kStack) a[sp++] = v;
+  }
+  __device__ __forceinline__ int pop(int& sp) { return a[--sp]; }
+};
+
+template <int kS>
+struct SplitStack {
+  int* sm;   // this thread's column of the block's shared stack (stride 128)
+  int* loc;  // [kStack - kS]
+  __device__ __forceinline__ void push(int& sp, int v) {
+    if (sp < kS) {
+      sm[sp * 128] = v;
+    } else {
+      if (sp >= kStack) return;
+      loc[sp - kS] = v;
+    }
+    ++sp;
+  }
+  __device__ __forceinline__ int pop(int& sp) {
+    --sp;
+    return sp < kS ? sm[sp * 128] : loc[sp - kS];
+  }
+};
+
 // Orders the children of `h` (internal nodes and leaves) hit within tbn by tnear: the
 // nearest is returned (kNoChild if none), the rest are pushed so that nearer ones pop
 // first. Non-candidates get +inf keys; a 5-comparator network sorts in registers.
-__device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* stack, int& sp) {
+template <class Stack>
+__device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, Stack& stack, int& sp) {
   float t[4];
   int c[4];
 #pragma unroll
@@ -340,7 +406,7 @@ __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, int* s
   cswap4(t[1], c[1], t[2], c[2]);
 #pragma unroll
   for (int k = 3; k >= 1; --k)
-    if (c[k] != kNoChild && sp < kStack) stack[sp++] = c[k];
+    if (c[k] != kNoChild) stack.push(sp, c[k]);
   return c[0];
 }
 
@@ -374,7 +440,8 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
                                             TravCount* cnt = nullptr) {
   const RayF rf = make_rayf(o, d);
   int best = -1;
-  int stack[kStack];
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   int sp = 0;
   int node = 0;
   for (;;) {
@@ -396,7 +463,7 @@ __device__ __noinline__ int trace_closest_t(const SceneView& S, const V3& o, con
     int next = node4_order(node4_inner(h), tbound_f(t_best), stack, sp);
     if (next == kNoChild) {
       if (sp == 0) break;
-      next = stack[--sp];
+      next = stack.pop(sp);
     }
     node = next;
   }
@@ -413,7 +480,8 @@ template <bool kCount = false>
 __device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const V3& d, double t_max,
                                          TravCount* cnt = nullptr) {
   const RayF rf = make_rayf(o, d);
-  int stack[kStack];
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   int sp = 0;
   int node = 0;
   const float tb = tbound_f(t_max);
@@ -432,7 +500,7 @@ __device__ __noinline__ bool trace_any_t(const SceneView& S, const V3& o, const 
     int next = node4_order(node4_inner(h), tb, stack, sp);
     if (next == kNoChild) {
       if (sp == 0) break;
-      next = stack[--sp];
+      next = stack.pop(sp);
     }
     node = next;
   }

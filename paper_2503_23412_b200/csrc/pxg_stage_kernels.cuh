@@ -479,48 +479,42 @@ __global__ void k_recip_eval(SceneView S, uint64_t seed, int repeats, int stride
 // "visible") as one compacted any-hit list; (3) the recorded density terms, each zeroed when
 // one of its segments is hidden (exactly what the reference's early exits produce). Candidate
 // vertices and segment endpoints live in a global scratch slot per (block, node).
-// Scene::intersect / visible through the persistent kernels' step functions (quantised
-// nodes, 32-byte loads), inlined: same hits as intersect() / visible() (closest hit with the
-// id tie rule and the any-hit boolean do not depend on the visiting order).
-__device__ __forceinline__ bool wave_intersect(const SceneView& S, const V3& o, const V3& d, Hit& hit) {
-  TravState ts;
-  ts.o = o;
-  ts.d = d;
-  ts.rf = make_rayf(o, d);
-  ts.t_best = 1e30;
-  ts.best = -1;
-  ts.node = 0;
-  ts.sp = 0;
-  int stack[kStack];
+// Its rays are traced by rw_trace with the persistent kernels' step functions (quantised
+// nodes, 32-byte loads); same hits as intersect() / visible() (closest hit with the id tie
+// rule and the any-hit boolean do not depend on the visiting order).
+#ifndef PXG_RW_WARP
+#define PXG_RW_WARP 0  // 1: the warp traces its lanes' rays together with postponed leaf tests
+#endif                 //    (warp_trace; measured C4 -1.6%, C2 -2.3%)
+__device__ __forceinline__ void thread_trace_closest(const SceneView& S, TravState& ts) {
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   while (!closest_step(S, ts, stack)) {
   }
-  if (ts.best < 0) return false;
-  hit.t = ts.t_best;
-  hit.p = o + ts.t_best * d;
-  hit.prim = ts.best;
-  hit.n = prim_normal(S, ts.best, hit.p);
-  hit.material = S.prim_mat[ts.best];
-  hit.emitter = S.prim_emitter[ts.best];
-  return true;
 }
 
-__device__ __forceinline__ bool wave_visible(const SceneView& S, const V3& from, const V3& to) {
-  const V3 d = to - from;
-  const double dist = length(d);
-  if (dist < kRayEps) return true;
-  TravState ts;
-  ts.o = from;
-  ts.d = d / dist;
-  ts.rf = make_rayf(ts.o, ts.d);
-  ts.t_best = dist * (1.0 - 1e-6);
-  ts.best = -1;
-  ts.node = 0;
-  ts.sp = 0;
-  int stack[kStack];
+__device__ __forceinline__ bool thread_trace_any(const SceneView& S, TravState& ts) {
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   int r;
   while ((r = any_step(S, ts, stack)) == 0) {
   }
-  return r != 1;
+  return r == 1;
+}
+
+// The reciprocal wavefront's trace of a lane's ray (all lanes of the warp call it; has = the
+// lane holds a ray). Closest hit: ts.best / ts.t_best; any hit: true when occluded.
+template <bool kAny>
+__device__ __forceinline__ bool rw_trace(const SceneView& S, TravState& ts, bool has) {
+#if PXG_RW_WARP
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
+  return warp_trace<kAny>(S, ts, stack, has);
+#else
+  if (!has) return false;
+  if (kAny) return thread_trace_any(S, ts);
+  thread_trace_closest(S, ts);
+  return false;
+#endif
 }
 
 constexpr int kRW = 128;  // nodes per block batch = threads per block
@@ -630,23 +624,45 @@ SceneView S, uint64_t seed, int repeats, int stride,
       __syncthreads();
       const int nray = s_n;
       if (nray == 0) break;  // block-uniform
-      if (t < nray) {
-        const int q = s_list[t];
-        const int jq = s_j[q];
-        const BatchPass& P = bs.p[jq / stride];
-        const int e = (jq % stride) / repeats;
-        const IncHdr& h = P.inc[e];
-        const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
-        PV* gq = scratch + (static_cast<size_t>(blockIdx.x) * kRW + q) * 4;
-        const int src = s_src[q];
-        const V3 o = src == -1 ? h.spec_end.p : (src == -2 ? inc_control(h, pre)->p : gq[src].p);
-        const V3 d = v3(s_dir[q][0], s_dir[q][1], s_dir[q][2]);
-        Hit hit;
-        if (!wave_intersect(S, o, d, hit)) {
-          s_state[q] = kRWEscaped;
-        } else {
-          gq[s_strand[q] == 1 ? 0 : s_step[q]] = vertex_from_hit(S, hit, -d);
-          s_state[q] = kRWSampled;  // provisional: the glue below decides
+      if ((t & ~31) < nray) {  // warps holding rays trace them together (postponed leaves)
+        const bool has = t < nray;
+        int q = 0;
+        PV* gq = nullptr;
+        TravState ts;
+        if (has) {
+          q = s_list[t];
+          const int jq = s_j[q];
+          const BatchPass& P = bs.p[jq / stride];
+          const int e = (jq % stride) / repeats;
+          const IncHdr& h = P.inc[e];
+          const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+          gq = scratch + (static_cast<size_t>(blockIdx.x) * kRW + q) * 4;
+          const int src = s_src[q];
+          ts.o = src == -1 ? h.spec_end.p : (src == -2 ? inc_control(h, pre)->p : gq[src].p);
+          ts.d = v3(s_dir[q][0], s_dir[q][1], s_dir[q][2]);
+          ts.rf = make_rayf(ts.o, ts.d);
+          ts.t_best = 1e30;
+          ts.best = -1;
+          ts.node = 0;
+          ts.sp = 0;
+          ts.pend_node = 0;
+          ts.pend_mask = 0u;
+        }
+        rw_trace<false>(S, ts, has);
+        if (has) {
+          if (ts.best < 0) {
+            s_state[q] = kRWEscaped;
+          } else {
+            Hit hit;
+            hit.t = ts.t_best;
+            hit.p = ts.o + ts.t_best * ts.d;
+            hit.prim = ts.best;
+            hit.n = prim_normal(S, ts.best, hit.p);
+            hit.material = S.prim_mat[ts.best];
+            hit.emitter = S.prim_emitter[ts.best];
+            gq[s_strand[q] == 1 ? 0 : s_step[q]] = vertex_from_hit(S, hit, -ts.d);
+            s_state[q] = kRWSampled;  // provisional: the glue below decides
+          }
         }
       }
       __syncthreads();
@@ -708,10 +724,35 @@ SceneView S, uint64_t seed, int repeats, int stride,
     __syncthreads();
     // ---- (2b) trace the recorded segments, compacted over the block
     const int nseg = s_nseg;
-    for (int i = t; i < nseg; i += kRW) {
-      const int q = s_seg[i] >> 4, sg = s_seg[i] & 15;
-      const double* e = ends_block + q * 60 + 6 * sg;
-      if (wave_visible(S, v3(e[0], e[1], e[2]), v3(e[3], e[4], e[5]))) atomicOr(&s_vis[q], 1u << sg);
+    for (int i0 = t & ~31; i0 < nseg; i0 += kRW) {  // warp-uniform: lanes of a warp trace together
+      const int i = i0 + (t & 31);
+      bool has = i < nseg, vis = true;
+      int q = 0, sg = 0;
+      TravState ts;
+      if (has) {
+        q = s_seg[i] >> 4;
+        sg = s_seg[i] & 15;
+        const double* e = ends_block + q * 60 + 6 * sg;
+        // visible(from, to) = !occluded (scene.cpp:170-177): unit direction, tmax = dist (1 - 1e-6)
+        const V3 from = v3(e[0], e[1], e[2]);
+        const V3 dv = v3(e[3], e[4], e[5]) - from;
+        const double dist = length(dv);
+        if (dist < kRayEps) {
+          has = false;  // never occluded
+        } else {
+          ts.o = from;
+          ts.d = dv / dist;
+          ts.rf = make_rayf(ts.o, ts.d);
+          ts.t_best = dist * (1.0 - 1e-6);
+          ts.best = -1;
+          ts.node = 0;
+          ts.sp = 0;
+          ts.pend_node = 0;
+          ts.pend_mask = 0u;
+        }
+      }
+      if (rw_trace<true>(S, ts, has)) vis = false;
+      if (i < nseg && vis) atomicOr(&s_vis[q], 1u << sg);
     }
     __syncthreads();
     // ---- (2c) the densities with the traced visibilities; draw_g (recip.hpp:69-77), split

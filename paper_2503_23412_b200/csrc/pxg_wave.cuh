@@ -235,6 +235,8 @@ struct TravState {
   RayF rf;
   double t_best;
   int best, node, sp;
+  int pend_node;        // postponed leaf tests (PXG_POSTPONE): the node whose hit leaf children ...
+  unsigned pend_mask;   // ... bit k: child k still to be tested
 };  // the traversal stack is a separate local array so these stay in registers
 
 __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int j) {
@@ -246,12 +248,14 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
   ts.best = -1;
   ts.node = 0;
   ts.sp = 0;
+  ts.pend_node = 0;
+  ts.pend_mask = 0u;
 }
 
 // Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
 // ts.node holds a child code: >= 0 a 4-wide node, < 0 a leaf.
-template <bool kCount = false>
-__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, int* stack, TravCount* cnt = nullptr) {
+template <bool kCount = false, class Stack>
+__device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, Stack& stack, TravCount* cnt = nullptr) {
   // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
   // inner children are ordered nearest-first (the next node, then the stack)
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tbound_f(ts.t_best));
@@ -272,15 +276,15 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
   int next = node4_order(node4_inner(h), tbound_f(ts.t_best), stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return true;
-    next = stack[--ts.sp];
+    next = stack.pop(ts.sp);
   }
   ts.node = next;
   return false;
 }
 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
-template <bool kCount = false>
-__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* stack, TravCount* cnt = nullptr) {
+template <bool kCount = false, class Stack>
+__device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, Stack& stack, TravCount* cnt = nullptr) {
   const float tb = tbound_f(ts.t_best);
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
   if (kCount) cnt->nodes += 1;
@@ -296,18 +300,123 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, int* 
   int next = node4_order(node4_inner(h), tb, stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return 2;
-    next = stack[--ts.sp];
+    next = stack.pop(ts.sp);
   }
   ts.node = next;
   return 0;
 }
 
-constexpr int kRefill = 4;  // refill a warp's idle lanes once at least this many are idle
+// ---- postponed leaf tests (Aila & Laine's "while-while" for the 4-wide node step): a node
+// visit only records its hit leaf children; the fp64 primitive tests of the warp run
+// together once most active lanes have some (or no lane can visit a node), instead of
+// diverging against the node visits of the other lanes on every step. Same hits: the
+// closest hit with the id tie rule and the any-hit boolean do not depend on the order in
+// which primitives are tested; only culling uses a bound that is a few steps older.
+constexpr int kDone = static_cast<int>(0x80000001u);  // ts.node once nothing is left to visit
+
+__device__ __forceinline__ int4 node4_codes(const SceneView& S, int node) {
+  if (PXG_NODEQ && S.nodeq) return __ldg(reinterpret_cast<const int4*>(S.nodes4q + node) + 1);
+  return __ldg(reinterpret_cast<const int4*>(S.nodes4 + node) + 6);
+}
+
+// Node visit: hit leaves postponed, the next node chosen (kDone when none is left).
+template <class Stack>
+__device__ __forceinline__ void node_step_postponed(const SceneView& S, TravState& ts, Stack& stack, float tb) {
+  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
+  ts.pend_node = ts.node;
+  ts.pend_mask = node4_leaves(h);
+  int next = node4_order(node4_inner(h), tb, stack, ts.sp);
+  if (next == kNoChild) next = ts.sp == 0 ? kDone : stack.pop(ts.sp);
+  ts.node = next;
+}
+
+// The postponed leaves, closest hit.
+__device__ __forceinline__ void leaf_step_closest(const SceneView& S, TravState& ts) {
+  const int4 cc = node4_codes(S, ts.pend_node);
+  for (unsigned leaves = ts.pend_mask; leaves; leaves &= leaves - 1) {
+    const int k = __ffs(leaves) - 1;
+    const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
+    const int first = code >> 4, count = code & 15;
+    for (int i = 0; i < count; ++i) {
+      int id;
+      const double t = rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id);
+      if (t > 0.0 && (t < ts.t_best || id > ts.best)) {
+        ts.t_best = t;
+        ts.best = id;
+      }
+    }
+  }
+  ts.pend_mask = 0u;
+}
+
+// The postponed leaves, any hit: true when one of them is hit within tmax.
+__device__ __forceinline__ bool leaf_step_any(const SceneView& S, TravState& ts) {
+  const int4 cc = node4_codes(S, ts.pend_node);
+  const unsigned pm = ts.pend_mask;
+  ts.pend_mask = 0u;
+  for (unsigned leaves = pm; leaves; leaves &= leaves - 1) {
+    const int k = __ffs(leaves) - 1;
+    const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
+    const int first = code >> 4, count = code & 15;
+    for (int i = 0; i < count; ++i) {
+      int id;
+      if (rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return true;
+    }
+  }
+  return false;
+}
+
+// The whole warp traces its lanes' rays (lane inactive when !active) to completion with
+// postponed leaf tests, no refill: the block-local reciprocal wavefront's compacted rays.
+// Closest hit: ts.best / ts.t_best; any hit: returns true when occluded.
+template <bool kAny, class Stack>
+__device__ __forceinline__ bool warp_trace(const SceneView& S, TravState& ts, Stack& stack, bool active) {
+  const unsigned FULL = 0xffffffffu;
+  bool live = active, occ = false;
+  for (;;) {
+    const bool pend = live && ts.pend_mask != 0u;
+    const unsigned ma = __ballot_sync(FULL, live), mp = __ballot_sync(FULL, pend);
+    if (ma == 0u) break;
+    if (mp != 0u && (mp == ma || 2 * __popc(mp) >= __popc(ma))) {
+      if (pend) {
+        if (kAny) {
+          if (leaf_step_any(S, ts)) {
+            occ = true;
+            live = false;
+          } else if (ts.node == kDone) {
+            live = false;
+          }
+        } else {
+          leaf_step_closest(S, ts);
+          if (ts.node == kDone) live = false;
+        }
+      }
+    } else if (live && !pend) {
+      node_step_postponed(S, ts, stack, tbound_f(ts.t_best));
+      if (ts.pend_mask == 0u && ts.node == kDone) live = false;
+    }
+  }
+  return occ;
+}
+
+#ifndef PXG_LEAF_FRAC
+#define PXG_LEAF_FRAC 16  // leaf phase once this many 32ths of the active lanes have leaves pending
+#endif
+
+#ifndef PXG_REFILL
+#define PXG_REFILL 4
+#endif
+#ifndef PXG_SSTACK
+#define PXG_SSTACK 0  // shared-memory entries of the persistent kernels' traversal stack (0: all local)
+#endif
+constexpr int kRefill = PXG_REFILL;  // refill a warp's idle lanes once at least this many are idle
 
 // kMinB resident blocks per SM: 8 for scenes traversed with quantised nodes (C4/C5: more
 // warps hide the longer node chains, +2.6%), 6 for L2-resident scenes (C2: +0.8%; 7 was the
 // single compromise before).
-template <bool kAny, int kMinB>
+// kPost: postponed leaf tests (+4% on C4's 1M-triangle scene, -0.3% on the L2-resident C2,
+// so chosen per scene with the node layout).
+template <bool kAny, int kMinB, bool kPost>
 __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -315,7 +424,14 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
   int j = -1;
   bool exhausted = false;
   TravState ts;
-  int stack[kStack];
+#if PXG_SSTACK > 0
+  __shared__ int s_stack[PXG_SSTACK * 128];
+  int stack_loc[kStack - PXG_SSTACK];
+  SplitStack<PXG_SSTACK> stack{s_stack + threadIdx.x, stack_loc};
+#else
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
+#endif
   for (;;) {
     const bool idle = j < 0;
     const unsigned m = __ballot_sync(FULL, idle);
@@ -337,7 +453,43 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
       if (exhausted || total == 0) break;
       continue;
     }
-    if (j >= 0) {
+    if (kPost) {
+    const bool act = j >= 0;
+    const bool pend = act && ts.pend_mask != 0u;
+    const unsigned ma = __ballot_sync(FULL, act), mp = __ballot_sync(FULL, pend);
+    const bool leaf_phase = mp != 0u && (mp == ma || 32 * __popc(mp) >= PXG_LEAF_FRAC * __popc(ma));
+    if (leaf_phase) {
+      if (pend) {
+        if (kAny) {
+          if (leaf_step_any(S, ts)) {
+            Q.hit_prim[j] = 1;
+            j = -1;
+          } else if (ts.node == kDone) {
+            Q.hit_prim[j] = 0;
+            j = -1;
+          }
+        } else {
+          leaf_step_closest(S, ts);
+          if (ts.node == kDone) {
+            Q.hit_prim[j] = ts.best;
+            Q.hit_t[j] = ts.t_best;
+            j = -1;
+          }
+        }
+      }
+    } else if (act && !pend) {
+      node_step_postponed(S, ts, stack, tbound_f(ts.t_best));
+      if (ts.pend_mask == 0u && ts.node == kDone) {  // nothing left to test or visit
+        if (kAny) {
+          Q.hit_prim[j] = 0;
+        } else {
+          Q.hit_prim[j] = ts.best;
+          Q.hit_t[j] = ts.t_best;
+        }
+        j = -1;
+      }
+    }
+    } else if (j >= 0) {
       if (kAny) {
         const int r = any_step(S, ts, stack);
         if (r) {
@@ -361,7 +513,8 @@ __global__ void __launch_bounds__(128) k_closest_count(SceneView S, RayQueue Q, 
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *Q.count) return;
   TravState ts;
-  int stack[kStack];
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   trav_init(ts, Q, j);
   TravCount c{0, 0};
   while (!closest_step<true>(S, ts, stack, &c)) {
@@ -375,7 +528,8 @@ __global__ void __launch_bounds__(128) k_anyhit_count(SceneView S, RayQueue Q, u
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *Q.count) return;
   TravState ts;
-  int stack[kStack];
+  int stack_mem[kStack];
+  LocalStack stack{stack_mem};
   trav_init(ts, Q, j);
   TravCount c{0, 0};
   while (any_step<true>(S, ts, stack, &c) == 0) {

@@ -132,10 +132,14 @@ def test_sample_sharded_quality_equals_single_gpu(pxg, parity_report):
 
 
 def test_caustic_box_deficit_is_the_references(pxg, oracle, parity_report):
-    """On caustic_box the proxy estimator sits ~28% below PT at a few hundred spp. This pins it
-    as the reference's own behaviour: 16 renders of 256 spp by the UNMODIFIED reference
-    render_proxy_bdpt (PCG32, liboracle_pcg) and 16 by the GPU (Philox) have the same mean
-    within 4 standard errors, and both are well below PT."""
+    """On caustic_box the proxy estimator's typical render sits ~28% below PT at a few hundred
+    spp, and rare single samples push a render far above PT (a heavy tail: the mean over
+    renders is not a stable statistic at this size). This pins the shape as the reference's
+    own: 16 renders of 256 spp by the UNMODIFIED reference render_proxy_bdpt (PCG32,
+    liboracle_pcg) and 16 by the GPU (Philox) are one distribution (Mann-Whitney U, p > 0.01;
+    medians within 10%), and both medians are well below PT."""
+    from scipy.stats import mannwhitneyu
+
     from oracle import oracle as orc
     sc = scenes.caustic_box(16)
     ref = render_pt(sc, 1024, 101, chunks=64)
@@ -147,11 +151,12 @@ def test_caustic_box_deficit_is_the_references(pxg, oracle, parity_report):
             r.render_passes(256)
             gpu.append(r.mean().mean())
     gpu = np.array(gpu)
-    se = np.sqrt(cpu.var(ddof=1) / cpu.size + gpu.var(ddof=1) / gpu.size)
-    rec = {"scene": "caustic_box_16", "pt_mean": float(ref.mean()), "reference_means": cpu.tolist(),
-           "gpu_means": gpu.tolist(), "reference_rel_to_pt": float(cpu.mean() / ref.mean() - 1),
-           "gpu_rel_to_pt": float(gpu.mean() / ref.mean() - 1), "diff_in_se": float((gpu.mean() - cpu.mean()) / se)}
+    p = float(mannwhitneyu(cpu, gpu).pvalue)
+    rec = {"scene": "caustic_box_16", "spp": 256, "pt_mean": float(ref.mean()), "reference_means": cpu.tolist(),
+           "gpu_means": gpu.tolist(), "reference_median_rel_to_pt": float(np.median(cpu) / ref.mean() - 1),
+           "gpu_median_rel_to_pt": float(np.median(gpu) / ref.mean() - 1), "mann_whitney_p": p}
     parity_report("convergence", rec)
     print(rec)
-    assert abs(gpu.mean() - cpu.mean()) <= 4 * se
-    assert cpu.mean() < 0.9 * ref.mean() and gpu.mean() < 0.9 * ref.mean()
+    assert p > 0.01
+    assert abs(np.median(gpu) / np.median(cpu) - 1) <= 0.1
+    assert np.median(cpu) < 0.85 * ref.mean() and np.median(gpu) < 0.85 * ref.mean()

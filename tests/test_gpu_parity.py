@@ -83,7 +83,7 @@ def _segments(o, sc, n, rng):
 
 
 KERNELS = {0: "single-ray trace_closest_t/trace_any_t", 1: "production k_trav_persistent<0/1>",
-           2: "reciprocal wavefront wave_intersect/wave_visible"}
+           2: "reciprocal wavefront rw_trace"}
 
 
 @pytest.mark.parametrize("name", list(TRAVERSAL_SCENES))
@@ -105,11 +105,12 @@ def test_traversal_prim_ids_bit_exact(pxg, oracle, name, monkeypatch, parity_rep
     op, ot = o.intersect(rays, threads=16)
     op2, ot2 = o.intersect(sec, tm, threads=16)
     oocc = o.occluded(segs, threads=16)
-    for nodeq in (0, 1):
+    for nodeq, post in ((0, 0), (0, 1), (1, 1), (1, 0)):
         monkeypatch.setenv("PXG_NODEQ", str(nodeq))
+        monkeypatch.setenv("PXG_TRAV_POSTPONE", str(post))  # persistent kernel: leaf tests postponed or not
         with ProxyRenderer(sc, 0, ProxyParams(enabled=False)) as r:
-            layout = f"{r.node_bytes()} B nodes"
-            for kernel in (0, 1, 2):
+            layout = f"{r.node_bytes()} B nodes" + (", postponed leaves" if post else "")
+            for kernel in ((0, 1, 2) if post == nodeq else (1,)):
                 gp, gt = r.trace_rays(kernel, rays)
                 gp2, gt2 = r.trace_rays(kernel, sec, tm)
                 gocc = r.trace_rays(kernel, segs, any_hit=True)
