@@ -142,7 +142,7 @@ int pxg_read_snapshot(pxg_ctx* ctx, int slot, double* rgb, int* passes_done);
 int pxg_measure_traversal(pxg_ctx* ctx, int n, double* out);
 /* Bytes of one BVH node visit of this context's persistent traversal kernels (the
  * roofline's algorithmic bytes per node): 64 for the quantised 4-wide node (scenes whose
- * 128 B node array exceeds 16 MB), 128 otherwise. */
+ * 128 B node array exceeds 2 MB), 128 otherwise. */
 int pxg_node_bytes(const pxg_ctx* ctx);
 int pxg_synchronize(pxg_ctx* ctx);
 

@@ -529,12 +529,13 @@ void finalize_scene(const SceneDesc& d, SceneHost& h) {
   h.nodes4.clear();
   h.nodes4.reserve(h.nodes.size() / 2 + 2);
   Collapser{h.nodes, h.nodes4}.build(0);
-  // Quantised nodes halve the bytes per visit: a win once the node array outgrows the L1/L2
-  // working set (C4: 43 MB of 128 B nodes, +5.5%); on L2-resident scenes the decode's extra
-  // latency makes the 128 B nodes as fast or faster (C2). PXG_NODEQ=0/1 forces the choice.
+  // Quantised nodes halve the bytes per visit: a win once the node array outgrows the L1
+  // working set (C4: 43 MB of 128 B nodes, +5.5%; C3: 4.5 MB, +3.3% since the near / far
+  // plane selection of node4q_test); on the smallest scenes the 128 B nodes stay as fast or
+  // faster (C2, 1 MB: -0.5% quantised). PXG_NODEQ=0/1 forces the choice.
   {
     const char* e = std::getenv("PXG_NODEQ");
-    h.nodeq = e ? std::atoi(e) != 0 : h.nodes4.size() * sizeof(HostNode4) > (16u << 20);
+    h.nodeq = e ? std::atoi(e) != 0 : h.nodes4.size() * sizeof(HostNode4) > (2u << 20);
   }
   h.nodes4q.clear();
   if (h.nodeq) {
