@@ -183,6 +183,55 @@ int pxg_dump_prims(pxg_ctx* ctx, int* eye, int* light);
 int pxg_dump_pool(pxg_ctx* ctx, int cap, int* n, long long* raw, int* walk, int* end, int* key,
                   double* inv_p, double* inv_p_m2, double* bound);
 
+/* proxima::PathVertex (proj/include/proxima/transport.hpp:17-27) as the device stores it
+ * (128 B): material = index into the scene's materials (-1: camera), flag = VertexFlag
+ * {kLight, kDiffuse, kSpecular, kCamera}. */
+typedef struct pxg_vertex {
+  double p[3], n[3], wi[3], throughput[3];
+  double pdf_fwd;
+  int material, primitive, emitter, flag;
+  double reserved;
+} pxg_vertex;
+
+/* Light vertices a repaired proxy path holds at most (prefix + retraced block + endpoint). */
+#define PXG_MAX_LIGHT 16
+
+/* Per-pixel record of the last pass for replay parity (SURVEY §8c mode ii: the device's
+ * vertices rescored by the reference's own functions). The pool entry fields are the
+ * IncompleteLightSubPath (proj/include/proxima/proxy.hpp:27-42) the pixel's proxy connection
+ * picked; block/retrace_density are its retrace_proxy result (proj/src/proxy.cpp:271-319). */
+typedef struct pxg_path_record {
+  int n_eye, n_light;  /* sub-path vertex counts (eye vertex 0 = camera) */
+  int tp;              /* eye cut at the first non-specular vertex (0: none), proxy.cpp:749-757 */
+  int flags;           /* bit0 tp >= 2, bit1 attempted, bit2 a pool entry was picked,
+                          bit4 retrace accepted (density > 0) */
+  int entry;           /* pool entry index (-1: none) */
+  int u, n_prefix, has_cdir, c_label, s_label, key, reserved;
+  double cdir[3];      /* control_dir (valid when has_cdir) */
+  double prefix_pdf, inverse_p, inverse_p_m2;
+  double retrace_density; /* sample-time density of the retraced block (bit4) */
+  double q_sel;        /* gamma row pmf / bucket size of the pick */
+  double bdpt[3];      /* standard strategies (weighted_bdpt_value) */
+  double c[3];         /* proxy_connect value before gating */
+  double val[3];       /* final per-pixel sample value of the pass */
+} pxg_path_record;
+
+/* Replay dump of the last rendered pass for pixels [px_begin, px_end) of this context
+ * (not for Stage-2 row-tiled contexts). Outputs, any pointer may be NULL:
+ *   rec[m]                                    per-pixel record (m = px_end - px_begin)
+ *   eye[m * (max_depth + 1)]                  eye sub-path vertices, pixel-major
+ *   light[m * (max_depth - 1)]                light sub-path vertices, pixel-major
+ *   proxy[m * PXG_MAX_LIGHT]                  the picked entry: prefix vertices [0, n_prefix),
+ *                                             the retraced block g in reference order
+ *                                             (g[0] nearest the specular endpoint, bit4 only)
+ *                                             at [n_prefix, n_prefix + u), the specular
+ *                                             endpoint at n_prefix + u
+ *   stats[4000 * 3]                           the pass's SubspaceStats snapshot the MIS
+ *                                             weights read: sum_est, sum_est_sq, est_count
+ *                                             per dense key ((u-1)*10+c)*100+s. */
+int pxg_dump_paths(pxg_ctx* ctx, int px_begin, int px_end, pxg_path_record* rec, pxg_vertex* eye, pxg_vertex* light,
+                   pxg_vertex* proxy, double* stats);
+
 /* Scene::intersect / Scene::occluded on the device (parity of the traversal kernel).
  * rays[n*6] = origin, unit direction; tmax may be NULL (1e30). */
 int pxg_intersect(pxg_ctx* ctx, int n, const double* rays, const double* tmax, int* prim, double* t);

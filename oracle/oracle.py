@@ -21,6 +21,17 @@ REF_DIR = os.path.join(_HERE, "_ref")
 N_BUCKETS = 4000
 
 
+# OrcVertex / OrcProxyIn / OrcProxyOut of oracle_driver.cpp (replay parity); OrcVertex has the
+# byte layout of the device's pxg_vertex (include/pxg.h)
+VERTEX_DTYPE = np.dtype([("p", "<f8", 3), ("n", "<f8", 3), ("wi", "<f8", 3), ("throughput", "<f8", 3),
+                         ("pdf_fwd", "<f8"), ("material", "<i4"), ("primitive", "<i4"), ("emitter", "<i4"),
+                         ("flag", "<i4"), ("reserved", "<f8")])
+REPLAY_IN_DTYPE = np.dtype([("tp", "<i4"), ("u", "<i4"), ("n_prefix", "<i4"), ("has_cdir", "<i4"),
+                            ("cdir", "<f8", 3), ("prefix_pdf", "<f8"), ("inverse_p", "<f8")])
+REPLAY_OUT_DTYPE = np.dtype([("prefix_pdf", "<f8"), ("retrace_density", "<f8"), ("weight", "<f8"),
+                             ("c", "<f8", 3), ("s_label", "<i4"), ("c_label", "<i4"), ("pad", "<i4", 2)])
+
+
 class OracleUnavailable(RuntimeError):
     pass
 
@@ -109,6 +120,12 @@ def lib(variant: str = "philox"):
         L.orc_render.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, C.POINTER(OrcParams), C.c_int, _DP,
                                  C.POINTER(OrcTrace)]
         L.orc_recip_twopoint.argtypes = [C.c_int, C.c_double, C.c_longlong, C.c_ulonglong, _DP, _LP, _IP]
+        L.orc_replay_bdpt.argtypes = [C.c_void_p, C.c_int, C.c_void_p, _IP, C.c_int, C.c_void_p, _IP, C.c_int, _DP,
+                                      C.c_int, _DP]
+        L.orc_trace_subpaths.argtypes = [C.c_void_p, C.c_ulonglong, C.c_int, C.c_void_p, _IP, C.c_int, C.c_void_p,
+                                         _IP, C.c_int, C.c_int]
+        L.orc_replay_proxy.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                       _DP, C.c_int, C.c_void_p]
         L.orc_rng_draws.argtypes = [C.c_ulonglong, C.c_uint, C.c_uint, C.c_ulonglong, C.c_int,
                                     C.POINTER(C.c_uint)]
     _libs[name] = L
@@ -194,6 +211,50 @@ class OracleScene:
         _check(self.L, self.L.orc_occluded(self.h, segs.shape[0], _ptr(segs, C.c_double), _ptr(occ, C.c_int),
                                            threads))
         return occ.astype(bool)
+
+    # -- replay parity (SURVEY §8c mode ii): device vertices rescored by the reference
+    def replay_bdpt(self, eye, n_eye, light, n_light, stats3, threads: int = 8) -> np.ndarray:
+        """weighted_bdpt_value (proj/src/proxy.cpp:621-643) of given sub-paths: eye [n, De] and
+        light [n, Dl] vertex rows (pxg_vertex layout), stats3 [4000, 3] the pass's snapshot."""
+        eye = np.ascontiguousarray(eye)
+        light = np.ascontiguousarray(light)
+        ne = np.ascontiguousarray(n_eye, np.int32)
+        nl = np.ascontiguousarray(n_light, np.int32)
+        s3 = np.ascontiguousarray(stats3, np.float64)
+        n = eye.shape[0]
+        out = np.zeros((n, 3))
+        _check(self.L, self.L.orc_replay_bdpt(self.h, n, eye.ctypes.data, _ptr(ne, C.c_int), eye.shape[1],
+                                              light.ctypes.data, _ptr(nl, C.c_int), light.shape[1],
+                                              _ptr(s3, C.c_double), threads, _ptr(out, C.c_double)))
+        return out
+
+    def trace_subpaths(self, seed: int, n: int, threads: int = 8):
+        """Pass 0's eye / light sub-paths of pixels [0, n) as the render loop traces them
+        (proj/src/proxy.cpp:742-744), in the replay vertex layout."""
+        eye = np.zeros((n, self.max_depth + 1), VERTEX_DTYPE)
+        light = np.zeros((n, max(self.max_depth - 1, 1)), VERTEX_DTYPE)
+        ne = np.zeros(n, np.int32)
+        nl = np.zeros(n, np.int32)
+        _check(self.L, self.L.orc_trace_subpaths(self.h, seed, n, eye.ctypes.data, _ptr(ne, C.c_int), eye.shape[1],
+                                                 light.ctypes.data, _ptr(nl, C.c_int), light.shape[1], threads))
+        return eye, ne, light, nl
+
+    def replay_proxy(self, eye, tp, proxy, u, n_prefix, cdir, has_cdir, prefix_pdf, inverse_p, stats3,
+                     threads: int = 8) -> np.ndarray:
+        """proxy_pdf_components (proj/src/proxy.cpp:321-378), dropout labels and the
+        proxy_connect value (proxy.cpp:562-602) of given proxy paths; returns REPLAY_OUT_DTYPE."""
+        n = len(tp)
+        inp = np.zeros(n, REPLAY_IN_DTYPE)
+        inp["tp"], inp["u"], inp["n_prefix"], inp["has_cdir"] = tp, u, n_prefix, has_cdir
+        inp["cdir"], inp["prefix_pdf"], inp["inverse_p"] = cdir, prefix_pdf, inverse_p
+        out = np.zeros(n, REPLAY_OUT_DTYPE)
+        eye = np.ascontiguousarray(eye)
+        proxy = np.ascontiguousarray(proxy)
+        s3 = np.ascontiguousarray(stats3, np.float64)
+        _check(self.L, self.L.orc_replay_proxy(self.h, n, eye.ctypes.data, eye.shape[1], proxy.ctypes.data,
+                                               proxy.shape[1], inp.ctypes.data, _ptr(s3, C.c_double), threads,
+                                               out.ctypes.data))
+        return out
 
     def render_bdpt(self, spp: int, seed: int) -> np.ndarray:
         out = np.zeros((self.height, self.width, 3))

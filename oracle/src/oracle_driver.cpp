@@ -806,6 +806,217 @@ ORC_API int orc_recip_twopoint(int n, double bound, long long cap, unsigned long
   }
 }
 
+// ---- Replay parity (SURVEY §8c mode ii): the device's vertices rescored by the reference.
+// The vertex record mirrors pxg_vertex / the device PathVertex (include/pxg.h).
+struct OrcVertex {
+  double p[3], n[3], wi[3], thr[3];
+  double pdf_fwd;
+  int material, primitive, emitter, flag;
+  double reserved;
+};
+
+// One pixel's proxy connection inputs (the pool entry the device picked).
+struct OrcProxyIn {
+  int tp;          // eye cut (eye vertices [0, tp))
+  int u, n_prefix, has_cdir;
+  double cdir[3];
+  double prefix_pdf, inverse_p;
+};
+
+// Rescored values: prefix / retrace densities (proxy_pdf_components), subspace labels,
+// the reciprocal-aware MIS weight and the proxy_connect value of the device's path.
+struct OrcProxyOut {
+  double prefix_pdf, retrace_density, weight;
+  double c[3];
+  int s_label, c_label, pad0, pad1;
+};
+
+static PathVertex to_vertex(const Scene& scene, const OrcVertex& v) {
+  PathVertex o;
+  o.p = Vec3(v.p[0], v.p[1], v.p[2]);
+  o.n = Vec3(v.n[0], v.n[1], v.n[2]);
+  o.wi = Vec3(v.wi[0], v.wi[1], v.wi[2]);
+  o.throughput = Vec3(v.thr[0], v.thr[1], v.thr[2]);
+  o.pdf_fwd = v.pdf_fwd;
+  o.material = v.material >= 0 ? &scene.materials[static_cast<size_t>(v.material)] : nullptr;
+  o.primitive = v.primitive;
+  o.emitter = v.emitter;
+  o.flag = static_cast<VertexFlag>(v.flag);
+  return o;
+}
+
+static SubspaceStats stats_from_dense(const double* s3) {
+  SubspaceStats st;
+  for (int k = 0; k < kBuckets; ++k) {
+    const long long cnt = static_cast<long long>(s3[3 * k + 2]);
+    if (cnt <= 0) continue;
+    BucketStats b;
+    b.sum_est = s3[3 * k];
+    b.sum_est_sq = s3[3 * k + 1];
+    b.est_count = cnt;
+    st.buckets[StatsKey{k / 1000 + 1, (k / 100) % 10, k % 100}] = b;
+  }
+  return st;
+}
+
+// weighted_bdpt_value (proj/src/proxy.cpp:621-643) of the device's sub-paths:
+// eye[i*eye_stride + k], k < n_eye[i]; light likewise; stats3 = the pass's snapshot
+// (pxg_dump_paths). out[i*3] = the standard-strategy sum.
+ORC_API int orc_replay_bdpt(void* h, int n, const OrcVertex* eye, const int* n_eye, int eye_stride,
+                            const OrcVertex* light, const int* n_light, int light_stride, const double* stats3,
+                            int threads, double* out) {
+  try {
+    const Scene& scene = static_cast<OrcScene*>(h)->scene;
+    const SubspaceMapper mapper = SubspaceMapper::for_scene(scene);
+    const SubspaceStats stats = stats_from_dense(stats3);
+    parallel_for(n, threads, [&](int i) {
+      SubPath e, l;
+      e.kind = SubPathKind::kEye;
+      l.kind = SubPathKind::kLight;
+      for (int k = 0; k < n_eye[i]; ++k) e.vertices.push_back(to_vertex(scene, eye[static_cast<size_t>(i) * eye_stride + k]));
+      for (int k = 0; k < n_light[i]; ++k)
+        l.vertices.push_back(to_vertex(scene, light[static_cast<size_t>(i) * light_stride + k]));
+      Vec3 v = weighted_bdpt(scene, e, l, mapper, stats);
+      out[3 * i] = v.x;
+      out[3 * i + 1] = v.y;
+      out[3 * i + 2] = v.z;
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+static OrcVertex from_vertex(const Scene& scene, const PathVertex& v) {
+  OrcVertex o;
+  std::memset(&o, 0, sizeof(o));
+  const Vec3* src[4] = {&v.p, &v.n, &v.wi, &v.throughput};
+  double* dst[4] = {o.p, o.n, o.wi, o.thr};
+  for (int k = 0; k < 4; ++k) {
+    dst[k][0] = src[k]->x;
+    dst[k][1] = src[k]->y;
+    dst[k][2] = src[k]->z;
+  }
+  o.pdf_fwd = v.pdf_fwd;
+  o.material = v.material ? static_cast<int>(v.material - scene.materials.data()) : -1;
+  o.primitive = v.primitive;
+  o.emitter = v.emitter;
+  o.flag = static_cast<int>(v.flag);
+  return o;
+}
+
+// The first pass's sub-paths of pixels [0, n) as the render loop traces them
+// (proj/src/proxy.cpp:742-744: eye then light sub-path on the pixel stream Rng(seed, idx)),
+// in the replay vertex layout: pins the replay evaluator against the restated loop on the CPU.
+ORC_API int orc_trace_subpaths(void* h, unsigned long long seed, int n, OrcVertex* eye, int* n_eye, int eye_stride,
+                               OrcVertex* light, int* n_light, int light_stride, int threads) {
+  try {
+    const Scene& scene = static_cast<OrcScene*>(h)->scene;
+    const int width = scene.camera.width;
+    const int max_depth = scene.settings.max_depth;
+    parallel_for(n, threads, [&](int idx) {
+      Rng rng(seed, static_cast<uint64_t>(idx));
+      SubPath e = trace_eye_subpath(scene, idx % width, idx / width, max_depth + 1, rng);
+      SubPath l = trace_light_subpath(scene, max_depth - 1, rng);
+      n_eye[idx] = static_cast<int>(e.vertices.size());
+      n_light[idx] = static_cast<int>(l.vertices.size());
+      for (int k = 0; k < n_eye[idx] && k < eye_stride; ++k)
+        eye[static_cast<size_t>(idx) * eye_stride + k] = from_vertex(scene, e.vertices[k]);
+      for (int k = 0; k < n_light[idx] && k < light_stride; ++k)
+        light[static_cast<size_t>(idx) * light_stride + k] = from_vertex(scene, l.vertices[k]);
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The proxy connection of the device's path: px[i*kMaxLight + ..] holds the picked entry's
+// prefix [0, n_prefix), the retraced block g (reference order) [n_prefix, n_prefix+u) and the
+// specular endpoint at n_prefix+u. Recomputes proxy_pdf_components (proj/src/proxy.cpp:321-378),
+// the labels dropout assigns (proxy.cpp:87-89) and the value proxy_connect forms after its
+// retrace (proxy.cpp:562-602, with the recomputed retrace density), all with the reference's
+// functions.
+ORC_API int orc_replay_proxy(void* h, int n, const OrcVertex* eye, int eye_stride, const OrcVertex* px, int px_stride,
+                             const OrcProxyIn* in, const double* stats3, int threads, OrcProxyOut* out) {
+  try {
+    const Scene& scene = static_cast<OrcScene*>(h)->scene;
+    const SubspaceMapper mapper = SubspaceMapper::for_scene(scene);
+    const SubspaceStats stats = stats_from_dense(stats3);
+    parallel_for(n, threads, [&](int i) {
+      const OrcProxyIn& a = in[i];
+      OrcProxyOut& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      const OrcVertex* pv = px + static_cast<size_t>(i) * px_stride;
+      IncompleteLightSubPath inc;
+      for (int k = 0; k < a.n_prefix; ++k) inc.prefix.push_back(to_vertex(scene, pv[k]));
+      inc.specular_end = to_vertex(scene, pv[a.n_prefix + a.u]);
+      if (a.has_cdir) inc.control_dir = Vec3(a.cdir[0], a.cdir[1], a.cdir[2]);
+      inc.u = a.u;
+      inc.prefix_pdf = a.prefix_pdf;
+      inc.inverse_p = a.inverse_p;
+      inc.s_label = mapper.classify_specular(inc.specular_end);
+      inc.c_label = mapper.classify_control(inc.control(), inc.control_dir);
+      o.s_label = inc.s_label;
+      o.c_label = inc.c_label;
+      std::vector<PathVertex> g;
+      for (int j = 0; j < a.u; ++j) g.push_back(to_vertex(scene, pv[a.n_prefix + j]));
+      SubPath e;
+      e.kind = SubPathKind::kEye;
+      for (int k = 0; k < a.tp; ++k) e.vertices.push_back(to_vertex(scene, eye[static_cast<size_t>(i) * eye_stride + k]));
+      const PathVertex& z = e.vertices[a.tp - 1];
+      ProxyPdfComponents comps = proxy_pdf_components(inc, g, z, scene);
+      o.prefix_pdf = comps.prefix_pdf;
+      o.retrace_density = comps.retrace_density;
+      if (!(comps.retrace_density > 0.0)) return;
+      // proxy_connect after retrace_proxy (proxy.cpp:562-602)
+      SubPath rep = repair(inc, g);
+      const auto& lv = rep.vertices;
+      const int s = static_cast<int>(lv.size());
+      const int t = a.tp;
+      Vec3 d01 = lv[1].p - lv[0].p;
+      double l01 = length(d01);
+      if (l01 <= 0.0 || lv[0].emitter < 0) return;
+      Vec3 value = scene.emitted(lv[0].emitter, lv[0].n, d01 / l01);
+      if (near_zero3(value)) return;
+      for (int k = 0; k + 1 < s; ++k) {
+        double gt = geometry_term(lv[k], lv[k + 1], scene);
+        if (gt <= 0.0) return;
+        value *= gt;
+      }
+      double gj = geometry_term(lv[s - 1], z, scene);
+      if (gj <= 0.0) return;
+      value *= gj;
+      for (int k = 1; k < s; ++k) {
+        Vec3 wi = normalize(lv[k - 1].p - lv[k].p);
+        Vec3 to = k + 1 < s ? lv[k + 1].p : z.p;
+        Vec3 wo = normalize(to - lv[k].p);
+        Vec3 fk = eval_bsdf(*lv[k].material, lv[k].n, wi, wo);
+        if (near_zero3(fk)) return;
+        value = value * fk;
+      }
+      Vec3 fz = eval_bsdf(*z.material, z.n, z.wi, normalize(lv[s - 1].p - z.p));
+      if (near_zero3(fz)) return;
+      value = value * fz * z.throughput;
+      FullPath fp;
+      fp.light = lv;
+      fp.eye = e.vertices;
+      fp.s = s;
+      fp.t = t;
+      const double w = reciprocal_mis_weight(fp, StrategyId{s, t, true}, scene, mapper, stats);
+      o.weight = w;
+      if (!(w > 0.0)) return;
+      Vec3 c = value * (inc.inverse_p * w / (inc.prefix_pdf * comps.retrace_density));
+      o.c[0] = c.x;
+      o.c[1] = c.y;
+      o.c[2] = c.z;
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // Philox stream check: first n draws of Rng::keyed(seed, kind, sub, stream).
 ORC_API void orc_rng_draws(unsigned long long seed, unsigned kind, unsigned sub,
                            unsigned long long stream, int n, unsigned* out) {

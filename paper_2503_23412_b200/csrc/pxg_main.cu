@@ -850,7 +850,7 @@ void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, 
       std::swap(in, out);
     }
     CK(cudaMemsetAsync(c->qPS.count, 0, sizeof(int), sp));
-    k_pxw_value<<<blocks(c->n, T), T, 0, sp>>>(C, W, c->qPS);
+    k_pxw_value<<<blocks(c->n, T), T, 0, sp>>>(C, W, c->qPS, c->d_prox);
     {
       int* fetch = c->d_trav_next + 4;
       CK(cudaMemsetAsync(fetch, 0, sizeof(int), sp));
@@ -1762,6 +1762,132 @@ int pxg_dump_pass(pxg_ctx* c, double* val, double* bdpt, double* cc, int* flags)
         for (int k = 0; k < 3; ++k) cc[3 * i + k] = c->proxy_on ? pr[i].c[k] : 0.0;
     }
     if (flags) CK(cudaMemcpy(flags, c->d_pflags, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+static_assert(sizeof(pxg_vertex) == sizeof(PV), "pxg_vertex mirrors PV");
+static_assert(PXG_MAX_LIGHT == kMaxLight, "repaired light sub-path capacity");
+static_assert(sizeof(pxg_path_record) == 184, "pxg_path_record layout (render.PATH_RECORD_DTYPE)");
+
+int pxg_dump_paths(pxg_ctx* c, int px_begin, int px_end, pxg_path_record* rec, pxg_vertex* eye, pxg_vertex* light,
+                   pxg_vertex* proxy, double* stats) {
+  return guarded(c, [&]() {
+    if (c->ntiles > 1) throw InvalidErr{"pxg_dump_paths: not available for Stage-2 row-tiled contexts"};
+    if (px_begin < 0 || px_end > c->n || px_begin > px_end) throw InvalidErr{"pxg_dump_paths: pixel range"};
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->stream1));
+    const int m = px_end - px_begin;
+    const size_t n = c->n;
+    const int de = c->max_depth + 1, dl = std::max(c->max_depth - 1, 1);
+    // vertex-major device pools [k][pixel] -> pixel-major host rows, one strided copy per vertex index
+    if (eye)
+      for (int k = 0; k < de; ++k)
+        CK(cudaMemcpy2D(eye + k, sizeof(PV) * de, c->d_eye + k * n + px_begin, sizeof(PV), sizeof(PV), m,
+                        cudaMemcpyDeviceToHost));
+    if (light)
+      for (int k = 0; k < dl; ++k)
+        CK(cudaMemcpy2D(light + k, sizeof(PV) * dl, c->d_light + k * n + px_begin, sizeof(PV), sizeof(PV), m,
+                        cudaMemcpyDeviceToHost));
+    std::vector<int> ne(m), nl(m);
+    if (m) {
+      CK(cudaMemcpy(ne.data(), c->d_neye + px_begin, sizeof(int) * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(nl.data(), c->d_nlight + px_begin, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    }
+    std::vector<double> val(3 * m), bdpt(3 * m);
+    if (m) {
+      CK(cudaMemcpy(val.data(), c->d_val + 3 * px_begin, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(bdpt.data(), c->d_bdpt + 3 * px_begin, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost));
+    }
+    std::vector<ProxRec> pr;
+    std::vector<int> entry, tp;
+    std::vector<double> dens;
+    std::vector<PV> lv;
+    std::vector<IncHdr> inc;
+    std::vector<PV> pre;
+    const bool px_on = c->proxy_on && c->passes_done > 0;
+    if (px_on && m) {
+      pr.resize(m);
+      entry.resize(m);
+      tp.resize(m);
+      dens.resize(m);
+      lv.resize(static_cast<size_t>(m) * kMaxLight);
+      CK(cudaMemcpy(pr.data(), c->d_prox + px_begin, sizeof(ProxRec) * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(entry.data(), c->pw.entry + px_begin, sizeof(int) * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(tp.data(), c->pw.tp + px_begin, sizeof(int) * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dens.data(), c->pw.density + px_begin, sizeof(double) * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(lv.data(), c->pw.lv + static_cast<size_t>(px_begin) * kMaxLight, sizeof(PV) * kMaxLight * m,
+                    cudaMemcpyDeviceToHost));
+      const PoolSlot& sl = c->slot_of(c->passes_done - 1);
+      PassState ps;
+      CK(cudaMemcpy(&ps, sl.ps, sizeof(PassState), cudaMemcpyDeviceToHost));
+      if (ps.n_ent > 0) {
+        inc.resize(ps.n_ent);
+        pre.resize(static_cast<size_t>(ps.n_ent) * kMaxLight);
+        CK(cudaMemcpy(inc.data(), sl.inc, sizeof(IncHdr) * ps.n_ent, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(pre.data(), sl.prefix, sizeof(PV) * kMaxLight * ps.n_ent, cudaMemcpyDeviceToHost));
+      }
+      if (stats) {
+        std::vector<double> s(kBuckets), q(kBuckets);
+        std::vector<long long> cnt(kBuckets);
+        CK(cudaMemcpy(s.data(), sl.snap_sum, sizeof(double) * kBuckets, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(q.data(), sl.snap_sq, sizeof(double) * kBuckets, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cnt.data(), sl.snap_cnt, sizeof(long long) * kBuckets, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < kBuckets; ++k) {
+          stats[3 * k] = s[k];
+          stats[3 * k + 1] = q[k];
+          stats[3 * k + 2] = static_cast<double>(cnt[k]);
+        }
+      }
+    } else if (stats) {
+      for (int k = 0; k < 3 * kBuckets; ++k) stats[k] = 0.0;
+    }
+    for (int i = 0; i < m; ++i) {
+      pxg_path_record r;
+      std::memset(&r, 0, sizeof(r));
+      r.n_eye = ne[i];
+      r.n_light = nl[i];
+      r.entry = -1;
+      for (int k = 0; k < 3; ++k) {
+        r.val[k] = val[3 * i + k];
+        r.bdpt[k] = bdpt[3 * i + k];
+      }
+      pxg_vertex* pv = proxy ? proxy + static_cast<size_t>(i) * kMaxLight : nullptr;
+      if (pv) std::memset(pv, 0, sizeof(pxg_vertex) * kMaxLight);
+      if (px_on) {
+        const ProxRec& o = pr[i];
+        r.flags = o.flags;
+        r.q_sel = o.q_sel;
+        for (int k = 0; k < 3; ++k) r.c[k] = o.c[k];
+        if (o.flags & 1) r.tp = tp[i];
+        if ((o.flags & 4) && entry[i] >= 0 && entry[i] < static_cast<int>(inc.size())) {
+          const int e = entry[i];
+          const IncHdr& h = inc[e];
+          r.entry = e;
+          r.u = h.u;
+          r.n_prefix = h.n_prefix;
+          r.has_cdir = h.has_cdir;
+          r.c_label = h.c_label;
+          r.s_label = h.s_label;
+          r.key = h.key;
+          r.cdir[0] = h.cdir.x;
+          r.cdir[1] = h.cdir.y;
+          r.cdir[2] = h.cdir.z;
+          r.prefix_pdf = h.prefix_pdf;
+          r.inverse_p = h.inverse_p;
+          r.inverse_p_m2 = h.inverse_p_m2;
+          if (o.flags & 16) r.retrace_density = dens[i];
+          if (pv) {
+            std::memcpy(pv, &pre[static_cast<size_t>(e) * kMaxLight], sizeof(PV) * h.n_prefix);
+            if (o.flags & 16)  // device slot n_prefix + (u-1-j) holds g[j]
+              for (int j = 0; j < h.u; ++j)
+                std::memcpy(pv + h.n_prefix + j, &lv[static_cast<size_t>(i) * kMaxLight + h.n_prefix + (h.u - 1 - j)],
+                            sizeof(PV));
+            std::memcpy(pv + h.n_prefix + h.u, &h.spec_end, sizeof(PV));
+          }
+        }
+      }
+      if (rec) rec[i] = r;
+    }
   });
 }
 

@@ -242,12 +242,13 @@ __global__ void PXW_BOUNDS k_pxw_retrace(ProxCtx C, ProxWave W, int pass, int n_
 }
 
 // Repair, value without visibility, and one shadow ray per segment (proxy.cpp:562-592).
-__global__ void PXW_BOUNDS k_pxw_value(ProxCtx C, ProxWave W, RayQueue shadow) {
+__global__ void PXW_BOUNDS k_pxw_value(ProxCtx C, ProxWave W, RayQueue shadow, ProxRec* rec) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C.n) return;
   W.occl[i] = 0;
   if (W.state[i] != kPxRetraced) return;
   W.state[i] = kPxNone;
+  rec[i].flags |= 16;  // retrace accepted (replay dump)
   const IncHdr& h = C.inc[W.entry[i]];
   const PV* pre = C.prefix + static_cast<size_t>(W.entry[i]) * kMaxLight;
   PV* lv = W.lv + static_cast<size_t>(i) * kMaxLight;

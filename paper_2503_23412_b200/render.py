@@ -22,6 +22,19 @@ from . import _lib
 from .scene import Scene
 
 N_BUCKETS = 4000
+MAX_LIGHT = 16  # PXG_MAX_LIGHT
+
+# pxg_vertex / pxg_path_record (include/pxg.h): the device PathVertex and the replay record.
+VERTEX_DTYPE = np.dtype([("p", "<f8", 3), ("n", "<f8", 3), ("wi", "<f8", 3), ("throughput", "<f8", 3),
+                         ("pdf_fwd", "<f8"), ("material", "<i4"), ("primitive", "<i4"), ("emitter", "<i4"),
+                         ("flag", "<i4"), ("reserved", "<f8")])
+PATH_RECORD_DTYPE = np.dtype([("n_eye", "<i4"), ("n_light", "<i4"), ("tp", "<i4"), ("flags", "<i4"),
+                              ("entry", "<i4"), ("u", "<i4"), ("n_prefix", "<i4"), ("has_cdir", "<i4"),
+                              ("c_label", "<i4"), ("s_label", "<i4"), ("key", "<i4"), ("reserved", "<i4"),
+                              ("cdir", "<f8", 3), ("prefix_pdf", "<f8"), ("inverse_p", "<f8"),
+                              ("inverse_p_m2", "<f8"), ("retrace_density", "<f8"), ("q_sel", "<f8"),
+                              ("bdpt", "<f8", 3), ("c", "<f8", 3), ("val", "<f8", 3)])
+assert VERTEX_DTYPE.itemsize == 128 and PATH_RECORD_DTYPE.itemsize == 48 + 24 + 40 + 72
 
 
 @dataclass
@@ -339,6 +352,22 @@ class ProxyRenderer:
         k = min(n.value, cap)
         return dict(n=n.value, raw=raw.value, walk=walk[:k], end=end[:k], key=key[:k], inv_p=ip[:k],
                     inv_p_m2=m2[:k], bound=bd[:k])
+
+    def dump_paths(self, px_begin: int = 0, px_end: int | None = None):
+        """Replay dump of the last pass (pxg_dump_paths): per-pixel records (PATH_RECORD_DTYPE),
+        eye [m, max_depth+1] / light [m, max_depth-1] / proxy [m, PXG_MAX_LIGHT] vertices
+        (VERTEX_DTYPE) and the pass's statistics snapshot [4000, 3] (sum_est, sum_est_sq,
+        est_count)."""
+        px_end = self.n if px_end is None else px_end
+        m = max(px_end - px_begin, 0)
+        rec = np.zeros(m, PATH_RECORD_DTYPE)
+        eye = np.zeros((m, self.max_depth + 1), VERTEX_DTYPE)
+        light = np.zeros((m, max(self.max_depth - 1, 1)), VERTEX_DTYPE)
+        proxy = np.zeros((m, MAX_LIGHT), VERTEX_DTYPE)
+        stats = np.zeros((N_BUCKETS, 3))
+        self._check(self._L.pxg_dump_paths(self._ctx, px_begin, px_end, rec.ctypes.data, eye.ctypes.data,
+                                           light.ctypes.data, proxy.ctypes.data, _dp(stats)))
+        return rec, eye, light, proxy, stats
 
     # -- traversal parity entry points (Scene::intersect / Scene::occluded)
     def intersect(self, rays: np.ndarray, tmax=None):

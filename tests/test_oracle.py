@@ -186,3 +186,22 @@ def test_scene_npz_cache_roundtrip(tmp_path):
         save_npz(sc, p)
         back = load_npz(p)
         assert json.loads(back.to_json()) == json.loads(sc.to_json())  # 0 == 0.0: same values
+
+
+@pytest.mark.parametrize("name", ["c1", "caustic_box", "glass_slab"])
+def test_replay_evaluator_reproduces_restated_loop(oracle, name):
+    """The replay evaluator (orc_replay_bdpt: weighted_bdpt_value over given vertex rows) on the
+    reference's own pass-0 sub-paths equals the restated loop's per-pixel standard-strategy value
+    bitwise (proxy off: empty statistics, the balance heuristic) — the harness the GPU replay
+    test (tests/test_replay.py) rescores device vertices with."""
+    from paper_2503_23412_b200 import scenes
+    sc = {"c1": lambda: scenes.cornell_c1(16, max_depth=8), "caustic_box": lambda: scenes.caustic_box(12),
+          "glass_slab": lambda: scenes.glass_slab(12)}[name]()
+    o = oracle.OracleScene(sc.to_json())
+    pd = {"enabled": 0}
+    _, run = o.render(1, 5, params=pd, threads=4, trace=True)
+    eye, ne, light, nl = o.trace_subpaths(5, sc.n_px, threads=4)
+    assert (ne >= 1).all()
+    bd = o.replay_bdpt(eye, ne, light, nl, np.zeros((oracle.N_BUCKETS, 3)), threads=4)
+    assert np.array_equal(bd, run.pass_bdpt[0])
+    assert np.count_nonzero(bd) > 0
