@@ -90,7 +90,10 @@ def test_replay_rescoring_matches_device(pxg, oracle, name, parity_report):
     assert rec["label_mismatch"] == 0
     assert rec["c_over_tol"] == 0
     assert rec["zero_c_without_retrace"]
-    if name in ("caustic_box", "glass_slab", "c2_small", "C2_full"):
+    # glass_slab's u = 2 retraces are accepted about once per 10 passes at this size (the restated
+    # loop agrees: no accepted retrace in these 4 passes), so it only pins the standard strategies
+    # and the zero-without-retrace rule
+    if name in ("caustic_box", "c2_small", "C2_full"):
         assert rec["proxy_paths"] > 0 and rec["c_nonzero"] > 0
 
 
