@@ -352,6 +352,9 @@ def run_ours(args):
     t_fin = time.perf_counter() - t_fin
     W, H = sc.camera.width, sc.camera.height
     params = ProxyParams(light_walks=walks)
+    if os.environ.get("PXG_TUNE_PARAMS") and args.quick:  # tuning sweeps only (--quick lines are never bench values)
+        for k, v in json.loads(os.environ["PXG_TUNE_PARAMS"]).items():
+            setattr(params, k, v)
 
     # ---- device-resident throughput: K passes after W warm-up passes (CUDA events)
     # N > 1: sample sharding (paper_2503_23412_b200/distributed.py): every rank renders K

@@ -481,7 +481,7 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
       launch_trav<false>(c, in, fetch, st);
     }
     CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
-    k_shade<<<blocks(P.n, T), T, 0, st>>>(c->S, P, in, out);
+    k_shade<<<blocks(P.n, PXG_SHADE_T), PXG_SHADE_T, 0, st>>>(c->S, P, in, out);
     c->launches += 2;
     std::swap(in, out);
   }
