@@ -237,6 +237,20 @@ int pxg_dump_paths(pxg_ctx* ctx, int px_begin, int px_end, pxg_path_record* rec,
 int pxg_intersect(pxg_ctx* ctx, int n, const double* rays, const double* tmax, int* prim, double* t);
 int pxg_occluded(pxg_ctx* ctx, int n, const double* segs, int* occ);
 
+/* Parity probe of the proxy densities on caller-supplied vertices (device-level pins of the
+ * reference's closed-form tests, proj/tests/test_proxy.cpp:480-618): the light walk
+ * walk[n_walk] goes through dropout (proj/src/proxy.cpp:59-94) on the device;
+ *   info[8]      {valid, u, n_prefix, has_control_dir, c_label, s_label, dense key, dropped flag}
+ *   prefix_pdf   IncompleteLightSubPath::prefix_pdf
+ *   q[i], f[i]   support_pdf (proxy.cpp:153-209) and target_density (proxy.cpp:106-151) of the
+ *                candidate block cand[i*u .. i*u+u) (g[0] nearest the specular endpoint)
+ *   draw_*[j]    support_sample (proxy.cpp:211-269) on stream (seed, PROBE, 0, j): the block
+ *                (u vertices, zero when escaped), its density (1 when escaped), the escape flag.
+ * Nothing is computed when dropout rejects the walk (info[0] = 0). */
+int pxg_proxy_probe(pxg_ctx* ctx, int n_walk, const pxg_vertex* walk, int n_cand, const pxg_vertex* cand, int n_draws,
+                    uint64_t seed, int* info, double* prefix_pdf, double* q, double* f, pxg_vertex* draw_cand,
+                    double* draw_q, int* draw_escaped);
+
 /* Parity of the traversal kernels that ship: the same rays as pxg_intersect (any_hit = 0:
  * rays[n*6] origin + unit direction, tmax may be NULL) or pxg_occluded (any_hit = 1:
  * segments[n*6] from + to, prim[i] = 1 when occluded, t unused) through

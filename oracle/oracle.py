@@ -126,6 +126,8 @@ def lib(variant: str = "philox"):
                                          _IP, C.c_int, C.c_int]
         L.orc_replay_proxy.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
                                        _DP, C.c_int, C.c_void_p]
+        L.orc_proxy_probe.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_ulonglong,
+                                      _IP, _DP, _DP, _DP, C.c_void_p, _DP, _IP]
         L.orc_rng_draws.argtypes = [C.c_ulonglong, C.c_uint, C.c_uint, C.c_ulonglong, C.c_int,
                                     C.POINTER(C.c_uint)]
     _libs[name] = L
@@ -238,6 +240,27 @@ class OracleScene:
         _check(self.L, self.L.orc_trace_subpaths(self.h, seed, n, eye.ctypes.data, _ptr(ne, C.c_int), eye.shape[1],
                                                  light.ctypes.data, _ptr(nl, C.c_int), light.shape[1], threads))
         return eye, ne, light, nl
+
+    def proxy_probe(self, walk, cand=None, n_draws: int = 0, seed: int = 0):
+        """The reference's dropout / support_pdf / target_density / support_sample
+        (proj/src/proxy.cpp:59-269) on caller-built vertices: the checker of pxg_proxy_probe."""
+        walk = np.ascontiguousarray(walk, VERTEX_DTYPE)
+        info = np.zeros(8, np.int32)
+        pp = np.zeros(1)
+        nc = 0 if cand is None else cand.shape[0]
+        cflat = None if cand is None else np.ascontiguousarray(cand, VERTEX_DTYPE)
+        q, f = np.zeros(max(nc, 1)), np.zeros(max(nc, 1))
+        dc = np.zeros((max(n_draws, 1), 4), VERTEX_DTYPE)
+        dq = np.zeros(max(n_draws, 1))
+        de = np.zeros(max(n_draws, 1), np.int32)
+        _check(self.L, self.L.orc_proxy_probe(self.h, len(walk), walk.ctypes.data, nc,
+                                              cflat.ctypes.data if nc else None, n_draws, seed, _ptr(info, C.c_int),
+                                              _ptr(pp, C.c_double), _ptr(q, C.c_double), _ptr(f, C.c_double),
+                                              dc.ctypes.data, _ptr(dq, C.c_double), _ptr(de, C.c_int)))
+        u = int(info[1]) if info[0] else 0
+        draws = dc.reshape(-1)[:n_draws * u].reshape(n_draws, u) if u else dc[:0]
+        return {"info": info, "prefix_pdf": float(pp[0]), "q": q[:nc], "f": f[:nc], "draw_cand": draws,
+                "draw_q": dq[:n_draws], "draw_escaped": de[:n_draws].astype(bool)}
 
     def replay_proxy(self, eye, tp, proxy, u, n_prefix, cdir, has_cdir, prefix_pdf, inverse_p, stats3,
                      threads: int = 8) -> np.ndarray:

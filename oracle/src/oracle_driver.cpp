@@ -1017,6 +1017,56 @@ ORC_API int orc_replay_proxy(void* h, int n, const OrcVertex* eye, int eye_strid
   }
 }
 
+// The reference's dropout, support_pdf, target_density and support_sample on caller-supplied
+// vertices (proj/src/proxy.cpp:59-269): the checker of pxg_proxy_probe. Draw j uses the stream
+// Rng::keyed(seed, 3 /* PROBE */, 0, j), like the device probe.
+ORC_API int orc_proxy_probe(void* h, int n_walk, const OrcVertex* walk, int n_cand, const OrcVertex* cand,
+                            int n_draws, unsigned long long seed, int* info, double* prefix_pdf, double* q,
+                            double* f, OrcVertex* draw_cand, double* draw_q, int* draw_escaped) {
+  try {
+    const Scene& scene = static_cast<OrcScene*>(h)->scene;
+    const SubspaceMapper mapper = SubspaceMapper::for_scene(scene);
+    SubPath sp;
+    sp.kind = SubPathKind::kLight;
+    for (int k = 0; k < n_walk; ++k) sp.vertices.push_back(to_vertex(scene, walk[k]));
+    for (int k = 0; k < 8; ++k) info[k] = 0;
+    *prefix_pdf = 0.0;
+    auto inc = dropout(sp, mapper);
+    if (!inc) return 0;
+    info[0] = 1;
+    info[1] = inc->u;
+    info[2] = static_cast<int>(inc->prefix.size());
+    info[3] = inc->control_dir.has_value() ? 1 : 0;
+    info[4] = inc->c_label;
+    info[5] = inc->s_label;
+    info[6] = ((inc->u - 1) * 10 + inc->c_label) * 100 + inc->s_label;
+    info[7] = static_cast<int>(sp.vertices[inc->prefix.size()].flag);
+    *prefix_pdf = inc->prefix_pdf;
+    const int u = inc->u;
+    for (int i = 0; i < n_cand; ++i) {
+      std::vector<PathVertex> g;
+      for (int k = 0; k < u; ++k) g.push_back(to_vertex(scene, cand[static_cast<size_t>(i) * u + k]));
+      q[i] = support_pdf(*inc, g, scene);
+      f[i] = target_density(*inc, g, scene);
+    }
+    for (int j = 0; j < n_draws; ++j) {
+      Rng rng = Rng::keyed(seed, 3, 0, static_cast<uint64_t>(j));
+      SupportCandidate c = support_sample(*inc, scene, rng);
+      draw_q[j] = c.q;
+      draw_escaped[j] = c.escaped ? 1 : 0;
+      for (int k = 0; k < u; ++k) {
+        OrcVertex z;
+        std::memset(&z, 0, sizeof(z));
+        draw_cand[static_cast<size_t>(j) * u + k] =
+            (!c.escaped && k < static_cast<int>(c.g.size())) ? from_vertex(scene, c.g[k]) : z;
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // Philox stream check: first n draws of Rng::keyed(seed, kind, sub, stream).
 ORC_API void orc_rng_draws(unsigned long long seed, unsigned kind, unsigned sub,
                            unsigned long long stream, int n, unsigned* out) {

@@ -233,8 +233,7 @@ struct pxg_ctx {
   double *d_grid_total = nullptr, *d_grid_proxy = nullptr;
   int *d_gbin = nullptr, *d_gbin_sorted = nullptr;
   double *d_gval = nullptr, *d_gval_sorted = nullptr;
-  void* d_gsort_tmp = nullptr;
-  size_t gsort_bytes = 0;
+  int* d_gsort_tmp = nullptr;  // stable_bin_sort scratch (pxg_prims.cuh)
   int* d_pflags = nullptr;
   int *d_eye_prims = nullptr, *d_light_prims = nullptr;
   // stats (live, written by Stage 1 only)
@@ -286,8 +285,7 @@ struct pxg_ctx {
   ConnBuf conn{};
   PathCache pcache{};
   double *d_ebeta = nullptr, *d_epdf = nullptr, *d_lbeta = nullptr, *d_lpdf = nullptr;
-  void* d_scan_tmp = nullptr;
-  size_t scan_tmp_bytes = 0;
+  int* d_scan_tmp = nullptr;  // exclusive_sum scratch (pxg_prims.cuh)
   int max_slots = 0;
   PV* d_wpool = nullptr;
   int* d_wnv = nullptr;
@@ -493,7 +491,7 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
   cudaStream_t st = c->stream;
   ConnBuf& C = c->conn;
   k_conn_count<<<blocks(n, T), T, 0, st>>>(c->d_neye, c->d_nlight, n, D, C.count);
-  CK(cub::DeviceScan::ExclusiveSum(c->d_scan_tmp, c->scan_tmp_bytes, C.count, C.offset, n + 1, st));
+  c->launches += exclusive_sum(C.count, C.offset, n + 1, c->d_scan_tmp, st);
   k_conn_enum<<<blocks(n, T), T, 0, st>>>(c->d_neye, c->d_nlight, n, D, C);
   CK(cudaMemsetAsync(c->qS.count, 0, sizeof(int), st));
   CK(cudaMemsetAsync(C.n_live, 0, sizeof(int), st));
@@ -517,7 +515,7 @@ void connections(pxg_ctx* c, bool use_stats, const PoolSlot& sl) {
                                              StatsView{c->d_max_ratio, sl.snap_sum, sl.snap_sq, sl.snap_cnt},
                                              use_stats ? 1 : 0, c->d_eye, c->d_light, n, C, c->pcache);
   k_conn_sum<<<blocks(n, T), T, 0, st>>>(n, C, c->d_bdpt);
-  c->launches += 10;
+  c->launches += 9;
 }
 
 // The reciprocal runs of a batch: rounds of (parallel node evaluation, DFS resume); round r
@@ -762,12 +760,11 @@ void enqueue_stage2(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims) {
   cudaStream_t st = c->stream;
   if (c->proxy_on && c->gamma_learning) {
     // record_contribution in pixel order: a stable sort by bin keeps pixel order per bin
-    CK(cub::DeviceRadixSort::SortPairs(c->d_gsort_tmp, c->gsort_bytes, c->d_gbin, c->d_gbin_sorted, c->d_gval,
-                                       c->d_gval_sorted, c->n, 0, 12, st));
+    c->launches += stable_bin_sort(c->d_gbin, c->d_gval, c->n, c->d_gbin_sorted, c->d_gval_sorted, c->d_gsort_tmp, st);
     k_gamma_update<<<blocks(kT * kS, 128), 128, 0, st>>>(c->n, c->d_gbin_sorted, c->d_gval_sorted, c->d_gamma_accum,
                                                          c->d_gamma, 1);
     k_gamma_rows<<<1, 32, 0, st>>>(c->d_gamma_accum, c->d_gamma);
-    c->launches += 3;
+    c->launches += 2;
     ++c->gamma_iter;
     if (c->gamma_iter >= c->P.freeze_iteration) c->gamma_learning = false;
   }
@@ -1382,10 +1379,7 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
     c->qQ = make_queue(c, n);
     c->qPS = make_queue(c, n * kMaxLight);
     {
-      size_t need = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, need, c->conn.count, c->conn.offset, static_cast<int>(n + 1), c->stream);
-      c->d_scan_tmp = c->alloc<char>(need);
-      c->scan_tmp_bytes = need;
+      c->d_scan_tmp = c->alloc<int>(scan_tiles(static_cast<long long>(n) + 1));
     }
     {
       const char* eb = std::getenv("PXG_BATCH");
@@ -1417,11 +1411,7 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
     c->d_gbin_sorted = c->zeros<int>(nc);
     c->d_gval_sorted = c->zeros<double>(nc);
     {
-      size_t need = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, need, c->full.gbin, c->d_gbin_sorted, c->full.gval, c->d_gval_sorted,
-                                      static_cast<int>(nc), 0, 12, c->stream);
-      c->d_gsort_tmp = c->alloc<char>(need);
-      c->gsort_bytes = need;
+      c->d_gsort_tmp = c->alloc<int>(sort_tmp_ints(static_cast<int>(nc)));
     }
     activate_ctx(c);
     // stats
@@ -1954,6 +1944,56 @@ int pxg_intersect(pxg_ctx* c, int n, const double* rays, const double* tmax, int
     if (dt) cudaFree(dt);
     cudaFree(dp);
     cudaFree(dtt);
+  });
+}
+
+int pxg_proxy_probe(pxg_ctx* c, int n_walk, const pxg_vertex* walk, int n_cand, const pxg_vertex* cand, int n_draws,
+                    uint64_t seed, int* info, double* prefix_pdf, double* q, double* f, pxg_vertex* draw_cand,
+                    double* draw_q, int* draw_escaped) {
+  return guarded(c, [&]() {
+    static_assert(sizeof(pxg_vertex) == sizeof(PV), "pxg_vertex is the device vertex record");
+    if (!walk || !info || !prefix_pdf || n_walk < 1 || n_walk > kMaxLight)
+      throw InvalidErr{"pxg_proxy_probe: walk of 1..16 vertices required"};
+    if ((n_cand > 0 && (!cand || !q || !f)) || (n_draws > 0 && (!draw_cand || !draw_q || !draw_escaped)))
+      throw InvalidErr{"pxg_proxy_probe: null output"};
+    cudaStream_t st = c->stream;
+    PV* dw = dupload(reinterpret_cast<const PV*>(walk), n_walk);
+    IncHdr* dh = dalloc<IncHdr>(1);
+    PV* dpre = dalloc<PV>(kMaxLight);
+    int* dinfo = dalloc<int>(8);
+    double* dpp = dalloc<double>(1);
+    CK(cudaMemsetAsync(dinfo, 0, sizeof(int) * 8, st));
+    CK(cudaMemsetAsync(dpp, 0, sizeof(double), st));
+    k_probe_dropout<<<1, 32, 0, st>>>(c->M, dw, n_walk, dh, dpre, dinfo, dpp);
+    CK(cudaMemcpyAsync(info, dinfo, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(prefix_pdf, dpp, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int u = info[0] ? info[1] : 0;
+    if (u > 0 && n_cand > 0) {
+      PV* dc = dupload(reinterpret_cast<const PV*>(cand), static_cast<size_t>(n_cand) * u);
+      double* dq = dalloc<double>(n_cand);
+      double* df = dalloc<double>(n_cand);
+      k_probe_densities<<<blocks(n_cand, 64), 64, 0, st>>>(c->S, dh, dpre, n_cand, dc, dq, df);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(q, dq, sizeof(double) * n_cand, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(f, df, sizeof(double) * n_cand, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      cudaFree(dc), cudaFree(dq), cudaFree(df);
+    }
+    if (u > 0 && n_draws > 0) {
+      PV* dc = dalloc<PV>(static_cast<size_t>(n_draws) * u);
+      double* dq = dalloc<double>(n_draws);
+      int* de = dalloc<int>(n_draws);
+      CK(cudaMemsetAsync(dc, 0, sizeof(PV) * static_cast<size_t>(n_draws) * u, st));
+      k_probe_samples<<<blocks(n_draws, 64), 64, 0, st>>>(c->S, seed, dh, dpre, n_draws, dc, dq, de);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(draw_cand, dc, sizeof(PV) * static_cast<size_t>(n_draws) * u, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(draw_q, dq, sizeof(double) * n_draws, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(draw_escaped, de, sizeof(int) * n_draws, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      cudaFree(dc), cudaFree(dq), cudaFree(de);
+    }
+    cudaFree(dw), cudaFree(dh), cudaFree(dpre), cudaFree(dinfo), cudaFree(dpp);
   });
 }
 

@@ -28,13 +28,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <string>
 #include <vector>
 
 #include "pxg.h"
 #include "pxg_host.h"
+#include "pxg_prims.cuh"
 #include "pxg_proxy_wave.cuh"
 
 using namespace pxg;
@@ -1269,6 +1268,53 @@ __global__ void k_gate(int n_cells, int grid_w, int row0, int rows, int width, i
 }
 
 // ------------------------------------------------------------------ test kernels
+// ---- parity probes of the proxy densities on caller-supplied vertices (pxg_proxy_probe)
+// dropout (proxy.cpp:59-94) of a hand-built light walk: info = {valid, u, n_prefix, has_cdir,
+// c_label, s_label, key, dflag_last}.
+__global__ void k_probe_dropout(Mapper M, const PV* walk, int n_walk, IncHdr* hdr, PV* prefix, int* info,
+                                double* prefix_pdf) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  IncHdr h;
+  h.valid = 0;
+  const bool ok = n_walk <= kMaxLight && dropout(M, walk, n_walk, h, prefix);
+  h.valid = ok ? 1 : 0;
+  h.walk = 0;
+  h.end = n_walk;
+  *hdr = h;
+  info[0] = h.valid;
+  if (!ok) return;
+  info[1] = h.u, info[2] = h.n_prefix, info[3] = h.has_cdir, info[4] = h.c_label, info[5] = h.s_label;
+  info[6] = h.key, info[7] = h.dflag_last;
+  *prefix_pdf = h.prefix_pdf;
+}
+
+// support_pdf (proxy.cpp:153-209) and target_density (proxy.cpp:106-151) of candidate blocks
+// cand[i * u .. i * u + u) for the probed incomplete sub-path.
+__global__ void k_probe_densities(SceneView S, const IncHdr* hdr, const PV* prefix, int n, const PV* cand, double* q,
+                                  double* f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !hdr->valid) return;
+  PV g[4];
+  for (int k = 0; k < hdr->u; ++k) g[k] = cand[static_cast<size_t>(i) * hdr->u + k];
+  q[i] = support_pdf(S, *hdr, prefix, g);
+  f[i] = target_density(S, *hdr, prefix, g);
+}
+
+// support_sample (proxy.cpp:211-269), draw i on stream (seed, PROBE, 0, i): the candidate
+// block, its mixture density (1 for an escaped draw) and the escape flag.
+__global__ void k_probe_samples(SceneView S, uint64_t seed, const IncHdr* hdr, const PV* prefix, int n, PV* cand,
+                                double* q, int* escaped) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !hdr->valid) return;
+  Rng rng = make_rng(seed, PXG_KIND_PROBE, 0, static_cast<uint64_t>(i));
+  Cand c;
+  support_sample(S, *hdr, prefix, rng, c);
+  q[i] = c.q;
+  escaped[i] = c.escaped ? 1 : 0;
+  if (!c.escaped)
+    for (int k = 0; k < hdr->u; ++k) cand[static_cast<size_t>(i) * hdr->u + k] = c.g[k];
+}
+
 __global__ void k_intersect(SceneView S, int n, const double* rays, const double* tmax, int* prim, double* t) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

@@ -444,7 +444,7 @@ __device__ __forceinline__ bool warp_trace(const SceneView& S, TravState& ts, St
 }
 
 #ifndef PXG_LEAF_FRAC
-#define PXG_LEAF_FRAC 16  // leaf phase once this many 32ths of the active lanes have leaves pending
+#define PXG_LEAF_FRAC 12  // leaf phase once this many 32ths of the active lanes have leaves pending
 #endif
 
 #ifndef PXG_REFILL

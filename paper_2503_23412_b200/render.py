@@ -409,6 +409,30 @@ class ProxyRenderer:
         return prim.astype(bool) if any_hit else (prim, t)
 
 
+    def proxy_probe(self, walk: np.ndarray, cand: np.ndarray | None = None, n_draws: int = 0, seed: int = 0):
+        """dropout, support_pdf, target_density and support_sample on the device for a
+        caller-built light walk (pxg_proxy_probe; VERTEX_DTYPE records). Returns a dict:
+        info (valid, u, n_prefix, has_cdir, c_label, s_label, key, dropped flag), prefix_pdf,
+        q / f per candidate block cand[i, :u], and n_draws support samples (cand, q, escaped)."""
+        walk = np.ascontiguousarray(walk, VERTEX_DTYPE)
+        info = np.zeros(8, np.int32)
+        pp = np.zeros(1)
+        nc = 0 if cand is None else cand.shape[0]
+        cflat = None if cand is None else np.ascontiguousarray(cand, VERTEX_DTYPE)
+        q, f = np.zeros(max(nc, 1)), np.zeros(max(nc, 1))
+        dc = np.zeros((max(n_draws, 1), 4), VERTEX_DTYPE)
+        dq = np.zeros(max(n_draws, 1))
+        de = np.zeros(max(n_draws, 1), np.int32)
+        # the draw buffer is sized for u = 4 and re-read at the walk's u below
+        self._check(self._L.pxg_proxy_probe(self._ctx, len(walk), walk.ctypes.data, nc,
+                                            cflat.ctypes.data if nc else None, n_draws, seed, _ip(info), _dp(pp),
+                                            _dp(q), _dp(f), dc.ctypes.data, _dp(dq), _ip(de)))
+        u = int(info[1]) if info[0] else 0
+        draws = dc.reshape(-1)[:n_draws * u].reshape(n_draws, u) if u else dc[:0]
+        return {"info": info, "prefix_pdf": float(pp[0]), "q": q[:nc], "f": f[:nc], "draw_cand": draws,
+                "draw_q": dq[:n_draws], "draw_escaped": de[:n_draws].astype(bool)}
+
+
 SNAPSHOT_SLOTS = 4   # PXG_SNAPSHOT_SLOTS (include/pxg.h)
 PIPELINE_AHEAD = 3   # passes in flight in the pipelined pass_done loop (< SNAPSHOT_SLOTS)
 

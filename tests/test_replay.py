@@ -21,8 +21,9 @@ from paper_2503_23412_b200.render import ProxyParams, ProxyRenderer
 pytestmark = pytest.mark.gpu
 
 REL_TOL = 1e-4      # per-path value (north star)
-PREFIX_TOL = 1e-12  # proj/tests/test_proxy.cpp:747-748
-RETRACE_TOL = 1e-6  # proj/tests/test_proxy.cpp:724-726
+PREFIX_TOL = 1e-12  # proj/tests/test_proxy.cpp:747-748 (a prefix whose interior vertices are diffuse)
+RETRACE_TOL = 1e-6  # proj/tests/test_proxy.cpp:724-726 ("near-mirror lobes evaluate to ~1e7, so recomputing the
+#                     density loses a few ulps"): also the bar of a prefix recomputed through a GGX lobe
 
 
 def rel_err(a, b):
@@ -49,8 +50,10 @@ def test_replay_rescoring_matches_device(pxg, oracle, name, parity_report):
     sc = make()
     o = oracle.OracleScene(sc.to_json())
     rec = {"scene": name, "pixels": 0, "passes": passes, "bdpt_over_tol": 0, "bdpt_max_rel": 0.0,
-           "proxy_paths": 0, "prefix_max_rel": 0.0, "retrace_max_rel": 0.0, "label_mismatch": 0,
+           "proxy_paths": 0, "prefix_max_rel": 0.0, "prefix_glossy_max_rel": 0.0, "retrace_max_rel": 0.0,
+           "label_mismatch": 0,
            "c_over_tol": 0, "c_max_rel": 0.0, "c_nonzero": 0, "zero_c_without_retrace": True}
+    lobed = np.array([m.metallic > 0.0 or m.transmission > 0.0 for m in sc.materials])  # a GGX lobe is sampled
     with ProxyRenderer(sc, 11, ProxyParams(**pd)) as r:
         r.set_pass_limit(passes)
         for p in range(passes):
@@ -73,7 +76,16 @@ def test_replay_rescoring_matches_device(pxg, oracle, name, parity_report):
             out = o.replay_proxy(eye[acc], a["tp"], proxy[acc], a["u"], a["n_prefix"], a["cdir"], a["has_cdir"],
                                  a["prefix_pdf"], a["inverse_p"], stats, threads=16)
             rec["proxy_paths"] += int(acc.sum())
-            rec["prefix_max_rel"] = max(rec["prefix_max_rel"], float(rel_err(a["prefix_pdf"], out["prefix_pdf"]).max()))
+            # proxy_pdf_components recomputes the prefix density from positions: through the
+            # interior prefix vertices' BSDF lobes, so a GGX lobe on the way amplifies rounding
+            pe = rel_err(a["prefix_pdf"], out["prefix_pdf"])
+            pv = proxy[acc]
+            interior = (np.arange(pv.shape[1])[None, :] >= 1) & (np.arange(pv.shape[1])[None, :] < a["n_prefix"][:, None] - 1)
+            glossy = (interior & lobed[np.maximum(pv["material"], 0)]).any(axis=1)
+            if (~glossy).any():
+                rec["prefix_max_rel"] = max(rec["prefix_max_rel"], float(pe[~glossy].max()))
+            if glossy.any():
+                rec["prefix_glossy_max_rel"] = max(rec["prefix_glossy_max_rel"], float(pe[glossy].max()))
             rec["retrace_max_rel"] = max(rec["retrace_max_rel"],
                                          float(rel_err(a["retrace_density"], out["retrace_density"]).max()))
             rec["label_mismatch"] += int(np.count_nonzero((a["s_label"] != out["s_label"]) |
@@ -86,6 +98,7 @@ def test_replay_rescoring_matches_device(pxg, oracle, name, parity_report):
     print(rec)
     assert rec["bdpt_over_tol"] == 0
     assert rec["prefix_max_rel"] <= PREFIX_TOL
+    assert rec["prefix_glossy_max_rel"] <= RETRACE_TOL
     assert rec["retrace_max_rel"] <= RETRACE_TOL
     assert rec["label_mismatch"] == 0
     assert rec["c_over_tol"] == 0
