@@ -284,6 +284,7 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
         ev1.record(ts)
         torch.cuda.synchronize()
     stage_ms, counts = r.timing()
+    recip = r.recip_counts()
     if world == 1:
         dev_ms = float(stage_ms[6])  # first pass start -> last pass end on the device, host gaps included
     else:
@@ -328,7 +329,7 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
                                          "counted by an instrumented copy on the same rays",
                     "per_kernel": roof}
     return {"value": value, "dev_ms": dev_ms, "warm": warm, "counts": counts, "stage_ms": stage_ms,
-            "roofline": roofline, "hbm_gb_used": hbm_gb_used}
+            "roofline": roofline, "hbm_gb_used": hbm_gb_used, "recip": recip}
 
 
 def run_ours(args):
@@ -458,6 +459,9 @@ def run_ours(args):
         "e2e": e2e,
         "stage_ms": {"stage1_batches_total": round(float(stage_ms[0]), 3),
                      "recip_rounds_total": round(float(stage_ms[1]), 3)},
+        # reciprocal tree nodes evaluated ahead of the DFS vs consumed by it (whole run so far)
+        "recip_nodes": dict(dev["recip"], evaluated_per_consumed=round(dev["recip"]["evaluated"] /
+                                                                      max(dev["recip"]["consumed"], 1), 3)),
     }
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -292,6 +292,11 @@ int pxg_sincos_2pi(int device, int n, const uint32_t* k, double* s, double* c);
  * counts[0] = kernel launches, counts[1] reserved. t holds 8 doubles. */
 int pxg_read_timing(pxg_ctx* ctx, double* t, long long* counts);
 
+/* Reciprocal estimation work so far (finished runs of every Stage-1 batch enqueued; waits for
+ * Stage 1): out[0] = tree nodes evaluated (draw_g calls made ahead of the DFS, recip.hpp:69-77),
+ * out[1] = tree nodes the runs consumed (ReciprocalRun::cost summed), out[2] = runs. */
+int pxg_read_recip_counts(pxg_ctx* ctx, long long* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -121,6 +121,7 @@ def lib():
     L.pxg_recip_twopoint.argtypes = [C.c_int, C.c_double, C.c_longlong, C.c_uint64, _DP, _LP, _IP]
     L.pxg_rng_draws.argtypes = [C.c_uint64, C.c_uint, C.c_uint, C.c_uint64, C.c_int, C.POINTER(C.c_uint)]
     L.pxg_read_timing.argtypes = [C.c_void_p, _DP, _LP]
+    L.pxg_read_recip_counts.argtypes = [C.c_void_p, _LP]
     L.pxg_sincos_2pi.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint), _DP, _DP]
     _lib = L
     return L
@@ -131,7 +132,7 @@ EXPORTED_SYMBOLS = [
     "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_render_passes_async", "pxg_snapshot_mean", "pxg_read_snapshot",
     "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_accum_to_device_async", "pxg_read_diag",
     "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_dump_paths", "pxg_intersect", "pxg_occluded", "pxg_trace_rays", "pxg_proxy_probe",
-    "pxg_render_pt", "pxg_recip_twopoint", "pxg_rng_draws", "pxg_read_timing", "pxg_sincos_2pi",
+    "pxg_render_pt", "pxg_recip_twopoint", "pxg_rng_draws", "pxg_read_timing", "pxg_read_recip_counts", "pxg_sincos_2pi",
 ]
 
 

@@ -312,6 +312,10 @@ struct pxg_ctx {
   int eval_blocks = 0;        // grid-stride reciprocal node evaluation grid
   int wave_blocks = 0;        // k_recip_eval_wave grid (0: the thread-per-node k_recip_eval)
   PV* d_rw_scratch = nullptr; // candidate vertices of k_recip_eval_wave: [wave_blocks][kRW][4]
+  // global reciprocal wavefront (pxg_recip_queue.cuh): per-node scratch + its ray queues
+  RqView rq{nullptr, nullptr, 0};
+  RayQueue rqA, rqB, rqS;
+  unsigned long long* d_node_stat = nullptr;  // reciprocal tree nodes evaluated / consumed, finished runs
   double* d_rw_ends = nullptr; // its visibility segment endpoints: [wave_blocks][kRW][10][6]
   int dfs_blocks = 0;         // grid-stride warp-DFS grid
   int sel_cap = 0;            // shared-memory capacity (entries) of the pool selection
@@ -662,18 +666,45 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
     k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, bs, c->d_rstate, c->d_ract[0], c->d_rnact,
                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc);
     c->recip_rounds = recip_rounds(st, cap, c->d_rnact, [&](int cur, int chunk) {
-      if (c->wave_blocks > 0)
+      if (c->wave_blocks > 0) {
+        int served = 0;
+        if (c->rq.cap > 0) {
+          // the global wavefront takes the first `served` runs of the list (all of them unless the
+          // round outgrows the scratch); the block-local kernel takes the rest (usually none)
+          served = c->rq.cap / chunk;
+          int* fetch = c->d_trav_next + 1;
+          RayQueue qa = c->rqA, qb = c->rqB;
+          const int gsb = c->gs_blocks;
+          CK(cudaMemsetAsync(qa.count, 0, sizeof(int), st));
+          CK(cudaMemsetAsync(c->rqS.count, 0, sizeof(int), st));
+          k_rq_setup<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, served,
+                                          chunk, c->d_rstate, c->rq, qa);
+          for (int step = 0; step < 4; ++step) {  // support_sample's chain: u <= 4 vertices
+            CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+            launch_trav<false>(c, qa, fetch, st);
+            CK(cudaMemsetAsync(qb.count, 0, sizeof(int), st));
+            k_rq_glue<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
+            std::swap(qa, qb);
+          }
+          k_rq_record<<<gsb, 128, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);
+          CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+          launch_trav<true>(c, c->rqS, fetch, st);
+          k_rq_vis<<<gsb, 256, 0, st>>>(c->rqS, c->rq);
+          k_rq_finish<<<gsb, 128, 0, st>>>(c->seed, R, stride, cap, bs, c->d_rnact + cur, served, chunk, c->rq,
+                                           c->d_rg, c->d_rn, c->d_re);
+          c->launches += 13;
+        }
         k_recip_eval_wave<<<c->wave_blocks, kRW, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur],
                                                           c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn,
-                                                          c->d_re, c->d_rw_scratch, c->d_rw_ends);
-      else
+                                                          c->d_re, c->d_rw_scratch, c->d_rw_ends, served);
+      } else
         k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
             c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
             c->d_rn, c->d_re);
       k_recip_dfs_warp<128><<<c->dfs_blocks, 128, 0, st>>>(R, stride, cap, bs, 0.0, c->d_ract[cur],
                                                     c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
                                                     c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
-                                                    c->d_rnact + (1 - cur), c->d_err);
+                                                    c->d_rnact + (1 - cur), c->d_err, c->d_node_stat);
       c->launches += 2;
     });
     c->launches += 1;
@@ -1520,7 +1551,21 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
         c->wave_blocks = std::max(1, sms * std::max(pw, 1));
         c->d_rw_scratch = c->alloc<PV>(static_cast<size_t>(c->wave_blocks) * kRW * 4);
         c->d_rw_ends = c->alloc<double>(static_cast<size_t>(c->wave_blocks) * kRW * 60);
+        // PXG_RECIP_QUEUE=0: block-local wavefront only (A/B); PXG_RQ_ITEMS: scratch capacity in nodes
+        static const bool queue = !std::getenv("PXG_RECIP_QUEUE") || std::atoi(std::getenv("PXG_RECIP_QUEUE")) != 0;
+        if (queue && c->P.recursion_cap > 0 && NR > 0) {
+          const long long want = std::getenv("PXG_RQ_ITEMS") ? std::atoll(std::getenv("PXG_RQ_ITEMS")) : (4ll << 20);
+          const long long most = static_cast<long long>(NR) * std::min<long long>(c->P.recursion_cap, 16384);
+          const size_t items = static_cast<size_t>(std::max<long long>(1024, std::min(want, most)));
+          c->rq.item = c->alloc<RqItem>(items);
+          c->rq.gv = c->alloc<PV>(items * 4);
+          c->rq.cap = static_cast<int>(items);
+          c->rqA = make_queue(c, items);
+          c->rqB = make_queue(c, items);
+          c->rqS = make_queue(c, items * 10);  // <= 10 visibility segments per node
+        }
       }
+      c->d_node_stat = c->zeros<unsigned long long>(4);
     }
     c->d_diag = c->zeros<long long>(kBuckets * 5);
     c->d_diag_attempt = c->zeros<unsigned long long>(kBuckets);
@@ -2175,6 +2220,18 @@ int pxg_read_timing(pxg_ctx* c, double* t, long long* counts) {
     counts[1] = 0;
   }
   return PXG_OK;
+}
+
+int pxg_read_recip_counts(pxg_ctx* c, long long* out) {
+  return guarded(c, [&]() {
+    if (!out) throw InvalidErr{"pxg_read_recip_counts: null output"};
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (c->d_node_stat) {
+      CK(cudaStreamSynchronize(c->stream1));
+      CK(cudaMemcpy(h, c->d_node_stat, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 3; ++k) out[k] = static_cast<long long>(h[k]);
+  });
 }
 
 }  // extern "C"

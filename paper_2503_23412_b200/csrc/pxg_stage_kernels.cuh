@@ -541,7 +541,7 @@ SceneView S, uint64_t seed, int repeats, int stride,
                                                           long long cap, const __grid_constant__ BatchSet bs,
                                                           const int* active, const int* n_active, int chunk,
                                                           const RunState* st, double* g, long long* nsplit,
-                                                          int* nerr, PV* scratch, double* seg_ends) {
+                                                          int* nerr, PV* scratch, double* seg_ends, int first_run) {
   __shared__ int s_j[kRW], s_k[kRW];
   __shared__ unsigned s_ctr[kRW], s_need[kRW], s_vis[kRW];
   __shared__ unsigned char s_state[kRW], s_strand[kRW], s_step[kRW];
@@ -554,8 +554,9 @@ SceneView S, uint64_t seed, int repeats, int stride,
   PV* gv = scratch + (static_cast<size_t>(blockIdx.x) * kRW + t) * 4;  // this thread's node's candidate
   double* ends_block = seg_ends + static_cast<size_t>(blockIdx.x) * kRW * 60;  // [node][seg][6]
   const long long total = static_cast<long long>(*n_active) * chunk;
-  for (long long base = static_cast<long long>(blockIdx.x) * kRW; base < total;
-       base += static_cast<long long>(gridDim.x) * kRW) {
+  // first_run > 0: the global wavefront (pxg_recip_queue.cuh) took the first runs of the list
+  for (long long base = static_cast<long long>(first_run) * chunk + static_cast<long long>(blockIdx.x) * kRW;
+       base < total; base += static_cast<long long>(gridDim.x) * kRW) {
     // ---- setup + first ray of support_sample (proxy.cpp:211-269)
     const long long tid = base + t;
     int j = -1, k = -1;
@@ -787,6 +788,10 @@ SceneView S, uint64_t seed, int repeats, int stride,
   }
 }
 
+}  // namespace
+#include "pxg_recip_queue.cuh"
+namespace {
+
 // The two-point fixture f = {1, 3}, q = 1/2 (proj/tests/test_recip.cpp:16-23) as Phase A.
 __global__ void k_twopoint_eval(uint64_t seed, double bound, long long cap, const int* active, const int* n_active,
                                 int chunk, const RunState* st, double* g, long long* nsplit, int* nerr) {
@@ -848,7 +853,7 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
                                                         int chunk, RunState* st, const double* g,
                                                         const long long* nsplit, const int* nerr, RecipFrame* frames,
                                                         double* est, long long* cost, int* trunc, int* next,
-                                                        int* n_next, int* err) {
+                                                        int* n_next, int* err, unsigned long long* node_stat = nullptr) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double s_ans[4][W];
   __shared__ long long s_rem[4][W];
@@ -985,6 +990,11 @@ __global__ void __launch_bounds__(128) k_recip_dfs_warp(int repeats, int stride,
       est[j] = s.ret;
       cost[j] = s.cost;
       trunc[j] = s.truncated;
+      if (node_stat) {  // evaluated vs consumed tree nodes of the finished run
+        atomicAdd(node_stat + 0, static_cast<unsigned long long>(s.avail));
+        atomicAdd(node_stat + 1, static_cast<unsigned long long>(s.cost));
+        atomicAdd(node_stat + 2, 1ull);
+      }
     }
   }
   __syncwarp();

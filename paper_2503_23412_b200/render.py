@@ -311,6 +311,13 @@ class ProxyRenderer:
         self._check(self._L.pxg_read_timing(self._ctx, _dp(t), _lp(cnt)))
         return t, cnt
 
+    def recip_counts(self):
+        """Reciprocal tree nodes evaluated ahead of the DFS, nodes the runs consumed, runs
+        (pxg_read_recip_counts): the waste of the round schedule is evaluated / consumed."""
+        out = np.zeros(3, np.int64)
+        self._check(self._L.pxg_read_recip_counts(self._ctx, _lp(out)))
+        return {"evaluated": int(out[0]), "consumed": int(out[1]), "runs": int(out[2])}
+
     def diagnostics(self) -> ProxyDiagnostics:
         rows = np.zeros((N_BUCKETS, 5), np.int64)
         touched = np.zeros(N_BUCKETS, np.int32)
