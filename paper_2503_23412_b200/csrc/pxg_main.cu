@@ -433,14 +433,17 @@ struct HostProbe {
   }
 };
 
+#ifndef PXG_TRAV_HI
+#define PXG_TRAV_HI 8  // resident blocks per SM of the high-occupancy traversal variant (A/B: 10, 12)
+#endif
 // Persistent traversal of queue q (closest hit or any hit) with the context's occupancy variant.
 template <bool kAny>
 void launch_trav(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
   if (c->trav_minb == 8) {
     if (c->trav_post)
-      k_trav_persistent<kAny, 8, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, PXG_TRAV_HI, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
     else
-      k_trav_persistent<kAny, 8, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, PXG_TRAV_HI, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
   } else {
     if (c->trav_post)
       k_trav_persistent<kAny, 6, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
@@ -542,7 +545,9 @@ int recip_rounds(cudaStream_t stream, long long cap, int* nact, Eval&& eval_and_
       std::fprintf(stderr, "[pxg]   round %d: %d runs x %d nodes\n", rounds, count, chunk);
     }
     CK(cudaMemsetAsync(nact + (1 - cur), 0, sizeof(int), stream));
-    eval_and_dfs(cur, chunk);
+    // every active run has the same nodes evaluated so far (`covered`): the last round's chunk
+    // stops at the cap, so no thread or scratch slot is spent on nodes past it
+    eval_and_dfs(cur, static_cast<int>(std::max<long long>(1, std::min<long long>(chunk, cap - covered))));
     cur = 1 - cur;
     covered += chunk;
     chunk = static_cast<int>(std::min<long long>(static_cast<long long>(chunk) * std::max(grow, 1), 16384));
@@ -1533,7 +1538,7 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
       c->trav_post = c->S.nodeq != 0;
       if (const char* e = std::getenv("PXG_TRAV_POSTPONE")) c->trav_post = std::atoi(e) != 0;
       if (c->trav_minb == 8)
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 8, true>, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, PXG_TRAV_HI, true>, 128, 0));
       else
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6, false>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));

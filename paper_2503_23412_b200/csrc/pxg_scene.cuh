@@ -237,7 +237,11 @@ __device__ __forceinline__ void ldg256(const void* p, float4& a, float4& b) {
 // 0x4B0000bb = 2^23 + b and one exact FADD removes 2^23 (two full-rate instructions instead
 // of the quarter-rate I2F.U8).
 __device__ __forceinline__ float qbyte(unsigned w, int k) {
-#if PXG_QCVT
+#if PXG_QCVT == 2
+  // byte k in mantissa bits 8-15 of 1.0f: 1 + q * 2^-15 exactly, one byte permute and no
+  // conversion; node4q_test folds the offset into its slopes (A * 2^15, B - A * 2^15)
+  return __uint_as_float(__byte_perm(w, 0x3F800000u, 0x7604u | (static_cast<unsigned>(k) << 4)));
+#elif PXG_QCVT
   return __uint_as_float(__byte_perm(w, 0x4B000000u, static_cast<unsigned>(k) | 0x7540u)) - 8388608.0f;
 #else
   return static_cast<float>((w >> (8 * k)) & 0xffu);
@@ -265,8 +269,16 @@ __device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, c
   const unsigned ex = __float_as_uint(a.w);
   const float sx = __uint_as_float((ex & 0xffu) << 23), sy = __uint_as_float(((ex >> 8) & 0xffu) << 23),
               sz = __uint_as_float(((ex >> 16) & 0xffu) << 23);
+#if PXG_QCVT == 2
+  // q * A + B = (1 + q 2^-15) * (A 2^15) + (B - A 2^15); the second term's rounding moves a
+  // plane by at most 1/512 of a grid step, inside the boxes' padding (pxg_host.cpp)
+  const float Ax = sx * rf.ix * 32768.0f, Ay = sy * rf.iy * 32768.0f, Az = sz * rf.iz * 32768.0f;
+  const float Bx = __fmaf_rn(a.x, rf.ix, rf.nx) - Ax, By = __fmaf_rn(a.y, rf.iy, rf.ny) - Ay,
+              Bz = __fmaf_rn(a.z, rf.iz, rf.nz) - Az;
+#else
   const float Ax = sx * rf.ix, Ay = sy * rf.iy, Az = sz * rf.iz;
   const float Bx = __fmaf_rn(a.x, rf.ix, rf.nx), By = __fmaf_rn(a.y, rf.iy, rf.ny), Bz = __fmaf_rn(a.z, rf.iz, rf.nz);
+#endif
   const unsigned lxw = __float_as_uint(c.x), lyw = __float_as_uint(c.y), lzw = __float_as_uint(c.z);
   const unsigned hxw = __float_as_uint(c.w), hyw = __float_as_uint(d.x), hzw = __float_as_uint(d.y);
   Node4Hits r;
