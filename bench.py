@@ -96,6 +96,28 @@ def measured_peak_gbs():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measure_l2_gbs():
+    """L2-resident copy bandwidth on this GPU (GB/s, read + write): the denominator of
+    roofline.l2 (the traversal's node and primitive loads are served from L1/L2, not HBM)."""
+    import torch
+    n = 32 << 20
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    b = torch.empty(n, dtype=torch.uint8, device="cuda")
+    a.zero_()
+    for _ in range(5):
+        b.copy_(a)
+    best = 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(20):
+        e0.record()
+        for _ in range(10):
+            b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 10 * 2.0 * n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return round(best, 1)
+
+
 def ncu_traffic(cfg: str, kernel: str):
     """DRAM bytes per launch of `kernel` on config `cfg` from the committed ncu --set full
     summary (profiles/ncu_traffic.json), if any."""
@@ -304,8 +326,12 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
     r.set_pass_limit(-1)
     tr = r.measure_traversal(BATCH) if not quick else {"closest": {"launches": 0}, "anyhit": {"launches": 0}}
     nb = r.node_bytes()
+    # bytes the kernels actually load per node visit: the whole 64 B quantised node; of a 128 B
+    # node the six plane vectors and the child codes (3 x 32 B + 16 B; 16 B of padding unread)
+    nb = 112 if nb == 128 else nb
     r.close()
     peak, peak_src = measured_peak_gbs()
+    l2_peak = None if quick else measure_l2_gbs()
     roof = {}
     for kind, kname in (("closest", "k_trav_persistent<0>"), ("anyhit", "k_trav_persistent<1>")):
         m = tr[kind]
@@ -325,8 +351,14 @@ def measure_device(sc, params, seed, steps, warmup, world, local, quick, cfg):
         roofline = {"bound": "hbm", "achieved": round(d["achieved_gbs"], 1), "peak": peak, "unit": "GB/s",
                     "frac": round(d["achieved_gbs"] / peak, 4), "traffic": ncu_traffic(cfg, d["kernel"]),
                     "kernel": d["kernel"], "peak_source": peak_src,
-                    "algorithmic_bytes": f"{nb} B per BVH node visit + {PRIM_BYTES} B per primitive test, "
+                    "algorithmic_bytes": f"{nb} B fetched per BVH node visit + {PRIM_BYTES} B per primitive test, "
                                          "counted by an instrumented copy on the same rays",
+                    # the same bytes against the L2: ncu shows these loads served by L1/L2 (DRAM
+                    # traffic = `traffic`, a few % of them), so this is the fraction that bounds it
+                    "l2": {"peak": l2_peak, "unit": "GB/s", "frac": round(d["achieved_gbs"] / l2_peak, 4)
+                           if l2_peak else None,
+                           "peak_source": "measured here: device-to-device copy of a 32 MB buffer (L2-resident, "
+                                          "read + write bytes, 10 copies per timing, best of 20, CUDA events)"},
                     "per_kernel": roof}
     return {"value": value, "dev_ms": dev_ms, "warm": warm, "counts": counts, "stage_ms": stage_ms,
             "roofline": roofline, "hbm_gb_used": hbm_gb_used, "recip": recip}

@@ -86,16 +86,25 @@ def test_restated_loop_deterministic_across_threads(oracle):
 
 
 def test_restated_loop_agrees_with_reference_in_distribution(oracle):
-    """The two documented stream deviations change trajectories, not the estimator: the
-    restated loop and the unmodified reference render_proxy_bdpt agree within noise (mean
-    over independent seeds; the caustic estimator is heavy-tailed, proj/tests/test_proxy.cpp:1125-1131)."""
+    """The documented stream deviations change trajectories, not the estimator: 48 renders of
+    64 spp by the restated loop (Philox, re-keyed streams) and 48 by the unmodified reference
+    render_proxy_bdpt (PCG32 as shipped) are one distribution: medians of the mean image luminance within 10%
+    (3.5 standard errors; round 1 accepted a flat 20% on the mean of 4 renders) and a
+    Mann-Whitney U test; the caustic estimator is heavy-tailed
+    (proj/tests/test_proxy.cpp:1125-1131), which rank statistics do not mind."""
+    from scipy.stats import mannwhitneyu
     sc = scenes.caustic_box(8)
     o = oracle.OracleScene(sc.to_json())
+    opcg = oracle.OracleScene(sc.to_json(), variant="pcg")
     p = {"pretrace_paths": 2000, "light_walks": 3000}
     lum = np.array([0.2126, 0.7152, 0.0722])
-    a = np.mean([(o.render(48, 10 + s, params=p, threads=8)[0] @ lum).mean() for s in range(4)])
-    b = np.mean([(o.render_proxy_ref(48, 20 + s, params=p)[0] @ lum).mean() for s in range(4)])
-    assert abs(a - b) / b < 0.2
+    n = 48
+    a = np.array([(o.render(64, 100 + s, params=p, threads=8)[0] @ lum).mean() for s in range(n)])
+    b = (opcg.render_proxy_ref_mt(64, 200, n, p, all_images=True) @ lum).mean(axis=(1, 2))
+    # the estimator is heavy-tailed (single rare samples move a render's mean by 10x its spread), so
+    # the comparison is on robust statistics: medians (standard error ~2% each) and rank sums
+    assert abs(np.median(a) / np.median(b) - 1.0) <= 0.10, (np.median(a), np.median(b))
+    assert mannwhitneyu(a, b).pvalue > 0.005
 
 
 def test_recip_two_point_closed_forms(oracle):
