@@ -101,16 +101,20 @@ constexpr int kBatchSetMax = 32;  // passes per Stage-1 batch, at most
 // keys / vals + b * cap, counted in count[b].
 __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L, uint64_t seed, int pass0,
                             int walk_begin, unsigned long long* keys, unsigned* vals, int* count, int cap) {
+  const unsigned FULL = 0xffffffffu;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = L * n_walks;
-  if (i >= total) return;
-  const int b = i / n_walks;
+  const bool live = i < total;
+  const int b = live ? i / n_walks : -1;
   const int pass = pass0 + b;
-  const int w = walk_begin + i % n_walks;
-  keys += static_cast<size_t>(b) * cap;
-  vals += static_cast<size_t>(b) * cap;
-  count += b;
-  const int n = wnv[i];
+  const int w = live ? walk_begin + i % n_walks : 0;
+  const int n = live ? wnv[i] : 0;
+  // the warp walks to its longest sub-path together so that the candidate slots of an iteration
+  // are taken with ONE atomic per (warp, pass) instead of one per candidate: the per-pass
+  // counters are single addresses that every eligible prefix of 2M walks used to hit
+  int nmax = n;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, d));
   // dropout eligibility (proxy.cpp:59-94) of every prefix end in one forward pass, in registers: the trailing
   // specular run length u, the running pdf product (the same left-to-right product the
   // reference forms for each end) and sliding windows of the last prefix products and
@@ -118,32 +122,44 @@ __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L,
   double P = 1.0, Pw[5] = {1.0, 1.0, 1.0, 1.0, 1.0};  // Pw[m] = product of pdf[0 .. k-m-1]
   int Ew[6] = {-1, -1, -1, -1, -1, -1};                 // Ew[m] = emitter[k-m]
   int flag0 = -1, run = 0;
-  for (int k = 0; k < n; ++k) {
-    const PV& v = wpool[static_cast<size_t>(k) * total + i];
-    const int fk = v.flag;
+  for (int k = 0; k < nmax; ++k) {
+    bool elig = false;
+    if (k < n) {
+      const PV& v = wpool[static_cast<size_t>(k) * total + i];
+      const int fk = v.flag;
 #pragma unroll
-    for (int m = 4; m > 0; --m) Pw[m] = Pw[m - 1];
-    Pw[0] = P;
+      for (int m = 4; m > 0; --m) Pw[m] = Pw[m - 1];
+      Pw[0] = P;
 #pragma unroll
-    for (int m = 5; m > 0; --m) Ew[m] = Ew[m - 1];
-    Ew[0] = v.emitter;
-    if (k == 0) flag0 = fk;
-    run = fk == kSpecular ? run + 1 : 0;
-    P *= v.pdf_fwd;
-    const int end = k + 1;
-    if (end < 2 || fk != kSpecular || run > 4 || run >= end) continue;
-    const int u = run, terminal = k - u;
-    const int em = u == 1 ? Ew[2] : u == 2 ? Ew[3] : u == 3 ? Ew[4] : Ew[5];  // emitter[terminal - 1]
-    const double pp = u == 1 ? Pw[1] : u == 2 ? Pw[2] : u == 3 ? Pw[3] : Pw[4];  // product of pdf[0 .. terminal-1]
-    if (terminal > 0 ? em < 0 : flag0 != kLight) continue;
-    if (!(pp > 0.0)) continue;
-    Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
-    unsigned long long hi = pxg_next_u32(&kr.r);
-    unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
-    int slot = atomicAdd(count, 1);
+      for (int m = 5; m > 0; --m) Ew[m] = Ew[m - 1];
+      Ew[0] = v.emitter;
+      if (k == 0) flag0 = fk;
+      run = fk == kSpecular ? run + 1 : 0;
+      P *= v.pdf_fwd;
+      const int end = k + 1;
+      if (!(end < 2 || fk != kSpecular || run > 4 || run >= end)) {
+        const int u = run, terminal = k - u;
+        const int em = u == 1 ? Ew[2] : u == 2 ? Ew[3] : u == 3 ? Ew[4] : Ew[5];  // emitter[terminal - 1]
+        const double pp = u == 1 ? Pw[1] : u == 2 ? Pw[2] : u == 3 ? Pw[3] : Pw[4];  // product of pdf[0 .. terminal-1]
+        elig = (terminal > 0 ? em >= 0 : flag0 == kLight) && pp > 0.0;
+      }
+    }
+    // lanes of one pass share an atomic (a warp straddles a pass boundary at most once per pass)
+    const unsigned peers = __match_any_sync(FULL, elig ? b : -1);
+    if (!elig) continue;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count + b, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const int slot = base + __popc(peers & ((1u << lane) - 1u));
     if (slot < cap) {
-      keys[slot] = key;
-      vals[slot] = (static_cast<unsigned>(w) << 5) | static_cast<unsigned>(end);
+      const int end = k + 1;
+      Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
+      unsigned long long hi = pxg_next_u32(&kr.r);
+      unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
+      keys[static_cast<size_t>(b) * cap + slot] = key;
+      vals[static_cast<size_t>(b) * cap + slot] = (static_cast<unsigned>(w) << 5) | static_cast<unsigned>(end);
     }
   }
 }
