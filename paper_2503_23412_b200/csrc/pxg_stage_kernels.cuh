@@ -109,58 +109,63 @@ __global__ void k_pool_keys(const PV* wpool, const int* wnv, int n_walks, int L,
   const int pass = pass0 + b;
   const int w = live ? walk_begin + i % n_walks : 0;
   const int n = live ? wnv[i] : 0;
-  // the warp walks to its longest sub-path together so that the candidate slots of an iteration
-  // are taken with ONE atomic per (warp, pass) instead of one per candidate: the per-pass
-  // counters are single addresses that every eligible prefix of 2M walks used to hit
-  int nmax = n;
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, d));
   // dropout eligibility (proxy.cpp:59-94) of every prefix end in one forward pass, in registers: the trailing
   // specular run length u, the running pdf product (the same left-to-right product the
   // reference forms for each end) and sliding windows of the last prefix products and
-  // emitter ids, enough for u <= 4 (proxy.cpp:59-94).
+  // emitter ids, enough for u <= 4 (proxy.cpp:59-94). The eligible ends are only recorded
+  // (bit `end` of emask): the per-pass candidate counters are single addresses, and an atomic
+  // per candidate inside this loop put its round trip on every iteration's critical path
+  // (ncu: 42% of the stall samples waited for it).
   double P = 1.0, Pw[5] = {1.0, 1.0, 1.0, 1.0, 1.0};  // Pw[m] = product of pdf[0 .. k-m-1]
   int Ew[6] = {-1, -1, -1, -1, -1, -1};                 // Ew[m] = emitter[k-m]
   int flag0 = -1, run = 0;
-  for (int k = 0; k < nmax; ++k) {
-    bool elig = false;
-    if (k < n) {
-      const PV& v = wpool[static_cast<size_t>(k) * total + i];
-      const int fk = v.flag;
+  unsigned emask = 0u;
+  for (int k = 0; k < n; ++k) {
+    const PV& v = wpool[static_cast<size_t>(k) * total + i];
+    const int fk = v.flag;
 #pragma unroll
-      for (int m = 4; m > 0; --m) Pw[m] = Pw[m - 1];
-      Pw[0] = P;
+    for (int m = 4; m > 0; --m) Pw[m] = Pw[m - 1];
+    Pw[0] = P;
 #pragma unroll
-      for (int m = 5; m > 0; --m) Ew[m] = Ew[m - 1];
-      Ew[0] = v.emitter;
-      if (k == 0) flag0 = fk;
-      run = fk == kSpecular ? run + 1 : 0;
-      P *= v.pdf_fwd;
-      const int end = k + 1;
-      if (!(end < 2 || fk != kSpecular || run > 4 || run >= end)) {
-        const int u = run, terminal = k - u;
-        const int em = u == 1 ? Ew[2] : u == 2 ? Ew[3] : u == 3 ? Ew[4] : Ew[5];  // emitter[terminal - 1]
-        const double pp = u == 1 ? Pw[1] : u == 2 ? Pw[2] : u == 3 ? Pw[3] : Pw[4];  // product of pdf[0 .. terminal-1]
-        elig = (terminal > 0 ? em >= 0 : flag0 == kLight) && pp > 0.0;
-      }
+    for (int m = 5; m > 0; --m) Ew[m] = Ew[m - 1];
+    Ew[0] = v.emitter;
+    if (k == 0) flag0 = fk;
+    run = fk == kSpecular ? run + 1 : 0;
+    P *= v.pdf_fwd;
+    const int end = k + 1;
+    if (end < 2 || fk != kSpecular || run > 4 || run >= end) continue;
+    const int u = run, terminal = k - u;
+    const int em = u == 1 ? Ew[2] : u == 2 ? Ew[3] : u == 3 ? Ew[4] : Ew[5];  // emitter[terminal - 1]
+    const double pp = u == 1 ? Pw[1] : u == 2 ? Pw[2] : u == 3 ? Pw[3] : Pw[4];  // product of pdf[0 .. terminal-1]
+    if ((terminal > 0 ? em >= 0 : flag0 == kLight) && pp > 0.0) emask |= 1u << end;
+  }
+  // one atomic per (warp, pass): the lanes of a pass take consecutive slots (a warp straddles a
+  // pass boundary at most once per pass, hence the grouping by pass)
+  const int lane = threadIdx.x & 31;
+  const int cnt = __popc(emask);
+  const unsigned peers = __match_any_sync(FULL, b);
+  int before = 0, group = 0;  // candidates of lower lanes of this lane's group / of the whole group
+#pragma unroll
+  for (int l = 0; l < 32; ++l) {
+    const int c = __shfl_sync(FULL, cnt, l);
+    if (peers >> l & 1u) {
+      group += c;
+      if (l < lane) before += c;
     }
-    // lanes of one pass share an atomic (a warp straddles a pass boundary at most once per pass)
-    const unsigned peers = __match_any_sync(FULL, elig ? b : -1);
-    if (!elig) continue;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(count + b, __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    const int slot = base + __popc(peers & ((1u << lane) - 1u));
-    if (slot < cap) {
-      const int end = k + 1;
-      Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
-      unsigned long long hi = pxg_next_u32(&kr.r);
-      unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
-      keys[static_cast<size_t>(b) * cap + slot] = key;
-      vals[static_cast<size_t>(b) * cap + slot] = (static_cast<unsigned>(w) << 5) | static_cast<unsigned>(end);
-    }
+  }
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (live && lane == leader && group > 0) base = atomicAdd(count + b, group);
+  base = __shfl_sync(FULL, base, leader);
+  int slot = base + before;
+  for (unsigned m = emask; m; m &= m - 1, ++slot) {
+    if (slot >= cap) break;
+    const int end = __ffs(m) - 1;
+    Rng kr = make_rng(seed, PXG_KIND_RESERVOIR, static_cast<uint32_t>(end), unit_stream(pass, w));
+    unsigned long long hi = pxg_next_u32(&kr.r);
+    unsigned long long key = (hi << 32) | pxg_next_u32(&kr.r);
+    keys[static_cast<size_t>(b) * cap + slot] = key;
+    vals[static_cast<size_t>(b) * cap + slot] = (static_cast<unsigned>(w) << 5) | static_cast<unsigned>(end);
   }
 }
 
