@@ -454,3 +454,35 @@ def test_stage2_row_tiles_equal_untiled(pxg, monkeypatch):
         assert np.array_equal(runs[tiles][1], base[1])
         for a, b in zip(runs[tiles][2], base[2]):
             assert np.array_equal(a, b)
+
+
+def test_recip_wavefront_overflow_path_equals_default(pxg, monkeypatch):
+    """The reciprocal node wavefront's scratch holds a bounded number of tree nodes per round
+    (pxg_recip_queue.cuh); a round's nodes beyond it are evaluated by the block-local kernel.
+    With the scratch cut to 2,048 / 20,000 nodes (most of every late round overflows, and the
+    split point lands inside a round) the estimates, the pool and the passes are bitwise those
+    of the default capacity."""
+    sc = scenes.caustic_box(24)
+    pd = ProxyParams(pretrace_paths=4000, light_walks=4000)
+    runs = {}
+    for items in (None, "2048", "20000"):
+        if items:
+            monkeypatch.setenv("PXG_RQ_ITEMS", items)
+        else:
+            monkeypatch.delenv("PXG_RQ_ITEMS", raising=False)
+        with ProxyRenderer(sc, 6, pd) as r:
+            vals, pools = [], []
+            for _ in range(3):
+                r.render_passes(1)
+                vals.append(r.dump_pass()[0])
+                p = r.dump_pool()
+                pools.append((p["walk"].copy(), p["end"].copy(), p["inv_p"].copy(), p["inv_p_m2"].copy()))
+            runs[items] = (np.stack(vals), pools, r.recip_counts())
+    base = runs[None]
+    assert base[2]["consumed"] > 0 and base[2]["evaluated"] >= base[2]["consumed"]
+    for items in ("2048", "20000"):
+        assert np.array_equal(runs[items][0], base[0])
+        for a, b in zip(runs[items][1], base[1]):
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y)
+        assert runs[items][2] == base[2]
