@@ -379,6 +379,27 @@ struct LocalStack {
   __device__ __forceinline__ int pop(int& sp) { return a[--sp]; }
 };
 
+// LocalStack with the top entry in a register: a pop returns the register and issues the load
+// of the entry below, which is consumed only by the NEXT pop, so the local-memory latency is
+// off the node chain (ncu: 8% of the traversal's stall samples waited for the popped child).
+// Entry i < sp - 1 lives at a[i], entry sp - 1 in tos.
+struct TosStack {
+  int* a;
+  int tos;
+  __device__ __forceinline__ void push(int& sp, int v) {
+    if (sp >= kStack) return;
+    if (sp > 0) a[sp - 1] = tos;
+    tos = v;
+    ++sp;
+  }
+  __device__ __forceinline__ int pop(int& sp) {
+    const int r = tos;
+    --sp;
+    if (sp > 0) tos = a[sp - 1];
+    return r;
+  }
+};
+
 template <int kS>
 struct SplitStack {
   int* sm;   // this thread's column of the block's shared stack (stride 128)

@@ -450,6 +450,9 @@ __device__ __forceinline__ bool warp_trace(const SceneView& S, TravState& ts, St
 #ifndef PXG_REFILL
 #define PXG_REFILL 4
 #endif
+#ifndef PXG_TOS
+#define PXG_TOS 0  // top of the traversal stack in a register (TosStack)
+#endif
 #ifndef PXG_SSTACK
 #define PXG_SSTACK 0  // shared-memory entries of the persistent kernels' traversal stack (0: all local)
 #endif
@@ -472,6 +475,9 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
   __shared__ int s_stack[PXG_SSTACK * 128];
   int stack_loc[kStack - PXG_SSTACK];
   SplitStack<PXG_SSTACK> stack{s_stack + threadIdx.x, stack_loc};
+#elif PXG_TOS
+  int stack_mem[kStack];
+  TosStack stack{stack_mem, 0};
 #else
   int stack_mem[kStack];
   LocalStack stack{stack_mem};
