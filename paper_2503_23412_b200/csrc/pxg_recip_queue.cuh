@@ -23,6 +23,10 @@
 // block-local kernel (same values), so no configuration can overflow it.
 #pragma once
 
+#ifndef PXG_RQ_MINB
+#define PXG_RQ_MINB 8  // resident 128-thread blocks per SM of the glue kernels (64 registers; C2 +1%, C4 neutral vs unbounded)
+#endif
+
 namespace {
 
 struct RqItem {  // 48 B per pending node
@@ -52,7 +56,7 @@ __device__ __forceinline__ void rq_push(const RayQueue& Q, int tag, const V3& o,
   Q.path[slot] = tag;
 }
 
-__global__ void __launch_bounds__(128) k_rq_setup(SceneView S, uint64_t seed, int repeats, int stride, long long cap,
+__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_setup(SceneView S, uint64_t seed, int repeats, int stride, long long cap,
                                                   const __grid_constant__ BatchSet bs, const int* active,
                                                   const int* n_active, int served, int chunk, const RunState* st,
                                                   RqView R, RayQueue Q) {
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(128) k_rq_setup(SceneView S, uint64_t seed, in
 
 // After a closest-hit round: the hit becomes the next candidate vertex; a from-specular chain
 // (strand 0) with vertices left samples its next direction and pushes the next ray.
-__global__ void __launch_bounds__(128) k_rq_glue(SceneView S, uint64_t seed, int repeats, int stride,
+__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_glue(SceneView S, uint64_t seed, int repeats, int stride,
                                                  const __grid_constant__ BatchSet bs, RqView R, RayQueue in,
                                                  RayQueue out) {
   const int n = *in.count;
@@ -193,7 +197,7 @@ struct VisPush {
   }
 };
 
-__global__ void __launch_bounds__(128) k_rq_record(SceneView S, int repeats, int stride,
+__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_record(SceneView S, int repeats, int stride,
                                                    const __grid_constant__ BatchSet bs, const int* n_active,
                                                    int served, int chunk, RqView R, RayQueue Q) {
   const long long total = rq_total(n_active, served, chunk);
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(256) k_rq_vis(RayQueue Q, RqView R) {
   }
 }
 
-__global__ void __launch_bounds__(128) k_rq_finish(uint64_t seed, int repeats, int stride, long long cap,
+__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_finish(uint64_t seed, int repeats, int stride, long long cap,
                                                    const __grid_constant__ BatchSet bs, const int* n_active,
                                                    int served, int chunk, RqView R, double* g, long long* nsplit,
                                                    int* nerr) {
