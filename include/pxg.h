@@ -251,6 +251,16 @@ int pxg_proxy_probe(pxg_ctx* ctx, int n_walk, const pxg_vertex* walk, int n_cand
                     uint64_t seed, int* info, double* prefix_pdf, double* q, double* f, pxg_vertex* draw_cand,
                     double* draw_q, int* draw_escaped);
 
+/* Reciprocal estimation of the probed incomplete sub-path on the device, through the
+ * production node wavefront and DFS (estimate_reciprocal, proj/include/proxima/recip.hpp:131-138,
+ * with the proxy integrand of estimate_inverse_p, proj/src/proxy.cpp:397-409) at the given
+ * bound: n_runs independent runs (run i on the node streams of (pass 0x700000 + i / 255, run
+ * i % 255)), est[i] an unbiased estimate of 1 / integral(target_density) when not truncated.
+ * The device-level analogue of proj/tests/test_proxy.cpp:620-673. Call between passes only
+ * (it uses the context's reciprocal run buffers; the call synchronises the device). */
+int pxg_proxy_recip(pxg_ctx* ctx, int n_walk, const pxg_vertex* walk, double bound, int n_runs, double* est,
+                    long long* cost, int* truncated);
+
 /* Parity of the traversal kernels that ship: the same rays as pxg_intersect (any_hit = 0:
  * rays[n*6] origin + unit direction, tmax may be NULL) or pxg_occluded (any_hit = 1:
  * segments[n*6] from + to, prim[i] = 1 when occluded, t unused) through

@@ -116,6 +116,7 @@ def lib():
     L.pxg_trace_rays.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _DP, _DP, _IP, _DP]
     L.pxg_proxy_probe.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_uint64, _IP, _DP,
                                   _DP, _DP, C.c_void_p, _DP, _IP]
+    L.pxg_proxy_recip.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_int, _DP, _LP, _IP]
     L.pxg_node_bytes.argtypes = [C.c_void_p]
     L.pxg_render_pt.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int, _DP]
     L.pxg_recip_twopoint.argtypes = [C.c_int, C.c_double, C.c_longlong, C.c_uint64, _DP, _LP, _IP]
@@ -131,7 +132,7 @@ EXPORTED_SYMBOLS = [
     "pxg_default_params", "pxg_abi_version", "pxg_node_bytes", "pxg_device_count", "pxg_create", "pxg_scene_create", "pxg_scene_destroy", "pxg_scene_device_bytes", "pxg_create_from_scene", "pxg_destroy", "pxg_last_error",
     "pxg_render_pass", "pxg_render_passes", "pxg_render_pass_traced", "pxg_set_pass_limit", "pxg_render_passes_async", "pxg_snapshot_mean", "pxg_read_snapshot",
     "pxg_measure_traversal", "pxg_synchronize", "pxg_read_mean", "pxg_read_accum", "pxg_accum_to_device", "pxg_accum_to_device_async", "pxg_read_diag",
-    "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_dump_paths", "pxg_intersect", "pxg_occluded", "pxg_trace_rays", "pxg_proxy_probe",
+    "pxg_read_stats", "pxg_dump_pass", "pxg_dump_prims", "pxg_dump_pool", "pxg_dump_paths", "pxg_intersect", "pxg_occluded", "pxg_trace_rays", "pxg_proxy_probe", "pxg_proxy_recip",
     "pxg_render_pt", "pxg_recip_twopoint", "pxg_rng_draws", "pxg_read_timing", "pxg_read_recip_counts", "pxg_sincos_2pi",
 ]
 

@@ -647,6 +647,52 @@ void stage1_fronts(pxg_ctx* c, int p0, int L) {
   hp.mark("entries+bounds");
 }
 
+// One reciprocal round on stream `st`: evaluate nodes [avail, avail + chunk) of every active
+// run (global wavefront, its overflow and the thread-per-node variant), then resume the DFS.
+void recip_round(pxg_ctx* c, cudaStream_t st, const BatchSet& bs, int R, int stride, long long cap, int cur,
+                 int chunk) {
+  if (c->wave_blocks > 0) {
+    int served = 0;
+    if (c->rq.cap > 0) {
+      // the global wavefront takes the first `served` runs of the list (all of them unless the
+      // round outgrows the scratch); the block-local kernel takes the rest (usually none)
+      served = c->rq.cap / chunk;
+      int* fetch = c->d_trav_next + 1;
+      RayQueue qa = c->rqA, qb = c->rqB;
+      const int gsb = c->gs_blocks;
+      CK(cudaMemsetAsync(qa.count, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(c->rqS.count, 0, sizeof(int), st));
+      k_rq_setup<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, served,
+                                      chunk, c->d_rstate, c->rq, qa);
+      for (int step = 0; step < 4; ++step) {  // support_sample's chain: u <= 4 vertices
+        CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+        launch_trav<false>(c, qa, fetch, st);
+        CK(cudaMemsetAsync(qb.count, 0, sizeof(int), st));
+        k_rq_glue<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
+        std::swap(qa, qb);
+      }
+      k_rq_record<<<gsb, 128, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);
+      CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
+      launch_trav<true>(c, c->rqS, fetch, st);
+      k_rq_vis<<<gsb, 256, 0, st>>>(c->rqS, c->rq);
+      k_rq_finish<<<gsb, 128, 0, st>>>(c->seed, R, stride, cap, bs, c->d_rnact + cur, served, chunk, c->rq,
+                                       c->d_rg, c->d_rn, c->d_re);
+      c->launches += 13;
+    }
+    k_recip_eval_wave<<<c->wave_blocks, kRW, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur],
+                                                      c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn,
+                                                      c->d_re, c->d_rw_scratch, c->d_rw_ends, served);
+  } else
+    k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
+        c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
+        c->d_rn, c->d_re);
+  k_recip_dfs_warp<128><<<c->dfs_blocks, 128, 0, st>>>(R, stride, cap, bs, 0.0, c->d_ract[cur],
+                                                c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
+                                                c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
+                                                c->d_rnact + (1 - cur), c->d_err, c->d_node_stat);
+  c->launches += 2;
+}
+
 // Stage 1 of passes [p0, p0 + L): the fronts in pass order, ONE set of reciprocal rounds
 // for all L x budget x repeats runs (the long-run tail is paid once per batch), then the
 // finishes in pass order (bucket estimate sums are sequential across passes).
@@ -671,46 +717,7 @@ void run_stage1_batch(pxg_ctx* c, int p0, int L) {
     k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, stride, bs, c->d_rstate, c->d_ract[0], c->d_rnact,
                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc);
     c->recip_rounds = recip_rounds(st, cap, c->d_rnact, [&](int cur, int chunk) {
-      if (c->wave_blocks > 0) {
-        int served = 0;
-        if (c->rq.cap > 0) {
-          // the global wavefront takes the first `served` runs of the list (all of them unless the
-          // round outgrows the scratch); the block-local kernel takes the rest (usually none)
-          served = c->rq.cap / chunk;
-          int* fetch = c->d_trav_next + 1;
-          RayQueue qa = c->rqA, qb = c->rqB;
-          const int gsb = c->gs_blocks;
-          CK(cudaMemsetAsync(qa.count, 0, sizeof(int), st));
-          CK(cudaMemsetAsync(c->rqS.count, 0, sizeof(int), st));
-          k_rq_setup<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, served,
-                                          chunk, c->d_rstate, c->rq, qa);
-          for (int step = 0; step < 4; ++step) {  // support_sample's chain: u <= 4 vertices
-            CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
-            launch_trav<false>(c, qa, fetch, st);
-            CK(cudaMemsetAsync(qb.count, 0, sizeof(int), st));
-            k_rq_glue<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
-            std::swap(qa, qb);
-          }
-          k_rq_record<<<gsb, 128, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);
-          CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
-          launch_trav<true>(c, c->rqS, fetch, st);
-          k_rq_vis<<<gsb, 256, 0, st>>>(c->rqS, c->rq);
-          k_rq_finish<<<gsb, 128, 0, st>>>(c->seed, R, stride, cap, bs, c->d_rnact + cur, served, chunk, c->rq,
-                                           c->d_rg, c->d_rn, c->d_re);
-          c->launches += 13;
-        }
-        k_recip_eval_wave<<<c->wave_blocks, kRW, 0, st>>>(c->S, c->seed, R, stride, cap, bs, c->d_ract[cur],
-                                                          c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn,
-                                                          c->d_re, c->d_rw_scratch, c->d_rw_ends, served);
-      } else
-        k_recip_eval<<<c->eval_blocks, 64, 0, st>>>(
-            c->S, c->seed, R, stride, cap, bs, c->d_ract[cur], c->d_rnact + cur, chunk, c->d_rstate, c->d_rg,
-            c->d_rn, c->d_re);
-      k_recip_dfs_warp<128><<<c->dfs_blocks, 128, 0, st>>>(R, stride, cap, bs, 0.0, c->d_ract[cur],
-                                                    c->d_rnact + cur, chunk, c->d_rstate, c->d_rg, c->d_rn, c->d_re, c->d_frames,
-                                                    c->d_run_est, c->d_run_cost, c->d_run_trunc, c->d_ract[1 - cur],
-                                                    c->d_rnact + (1 - cur), c->d_err, c->d_node_stat);
-      c->launches += 2;
+      recip_round(c, st, bs, R, stride, cap, cur, chunk);
     });
     c->launches += 1;
     if (std::getenv("PXG_PROFILE")) {  // run-cost distribution of this batch
@@ -2044,6 +2051,57 @@ int pxg_proxy_probe(pxg_ctx* c, int n_walk, const pxg_vertex* walk, int n_cand, 
       cudaFree(dc), cudaFree(dq), cudaFree(de);
     }
     cudaFree(dw), cudaFree(dh), cudaFree(dpre), cudaFree(dinfo), cudaFree(dpp);
+  });
+}
+
+int pxg_proxy_recip(pxg_ctx* c, int n_walk, const pxg_vertex* walk, double bound, int n_runs, double* est,
+                    long long* cost, int* truncated) {
+  return guarded(c, [&]() {
+    if (!walk || !est || !cost || !truncated || n_walk < 1 || n_walk > kMaxLight || n_runs < 1)
+      throw InvalidErr{"pxg_proxy_recip: walk of 1..16 vertices and output arrays required"};
+    if (!(bound > 0.0)) throw RuntimeErr{"reciprocal: bound must be positive"};
+    if (!c->proxy_on || c->P.recursion_cap <= 0 || !c->d_rg)
+      throw InvalidErr{"pxg_proxy_recip: the context has proxy sampling off"};
+    const int R = 255;  // runs per (pass, entry): pxg_recip_stream packs the run index in 8 bits
+    const int L = (n_runs + R - 1) / R;
+    const size_t NR = static_cast<size_t>(std::max(c->P.pool_budget, 1)) * std::max(c->P.recip_repeats, 1) * c->batch;
+    if (L > kBatchSetMax || static_cast<size_t>(L) * R > NR)
+      throw InvalidErr{"pxg_proxy_recip: more runs than the context's reciprocal buffers hold"};
+    CK(cudaDeviceSynchronize());  // the run buffers belong to Stage 1: nothing of it may be in flight
+    cudaStream_t st = c->stream1;
+    PV* dw = dupload(reinterpret_cast<const PV*>(walk), n_walk);
+    IncHdr* dh = dalloc<IncHdr>(1);
+    PV* dpre = dalloc<PV>(kMaxLight);
+    int* dinfo = dalloc<int>(8);
+    double* dpp = dalloc<double>(1);
+    double* db = dupload(&bound, 1);
+    PassState hps{};
+    hps.n_ent = 1;
+    PassState* dps = dupload(&hps, 1);
+    k_probe_dropout<<<1, 32, 0, st>>>(c->M, dw, n_walk, dh, dpre, dinfo, dpp);
+    int info0 = 0;
+    CK(cudaMemcpyAsync(&info0, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!info0) {
+      cudaFree(dw), cudaFree(dh), cudaFree(dpre), cudaFree(dinfo), cudaFree(dpp), cudaFree(db), cudaFree(dps);
+      throw InvalidErr{"pxg_proxy_recip: dropout rejects the walk"};
+    }
+    BatchSet bs{};
+    bs.n = L;
+    for (int b = 0; b < L; ++b) bs.p[b] = BatchPass{dh, dpre, db, dps, 0x700000 + b};  // passes no render uses
+    const int runs = L * R;
+    const long long cap = c->P.recursion_cap;
+    CK(cudaMemsetAsync(c->d_rnact, 0, 2 * sizeof(int), st));
+    k_recip_init<<<blocks(runs, 128), 128, 0, st>>>(runs, R, R, bs, c->d_rstate, c->d_ract[0], c->d_rnact, c->d_run_est,
+                                                   c->d_run_cost, c->d_run_trunc);
+    recip_rounds(st, cap, c->d_rnact, [&](int cur, int chunk) { recip_round(c, st, bs, R, R, cap, cur, chunk); });
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(est, c->d_run_est, sizeof(double) * n_runs, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cost, c->d_run_cost, sizeof(long long) * n_runs, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(truncated, c->d_run_trunc, sizeof(int) * n_runs, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(dw), cudaFree(dh), cudaFree(dpre), cudaFree(dinfo), cudaFree(dpp), cudaFree(db), cudaFree(dps);
+    check_err(c, st);
   });
 }
 

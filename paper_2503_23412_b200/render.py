@@ -440,6 +440,18 @@ class ProxyRenderer:
                 "draw_q": dq[:n_draws], "draw_escaped": de[:n_draws].astype(bool)}
 
 
+    def proxy_recip(self, walk: np.ndarray, bound: float, n_runs: int):
+        """n_runs reciprocal runs for the incomplete sub-path of `walk` at a fixed bound, through
+        the production node wavefront and DFS (pxg_proxy_recip). Returns (est, cost, truncated)."""
+        walk = np.ascontiguousarray(walk, VERTEX_DTYPE)
+        est = np.zeros(n_runs)
+        cost = np.zeros(n_runs, np.int64)
+        tr = np.zeros(n_runs, np.int32)
+        self._check(self._L.pxg_proxy_recip(self._ctx, len(walk), walk.ctypes.data, float(bound), n_runs, _dp(est),
+                                            _lp(cost), _ip(tr)))
+        return est, cost, tr.astype(bool)
+
+
 SNAPSHOT_SLOTS = 4   # PXG_SNAPSHOT_SLOTS (include/pxg.h)
 PIPELINE_AHEAD = 3   # passes in flight in the pipelined pass_done loop (< SNAPSHOT_SLOTS)
 

@@ -294,3 +294,44 @@ def test_device_support_mixture_integrates_to_one(pxg, parity_report):
     print(rec)
     assert 0.1 < escape < 0.4
     assert surface + escape == pytest.approx(1.0, rel=0.025)
+
+
+@pytest.mark.gpu
+def test_device_reciprocal_estimates_invert_the_density_integral(pxg, parity_report):
+    """The production reciprocal machinery (global node wavefront + warp DFS) on a hand-built
+    incomplete sub-path: the mean of 2,000 runs equals 1 / integral(target_density), the
+    integral taken by midpoint quadrature of the device's target_density over the lamp (the
+    dropped vertex is a light start, so the integrand lives there). The reference's own check
+    (proj/tests/test_proxy.cpp:620-673: 4 standard errors + 0.5%), untruncated at the default
+    recursion budget."""
+    sc = scenes.caustic_box(8)
+    mirror, shell = 1, 2
+    y = vertex((1.3, 0.0, 1.1), (0, 1, 0), mirror, 0, K_SPECULAR, wi=unit((-0.3, 0.42, -0.1)))
+    lamp0 = vertex((1.0, 0.42, 1.0), (0, -1, 0), shell, 6, K_LIGHT, emitter=0, pdf_fwd=1 / 0.28 ** 2)
+    walk = stack(lamp0, y)
+    res = 600
+    fu = (np.arange(res) + 0.5) / res
+    P = np.stack(np.meshgrid(0.86 + 0.28 * fu, [0.42], 0.86 + 0.28 * fu, indexing="ij"), axis=-1).reshape(-1, 3)
+    cand = np.zeros((len(P), 1), VERTEX_DTYPE)
+    cand["p"][:, 0] = P
+    cand["n"][:, 0] = (0, -1, 0)
+    cand["throughput"][:, 0] = 1.0
+    cand["material"], cand["primitive"], cand["emitter"], cand["flag"] = shell, 6, 0, K_LIGHT
+    with ProxyRenderer(sc, 1, ProxyParams(pretrace_paths=500, light_walks=100)) as r:
+        pr = r.proxy_probe(walk, cand)
+        f, q = pr["f"], pr["q"]
+        total = float(f.sum()) * 0.28 ** 2 / res ** 2
+        assert total > 0.0
+        # the bound the estimator needs: f <= B q on the support (proxy.cpp:389-395 seeds it from
+        # probes; here from the quadrature points, with the reference's 2x slack)
+        bound = 2.0 * float(np.max(f[q > 0] / q[q > 0]))
+        est, cost, tr = r.proxy_recip(walk, bound, 2000)
+    se = est.std(ddof=1) / np.sqrt(est.size)
+    want = 1.0 / total
+    rec = {"case": "reciprocal vs quadrature", "want": want, "mean": float(est.mean()), "se": float(se),
+           "mean_cost": float(cost.mean()), "truncated": int(tr.sum()), "bound": bound}
+    parity_report("proxy_pins", rec)
+    print(rec)
+    assert tr.sum() <= est.size // 100
+    assert abs(est.mean() - want) <= 4.0 * se + 0.005 * want
+    assert cost.min() >= 1
