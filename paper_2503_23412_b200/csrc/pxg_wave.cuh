@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
   int j = -1;
   bool exhausted = false;
   TravState ts;
+  float tb = 0.0f;  // tbound_f(ts.t_best) of the postponed-leaf path: changes only when a leaf test improves the hit
 #if PXG_SSTACK > 0
   __shared__ int s_stack[PXG_SSTACK * 128];
   int stack_loc[kStack - PXG_SSTACK];
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
 #endif
   for (;;) {
     const bool idle = j < 0;
-    const unsigned m = __ballot_sync(FULL, idle);
+    unsigned m = __ballot_sync(FULL, idle);  // idle lanes; the active mask is its complement
     if (!exhausted && m && (__popc(m) >= kRefill || m == FULL)) {
       const int leader = __ffs(m) - 1;
       int base = 0;
@@ -496,17 +497,19 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
         if (jj < total) {
           j = jj;
           trav_init(ts, Q, j);
+          tb = tbound_f(ts.t_best);
         }
       }
+      m = __ballot_sync(FULL, j < 0);  // only a refill changes the mask before the step
     }
-    if (__ballot_sync(FULL, j >= 0) == 0) {
+    if (m == FULL) {
       if (exhausted || total == 0) break;
       continue;
     }
     if (kPost) {
     const bool act = j >= 0;
     const bool pend = act && ts.pend_mask != 0u;
-    const unsigned ma = __ballot_sync(FULL, act), mp = __ballot_sync(FULL, pend);
+    const unsigned ma = ~m, mp = __ballot_sync(FULL, pend);
     const bool leaf_phase = mp != 0u && (mp == ma || 32 * __popc(mp) >= PXG_LEAF_FRAC * __popc(ma));
     if (leaf_phase) {
       if (pend) {
@@ -520,6 +523,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
           }
         } else {
           leaf_step_closest(S, ts);
+          tb = tbound_f(ts.t_best);
           if (ts.node == kDone) {
             Q.hit_prim[j] = ts.best;
             Q.hit_t[j] = ts.t_best;
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
         }
       }
     } else if (act && !pend) {
-      node_step_postponed(S, ts, stack, tbound_f(ts.t_best));
+      node_step_postponed(S, ts, stack, tb);
       if (ts.pend_mask == 0u && ts.node == kDone) {  // nothing left to test or visit
         if (kAny) {
           Q.hit_prim[j] = 0;
