@@ -418,7 +418,10 @@ HostNode4Q quantize_node(const HostNode4& w) {
       q.qhi[a] |= hi << (8 * k);
     }
   }
-  for (int k = 0; k < 4; ++k) q.child[k] = w.child[k];
+  for (int k = 0; k < 4; ++k) {
+    q.child[k] = w.child[k];
+    if (w.child[k] < 0) q.exps |= 1u << (24 + k);  // bits 24-27: child k is a leaf (or empty: never hit)
+  }
   return q;
 }
 

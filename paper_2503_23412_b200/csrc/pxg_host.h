@@ -41,7 +41,7 @@ static_assert(sizeof(HostNode4) == 128, "node4 size");
 // rounded outward, so the quantised boxes contain the fp32 boxes).
 struct alignas(32) HostNode4Q {
   float origin[3];
-  unsigned exps;     // byte a: biased exponent of the axis-a grid step 2^(e-127)
+  unsigned exps;     // byte a: biased exponent of the axis-a grid step 2^(e-127); bits 24-27: child k is a leaf
   int child[4];
   unsigned qlo[3];   // byte k of qlo[a]: child k's lower plane on axis a
   unsigned qhi[3];

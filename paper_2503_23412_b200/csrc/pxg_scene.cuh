@@ -201,7 +201,8 @@ struct TravCount {
 struct Node4Hits {
   float tn[4];
   int code[4];
-  unsigned hit;  // bit k: child k's box is hit
+  unsigned hit;    // bit k: child k's box is hit
+  unsigned leafm;  // bit k: child k is a leaf (code < 0)
 };
 
 #ifndef PXG_NODE256
@@ -283,6 +284,7 @@ __device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, c
   const unsigned hxw = __float_as_uint(c.w), hyw = __float_as_uint(d.x), hzw = __float_as_uint(d.y);
   Node4Hits r;
   r.hit = 0u;
+  r.leafm = (ex >> 24) & 0xfu;  // written by the host quantiser (pxg_host.cpp quantize_node)
   r.code[0] = __float_as_int(b.x);
   r.code[1] = __float_as_int(b.y);
   r.code[2] = __float_as_int(b.z);
@@ -343,6 +345,7 @@ __device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, co
   r.code[1] = ch.y;
   r.code[2] = ch.z;
   r.code[3] = ch.w;
+  r.leafm = (ch.x < 0 ? 1u : 0u) | (ch.y < 0 ? 2u : 0u) | (ch.z < 0 ? 4u : 0u) | (ch.w < 0 ? 8u : 0u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float lo[3] = {lxs[k], lys[k], lzs[k]}, hi[3] = {hxs[k], hys[k], hzs[k]};
@@ -422,13 +425,15 @@ struct SplitStack {
 // Orders the children of `h` (internal nodes and leaves) hit within tbn by tnear: the
 // nearest is returned (kNoChild if none), the rest are pushed so that nearer ones pop
 // first. Non-candidates get +inf keys; a 5-comparator network sorts in registers.
-template <class Stack>
+// kSameBound: tbn is the bound the node test itself used (the postponed-leaf path: no leaf
+// test ran in between), so a hit child already satisfies tn <= tbn.
+template <bool kSameBound = false, class Stack>
 __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, Stack& stack, int& sp) {
   float t[4];
   int c[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const bool ok = (h.hit >> k & 1u) && h.tn[k] <= tbn;
+    const bool ok = (h.hit >> k & 1u) && (kSameBound || h.tn[k] <= tbn);
     t[k] = ok ? h.tn[k] : __int_as_float(0x7f800000);
     c[k] = ok ? h.code[k] : kNoChild;
   }
@@ -444,13 +449,7 @@ __device__ __forceinline__ int node4_order(const Node4Hits& h, float tbn, Stack&
 }
 
 // Hit leaf children of a visited node (bit k of the result: child k is a hit leaf).
-__device__ __forceinline__ unsigned node4_leaves(const Node4Hits& h) {
-  unsigned leaves = 0u;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if ((h.hit >> k & 1u) && h.code[k] < 0) leaves |= 1u << k;
-  return leaves;
-}
+__device__ __forceinline__ unsigned node4_leaves(const Node4Hits& h) { return h.hit & h.leafm; }
 
 __device__ __forceinline__ int node4_code(const Node4Hits& h, int k) {
   return k == 0 ? h.code[0] : k == 1 ? h.code[1] : k == 2 ? h.code[2] : h.code[3];
@@ -459,9 +458,7 @@ __device__ __forceinline__ int node4_code(const Node4Hits& h, int k) {
 // h with only its inner (node) children left in the hit mask.
 __device__ __forceinline__ Node4Hits node4_inner(const Node4Hits& h) {
   Node4Hits hn = h;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (h.code[k] < 0) hn.hit &= ~(1u << k);
+  hn.hit &= ~h.leafm;
   return hn;
 }
 

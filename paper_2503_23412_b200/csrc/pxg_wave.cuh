@@ -341,7 +341,7 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, Stack
       if (rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id) > 0.0) return 1;
     }
   }
-  int next = node4_order(node4_inner(h), tb, stack, ts.sp);
+  int next = node4_order<true>(node4_inner(h), tb, stack, ts.sp);
   if (next == kNoChild) {
     if (ts.sp == 0) return 2;
     next = stack.pop(ts.sp);
@@ -369,7 +369,7 @@ __device__ __forceinline__ void node_step_postponed(const SceneView& S, TravStat
   const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
   ts.pend_node = ts.node;
   ts.pend_mask = node4_leaves(h);
-  int next = node4_order(node4_inner(h), tb, stack, ts.sp);
+  int next = node4_order<true>(node4_inner(h), tb, stack, ts.sp);
   if (next == kNoChild) next = ts.sp == 0 ? kDone : stack.pop(ts.sp);
   ts.node = next;
 }
