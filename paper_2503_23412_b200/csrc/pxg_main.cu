@@ -437,19 +437,28 @@ struct HostProbe {
 #define PXG_TRAV_HI 8  // resident blocks per SM of the high-occupancy traversal variant (A/B: 10, 12)
 #endif
 // Persistent traversal of queue q (closest hit or any hit) with the context's occupancy variant.
-template <bool kAny>
-void launch_trav(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
+template <bool kAny, int kL>
+void launch_trav_layout(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
   if (c->trav_minb == 8) {
     if (c->trav_post)
-      k_trav_persistent<kAny, PXG_TRAV_HI, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, PXG_TRAV_HI, true, kL><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
     else
-      k_trav_persistent<kAny, PXG_TRAV_HI, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, PXG_TRAV_HI, false, kL><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
   } else {
     if (c->trav_post)
-      k_trav_persistent<kAny, 6, true><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, 6, true, kL><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
     else
-      k_trav_persistent<kAny, 6, false><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
+      k_trav_persistent<kAny, 6, false, kL><<<c->trav_blocks, 128, 0, st>>>(c->S, q, fetch);
   }
+}
+
+// The node layout is a template parameter of the kernels (no per-visit test of S.nodeq).
+template <bool kAny>
+void launch_trav(pxg_ctx* c, const RayQueue& q, int* fetch, cudaStream_t st) {
+  if (c->S.nodeq)
+    launch_trav_layout<kAny, 1>(c, q, fetch, st);
+  else
+    launch_trav_layout<kAny, 0>(c, q, fetch, st);
 }
 
 RayQueue make_queue(pxg_ctx* c, size_t cap) {
@@ -1545,9 +1554,9 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
       c->trav_post = c->S.nodeq != 0;
       if (const char* e = std::getenv("PXG_TRAV_POSTPONE")) c->trav_post = std::atoi(e) != 0;
       if (c->trav_minb == 8)
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, PXG_TRAV_HI, true>, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, PXG_TRAV_HI, true, 1>, 128, 0));
       else
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6, false>, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_persistent<false, 6, false, 0>, 128, 0));
       c->trav_blocks = std::max(1, sms * std::max(per_sm, 1));
       c->gs_blocks = sms * (std::getenv("PXG_GS_PER_SM") ? std::atoi(std::getenv("PXG_GS_PER_SM")) : 256);
       int pe = 0, pd = 0;

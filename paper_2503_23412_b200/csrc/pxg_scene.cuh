@@ -321,11 +321,13 @@ __device__ __forceinline__ Node4Hits node4q_test(const SceneView& S, int node, c
   return r;
 }
 
-template <bool kWide = false>
+// kLayout: -1 the context's layout read from S.nodeq on every visit; 0 / 1: 128 B / quantised
+// nodes known at compile time (the persistent kernels are instantiated per layout).
+template <bool kWide = false, int kLayout = -1>
 __device__ __forceinline__ Node4Hits node4_test(const SceneView& S, int node, const RayF& rf, float tb) {
   // the single-ray path keeps the 128 B nodes: 4 x 16 B loads of the quantised node plus its
   // decode measured 1% slower there (C4, same box)
-  if (kWide && PXG_NODEQ && S.nodeq) return node4q_test<true>(S, node, rf, tb);
+  if (kWide && PXG_NODEQ && (kLayout == 1 || (kLayout < 0 && S.nodeq))) return node4q_test<true>(S, node, rf, tb);
   const float4* __restrict__ q = reinterpret_cast<const float4*>(S.nodes4 + node);
   float4 lx, ly, lz, hx, hy, hz;
   if (kWide && PXG_NODE256) {

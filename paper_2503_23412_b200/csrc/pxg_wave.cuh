@@ -298,11 +298,11 @@ __device__ __forceinline__ void trav_init(TravState& ts, const RayQueue& Q, int 
 
 // Returns true when the traversal is complete (closest hit in ts.best / ts.t_best).
 // ts.node holds a child code: >= 0 a 4-wide node, < 0 a leaf.
-template <bool kCount = false, class Stack>
+template <bool kCount = false, int kL = -1, class Stack>
 __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, Stack& stack, TravCount* cnt = nullptr) {
   // every step visits one 4-wide node; its hit leaf children are tested right away, its hit
   // inner children are ordered nearest-first (the next node, then the stack)
-  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tbound_f(ts.t_best));
+  const Node4Hits h = node4_test<true, kL>(S, ts.node, ts.rf, tbound_f(ts.t_best));
   if (kCount) cnt->nodes += 1;
   for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
@@ -327,10 +327,10 @@ __device__ __forceinline__ bool closest_step(const SceneView& S, TravState& ts, 
 }
 
 // Returns 0 while running, 1 on a hit in [kRayEps, tmax] (occluded), 2 when no hit.
-template <bool kCount = false, class Stack>
+template <bool kCount = false, int kL = -1, class Stack>
 __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, Stack& stack, TravCount* cnt = nullptr) {
   const float tb = tbound_f(ts.t_best);
-  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
+  const Node4Hits h = node4_test<true, kL>(S, ts.node, ts.rf, tb);
   if (kCount) cnt->nodes += 1;
   for (unsigned leaves = node4_leaves(h); leaves; leaves &= leaves - 1) {
     const int code = ~node4_code(h, __ffs(leaves) - 1);
@@ -358,15 +358,16 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, Stack
 // which primitives are tested; only culling uses a bound that is a few steps older.
 constexpr int kDone = static_cast<int>(0x80000001u);  // ts.node once nothing is left to visit
 
+template <int kL = -1>
 __device__ __forceinline__ int4 node4_codes(const SceneView& S, int node) {
-  if (PXG_NODEQ && S.nodeq) return __ldg(reinterpret_cast<const int4*>(S.nodes4q + node) + 1);
+  if (PXG_NODEQ && (kL == 1 || (kL < 0 && S.nodeq))) return __ldg(reinterpret_cast<const int4*>(S.nodes4q + node) + 1);
   return __ldg(reinterpret_cast<const int4*>(S.nodes4 + node) + 6);
 }
 
 // Node visit: hit leaves postponed, the next node chosen (kDone when none is left).
-template <class Stack>
+template <int kL = -1, class Stack>
 __device__ __forceinline__ void node_step_postponed(const SceneView& S, TravState& ts, Stack& stack, float tb) {
-  const Node4Hits h = node4_test<true>(S, ts.node, ts.rf, tb);
+  const Node4Hits h = node4_test<true, kL>(S, ts.node, ts.rf, tb);
   ts.pend_node = ts.node;
   ts.pend_mask = node4_leaves(h);
   int next = node4_order<true>(node4_inner(h), tb, stack, ts.sp);
@@ -375,8 +376,9 @@ __device__ __forceinline__ void node_step_postponed(const SceneView& S, TravStat
 }
 
 // The postponed leaves, closest hit.
+template <int kL = -1>
 __device__ __forceinline__ void leaf_step_closest(const SceneView& S, TravState& ts) {
-  const int4 cc = node4_codes(S, ts.pend_node);
+  const int4 cc = node4_codes<kL>(S, ts.pend_node);
   for (unsigned leaves = ts.pend_mask; leaves; leaves &= leaves - 1) {
     const int k = __ffs(leaves) - 1;
     const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
@@ -394,8 +396,9 @@ __device__ __forceinline__ void leaf_step_closest(const SceneView& S, TravState&
 }
 
 // The postponed leaves, any hit: true when one of them is hit within tmax.
+template <int kL = -1>
 __device__ __forceinline__ bool leaf_step_any(const SceneView& S, TravState& ts) {
-  const int4 cc = node4_codes(S, ts.pend_node);
+  const int4 cc = node4_codes<kL>(S, ts.pend_node);
   const unsigned pm = ts.pend_mask;
   ts.pend_mask = 0u;
   for (unsigned leaves = pm; leaves; leaves &= leaves - 1) {
@@ -463,7 +466,7 @@ constexpr int kRefill = PXG_REFILL;  // refill a warp's idle lanes once at least
 // single compromise before).
 // kPost: postponed leaf tests (+4% on C4's 1M-triangle scene, -0.3% on the L2-resident C2,
 // so chosen per scene with the node layout).
-template <bool kAny, int kMinB, bool kPost>
+template <bool kAny, int kMinB, bool kPost, int kL = -1>
 __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, RayQueue Q, int* next_ray) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
     if (leaf_phase) {
       if (pend) {
         if (kAny) {
-          if (leaf_step_any(S, ts)) {
+          if (leaf_step_any<kL>(S, ts)) {
             Q.hit_prim[j] = 1;
             j = -1;
           } else if (ts.node == kDone) {
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
             j = -1;
           }
         } else {
-          leaf_step_closest(S, ts);
+          leaf_step_closest<kL>(S, ts);
           tb = tbound_f(ts.t_best);
           if (ts.node == kDone) {
             Q.hit_prim[j] = ts.best;
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
         }
       }
     } else if (act && !pend) {
-      node_step_postponed(S, ts, stack, tb);
+      node_step_postponed<kL>(S, ts, stack, tb);
       if (ts.pend_mask == 0u && ts.node == kDone) {  // nothing left to test or visit
         if (kAny) {
           Q.hit_prim[j] = 0;
@@ -545,12 +548,12 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
     }
     } else if (j >= 0) {
       if (kAny) {
-        const int r = any_step(S, ts, stack);
+        const int r = any_step<false, kL>(S, ts, stack);
         if (r) {
           Q.hit_prim[j] = r == 1 ? 1 : 0;
           j = -1;
         }
-      } else if (closest_step(S, ts, stack)) {
+      } else if (closest_step<false, kL>(S, ts, stack)) {
         Q.hit_prim[j] = ts.best;
         Q.hit_t[j] = ts.t_best;
         j = -1;
