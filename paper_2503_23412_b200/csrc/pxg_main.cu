@@ -677,7 +677,7 @@ void recip_round(pxg_ctx* c, cudaStream_t st, const BatchSet& bs, int R, int str
         CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
         launch_trav<false>(c, qa, fetch, st);
         CK(cudaMemsetAsync(qb.count, 0, sizeof(int), st));
-        k_rq_glue<<<gsb, 128, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
+        k_rq_glue<<<gsb / 2, kGlueT, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
         std::swap(qa, qb);
       }
       k_rq_record<<<gsb, 128, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);

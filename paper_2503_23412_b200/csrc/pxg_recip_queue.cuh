@@ -123,56 +123,98 @@ __global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_setup(SceneView S, uint
 }
 
 // After a closest-hit round: the hit becomes the next candidate vertex; a from-specular chain
-// (strand 0) with vertices left samples its next direction and pushes the next ray.
-__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_glue(SceneView S, uint64_t seed, int repeats, int stride,
-                                                 const __grid_constant__ BatchSet bs, RqView R, RayQueue in,
-                                                 RayQueue out) {
+// (strand 0) with vertices left samples its next direction and pushes the next ray. A block
+// takes 256 consecutive rays and regroups them in shared memory (counting sort, as k_shade
+// does) by what they need: a BSDF sample (by the lobe set of the hit material), only the
+// vertex, or nothing (escaped), so the warps that sample run one kind of BSDF and the escaped
+// rays cost whole idle warps, not idle lanes (ncu before: 9.4 of 32 lanes).
+constexpr int kGlueT = 256;
+__global__ void __launch_bounds__(kGlueT, PXG_RQ_MINB / 2) k_rq_glue(SceneView S, uint64_t seed, int repeats, int stride,
+                                                                     const __grid_constant__ BatchSet bs, RqView R,
+                                                                     RayQueue in, RayQueue out) {
+  __shared__ int s_cnt[8];
+  __shared__ short s_perm[kGlueT];
   const int n = *in.count;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    const int t = in.path[s];
-    RqItem& it = R.item[t];
-    const int prim = in.hit_prim[s];
-    if (prim < 0) {
-      it.state = kRWEscaped;
-      continue;
-    }
-    const double4 r0 = in.ray[2 * s], r1 = in.ray[2 * s + 1];
-    const V3 o = v3(r0.x, r0.y, r0.z), d = v3(r0.w, r1.x, r1.y);
-    Hit hit;
-    hit.t = in.hit_t[s];
-    hit.p = o + hit.t * d;
-    hit.prim = prim;
-    hit.n = prim_normal(S, prim, hit.p);
-    hit.material = S.prim_mat[prim];
-    hit.emitter = S.prim_emitter[prim];
-    PV* gv = R.gv + static_cast<size_t>(t) * 4;
-    const int strand = it.strand;
-    int step = it.step;
-    const PV v = vertex_from_hit(S, hit, -d);
-    gv[strand == 1 ? 0 : step] = v;
-    unsigned char state = kRWSampled;
-    if (strand == 0) {
-      ++step;
-      it.step = static_cast<unsigned char>(step);
-      if (step < it.u) {
-        const int j = it.j;
-        const BatchPass& P = bs.p[j / stride];
-        const int w = j % stride;
-        const IncHdr& h = P.inc[w / repeats];
-        Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(it.k),
-                          pxg_recip_stream(P.pass, h.walk, h.end, w % repeats));
-        nr.r.i = it.ctr;
-        BsdfSample b = sample_bsdf(S.materials[v.mat], v.n, v.wi, nr);
-        it.ctr = nr.r.i;
-        if (!b.valid || b.pdf <= 0.0) {
-          state = kRWEscaped;
+  for (int s0 = blockIdx.x * kGlueT; s0 < n; s0 += gridDim.x * kGlueT) {  // block-uniform trips
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int cls = 7;  // past the end of the queue
+    {
+      const int s = s0 + threadIdx.x;
+      if (s < n) {
+        const int prim = in.hit_prim[s];
+        if (prim < 0) {
+          cls = 6;  // escaped: only the state changes
         } else {
-          state = kRWRay;
-          rq_push(out, t, v.p, b.wo, 1e30);
+          const RqItem& it = R.item[in.path[s]];
+          cls = 5;  // vertex only
+          if (it.strand == 0 && it.step + 1 < it.u) {
+            const Material& m = S.materials[S.prim_mat[prim]];
+            double wd, wm, wt;
+            lobes(m, wd, wm, wt);
+            const int bits = ((wd > 0.0) ? 1 : 0) | ((wm > 0.0) ? 2 : 0) | ((wt > 0.0) ? 4 : 0);
+            cls = bits == 1 ? 0 : bits == 2 ? 1 : bits == 4 ? 2 : bits == 3 ? 3 : 4;
+          }
         }
       }
     }
-    it.state = state;
+    const int pos = atomicAdd(&s_cnt[cls], 1);
+    __syncthreads();
+    int base = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      if (k < cls) base += s_cnt[k];
+    if (cls < 7) s_perm[base + pos] = static_cast<short>(threadIdx.x);
+    const int live = kGlueT - s_cnt[7];
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < live) {
+      const int s = s0 + s_perm[threadIdx.x];
+      const int t = in.path[s];
+      RqItem& it = R.item[t];
+      const int prim = in.hit_prim[s];
+      if (prim < 0) {
+        it.state = kRWEscaped;
+      } else {
+        const double4 r0 = in.ray[2 * s], r1 = in.ray[2 * s + 1];
+        const V3 o = v3(r0.x, r0.y, r0.z), d = v3(r0.w, r1.x, r1.y);
+        Hit hit;
+        hit.t = in.hit_t[s];
+        hit.p = o + hit.t * d;
+        hit.prim = prim;
+        hit.n = prim_normal(S, prim, hit.p);
+        hit.material = S.prim_mat[prim];
+        hit.emitter = S.prim_emitter[prim];
+        PV* gv = R.gv + static_cast<size_t>(t) * 4;
+        const int strand = it.strand;
+        int step = it.step;
+        const PV v = vertex_from_hit(S, hit, -d);
+        gv[strand == 1 ? 0 : step] = v;
+        unsigned char state = kRWSampled;
+        if (strand == 0) {
+          ++step;
+          it.step = static_cast<unsigned char>(step);
+          if (step < it.u) {
+            const int j = it.j;
+            const BatchPass& P = bs.p[j / stride];
+            const int w = j % stride;
+            const IncHdr& h = P.inc[w / repeats];
+            Rng nr = make_rng(seed, PXG_KIND_RECIP_NODE, static_cast<uint32_t>(it.k),
+                              pxg_recip_stream(P.pass, h.walk, h.end, w % repeats));
+            nr.r.i = it.ctr;
+            BsdfSample b = sample_bsdf(S.materials[v.mat], v.n, v.wi, nr);
+            it.ctr = nr.r.i;
+            if (!b.valid || b.pdf <= 0.0) {
+              state = kRWEscaped;
+            } else {
+              state = kRWRay;
+              rq_push(out, t, v.p, b.wo, 1e30);
+            }
+          }
+        }
+        it.state = state;
+      }
+    }
+    __syncthreads();  // s_cnt / s_perm are reused by the next tile
   }
 }
 
