@@ -680,7 +680,7 @@ void recip_round(pxg_ctx* c, cudaStream_t st, const BatchSet& bs, int R, int str
         k_rq_glue<<<gsb / 2, kGlueT, 0, st>>>(c->S, c->seed, R, stride, bs, c->rq, qa, qb);
         std::swap(qa, qb);
       }
-      k_rq_record<<<gsb, 128, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);
+      k_rq_record<<<gsb / 2, kGlueT, 0, st>>>(c->S, R, stride, bs, c->d_rnact + cur, served, chunk, c->rq, c->rqS);
       CK(cudaMemsetAsync(fetch, 0, sizeof(int), st));
       launch_trav<true>(c, c->rqS, fetch, st);
       k_rq_vis<<<gsb, 256, 0, st>>>(c->rqS, c->rq);

@@ -239,30 +239,62 @@ struct VisPush {
   }
 };
 
-__global__ void __launch_bounds__(128, PXG_RQ_MINB) k_rq_record(SceneView S, int repeats, int stride,
-                                                   const __grid_constant__ BatchSet bs, const int* n_active,
-                                                   int served, int chunk, RqView R, RayQueue Q) {
+// The nodes of a block's tile are regrouped like k_rq_glue's rays: by the dropped block's
+// length u and by whether a control vertex exists (the two things that decide which density
+// terms and how many segments a node has); nodes without a sampled candidate drop out.
+__global__ void __launch_bounds__(kGlueT, PXG_RQ_MINB / 2) k_rq_record(SceneView S, int repeats, int stride,
+                                                                       const __grid_constant__ BatchSet bs,
+                                                                       const int* n_active, int served, int chunk,
+                                                                       RqView R, RayQueue Q) {
+  __shared__ int s_cnt[9];
+  __shared__ short s_perm[kGlueT];
   const long long total = rq_total(n_active, served, chunk);
-  for (long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; tid < total;
-       tid += static_cast<long long>(gridDim.x) * blockDim.x) {
-    RqItem& it = R.item[tid];
-    if (it.k < 0 || it.state != kRWSampled) continue;
-    const int j = it.j;
-    const BatchPass& P = bs.p[j / stride];
-    const int e = (j % stride) / repeats;
-    const IncHdr& h = P.inc[e];
-    const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
-    const PV* gv = R.gv + static_cast<size_t>(tid) * 4;
-    unsigned need = 0u, vis = 0u;
-    double qfs = 0.0, qoth = 0.0, f = 0.0;
-    const VisPush rec{&need, &vis, Q, static_cast<int>(tid)};
-    support_terms_v(S, h, pre, gv, rec, qfs, qoth);
-    if (support_combine(h.u, qfs, qoth) > 0.0) f = target_density_v(S, h, pre, gv, rec);
-    it.need = need;
-    it.vis = vis;
-    it.qfs = qfs;
-    it.qoth = qoth;
-    it.f = f;
+  for (long long t0 = static_cast<long long>(blockIdx.x) * kGlueT; t0 < total;
+       t0 += static_cast<long long>(gridDim.x) * kGlueT) {  // block-uniform trips
+    if (threadIdx.x < 9) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int cls = 8;  // nothing to record
+    {
+      const long long tid = t0 + threadIdx.x;
+      if (tid < total) {
+        const RqItem& it = R.item[tid];
+        if (it.k >= 0 && it.state == kRWSampled) {
+          const BatchPass& P = bs.p[it.j / stride];
+          const IncHdr& h = P.inc[(it.j % stride) / repeats];
+          cls = 2 * (min(max(h.u, 1), 4) - 1) + (h.n_prefix > 0 ? 1 : 0);
+        }
+      }
+    }
+    const int pos = atomicAdd(&s_cnt[cls], 1);
+    __syncthreads();
+    int base = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < cls) base += s_cnt[k];
+    if (cls < 8) s_perm[base + pos] = static_cast<short>(threadIdx.x);
+    const int live = kGlueT - s_cnt[8];
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < live) {
+      const long long tid = t0 + s_perm[threadIdx.x];
+      RqItem& it = R.item[tid];
+      const int j = it.j;
+      const BatchPass& P = bs.p[j / stride];
+      const int e = (j % stride) / repeats;
+      const IncHdr& h = P.inc[e];
+      const PV* pre = P.prefix + static_cast<size_t>(e) * kMaxLight;
+      const PV* gv = R.gv + static_cast<size_t>(tid) * 4;
+      unsigned need = 0u, vis = 0u;
+      double qfs = 0.0, qoth = 0.0, f = 0.0;
+      const VisPush rec{&need, &vis, Q, static_cast<int>(tid)};
+      support_terms_v(S, h, pre, gv, rec, qfs, qoth);
+      if (support_combine(h.u, qfs, qoth) > 0.0) f = target_density_v(S, h, pre, gv, rec);
+      it.need = need;
+      it.vis = vis;
+      it.qfs = qfs;
+      it.qoth = qoth;
+      it.f = f;
+    }
+    __syncthreads();  // s_cnt / s_perm are reused by the next tile
   }
 }
 
