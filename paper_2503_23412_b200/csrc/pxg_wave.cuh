@@ -350,10 +350,16 @@ __device__ __forceinline__ int any_step(const SceneView& S, TravState& ts, Stack
   return 0;
 }
 
+#ifndef PXG_LEAF_ONE
+#define PXG_LEAF_ONE 1  // a leaf phase tests ONE pending leaf per lane (0: all of a lane's; C4 -1.8%)
+#endif
 // ---- postponed leaf tests (Aila & Laine's "while-while" for the 4-wide node step): a node
 // visit only records its hit leaf children; the fp64 primitive tests of the warp run
 // together once most active lanes have some (or no lane can visit a node), instead of
-// diverging against the node visits of the other lanes on every step. Same hits: the
+// diverging against the node visits of the other lanes on every step. A leaf phase tests ONE
+// pending leaf per lane, so its lanes stay together through the fp64 test; a lane with more
+// waits for the next phase (testing all of a lane's leaves in one phase ran the 2nd-4th tests
+// at 1-5 lanes). Same hits: the
 // closest hit with the id tie rule and the any-hit boolean do not depend on the order in
 // which primitives are tested; only culling uses a bound that is a few steps older.
 constexpr int kDone = static_cast<int>(0x80000001u);  // ts.node once nothing is left to visit
@@ -379,6 +385,23 @@ __device__ __forceinline__ void node_step_postponed(const SceneView& S, TravStat
 template <int kL = -1>
 __device__ __forceinline__ void leaf_step_closest(const SceneView& S, TravState& ts) {
   const int4 cc = node4_codes<kL>(S, ts.pend_node);
+#if PXG_LEAF_ONE
+  {  // one pending leaf per leaf phase: the lanes of a phase stay together through the fp64 test
+    const int k = __ffs(ts.pend_mask) - 1;
+    ts.pend_mask &= ts.pend_mask - 1;
+    const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
+    const int first = code >> 4, count = code & 15;
+    for (int i = 0; i < count; ++i) {
+      int id;
+      const double t = rec_hit(S, first + i, ts.o, ts.d, ts.t_best, id);
+      if (t > 0.0 && (t < ts.t_best || id > ts.best)) {
+        ts.t_best = t;
+        ts.best = id;
+      }
+    }
+    return;
+  }
+#endif
   for (unsigned leaves = ts.pend_mask; leaves; leaves &= leaves - 1) {
     const int k = __ffs(leaves) - 1;
     const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
@@ -399,8 +422,13 @@ __device__ __forceinline__ void leaf_step_closest(const SceneView& S, TravState&
 template <int kL = -1>
 __device__ __forceinline__ bool leaf_step_any(const SceneView& S, TravState& ts) {
   const int4 cc = node4_codes<kL>(S, ts.pend_node);
+#if PXG_LEAF_ONE
+  const unsigned pm = ts.pend_mask & (0u - ts.pend_mask);  // the lowest pending leaf only
+  ts.pend_mask &= ts.pend_mask - 1;
+#else
   const unsigned pm = ts.pend_mask;
   ts.pend_mask = 0u;
+#endif
   for (unsigned leaves = pm; leaves; leaves &= leaves - 1) {
     const int k = __ffs(leaves) - 1;
     const int code = ~(k == 0 ? cc.x : k == 1 ? cc.y : k == 2 ? cc.z : cc.w);
@@ -430,12 +458,12 @@ __device__ __forceinline__ bool warp_trace(const SceneView& S, TravState& ts, St
           if (leaf_step_any(S, ts)) {
             occ = true;
             live = false;
-          } else if (ts.node == kDone) {
+          } else if (ts.pend_mask == 0u && ts.node == kDone) {
             live = false;
           }
         } else {
           leaf_step_closest(S, ts);
-          if (ts.node == kDone) live = false;
+          if (ts.pend_mask == 0u && ts.node == kDone) live = false;
         }
       }
     } else if (live && !pend) {
@@ -520,14 +548,14 @@ __global__ void __launch_bounds__(128, kMinB) k_trav_persistent(SceneView S, Ray
           if (leaf_step_any<kL>(S, ts)) {
             Q.hit_prim[j] = 1;
             j = -1;
-          } else if (ts.node == kDone) {
+          } else if (ts.pend_mask == 0u && ts.node == kDone) {
             Q.hit_prim[j] = 0;
             j = -1;
           }
         } else {
           leaf_step_closest<kL>(S, ts);
           tb = tbound_f(ts.t_best);
-          if (ts.node == kDone) {
+          if (ts.pend_mask == 0u && ts.node == kDone) {
             Q.hit_prim[j] = ts.best;
             Q.hit_t[j] = ts.t_best;
             j = -1;
