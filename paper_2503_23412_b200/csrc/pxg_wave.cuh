@@ -196,10 +196,10 @@ __device__ __forceinline__ bool shade_one(const SceneView& S, const PathSet& P, 
 // (ncu, C4: pxg_bsdf.cuh ran at 7.3 of 32 lanes with the queue order). Every path keeps its
 // own Philox stream and vertex slots, so the grouping cannot change a result.
 #ifndef PXG_SHADE_T
-#define PXG_SHADE_T 256  // threads per block = rays regrouped together
+#define PXG_SHADE_T 512  // threads per block = rays regrouped together (256: C4 -1.2%, 1024: = on C4, -1% on C2)
 #endif
 #ifndef PXG_SHADE_MINB
-#define PXG_SHADE_MINB 4  // 64 registers: 1024 resident threads per SM (C4 +2.4%, C2 +2.5% with the regrouping; 3: +1.4%)
+#define PXG_SHADE_MINB 2  // 64 registers: 1024 resident threads per SM (1280 / 1536: -1.8% / -3.1% from spills)
 #endif
 #ifndef PXG_SHADE_SORT
 #define PXG_SHADE_SORT 1
