@@ -852,7 +852,7 @@ void enqueue_stage2_tile(pxg_ctx* c, int pass, PoolSlot& sl, bool record_prims, 
       ++c->launches;
     }
     // sub-path-only MIS step densities (used by the connections of this pass)
-    k_path_factors<<<blocks(4ll * c->n, T), T, 0, tt>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
+    k_path_factors<<<blocks((PXG_PF_MERGE ? 2ll : 4ll) * c->n, T), T, 0, tt>>>(c->S, c->d_eye, c->d_neye, c->d_light, c->d_nlight, c->n,
                                                   c->pcache);
     ++c->launches;
   }

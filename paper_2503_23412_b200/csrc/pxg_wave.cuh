@@ -858,14 +858,63 @@ __global__ void k_conn_visibility(RayQueue shadow, ConnBuf C) {
 }
 
 // Per-pixel sub-path step densities (PathCache), evaluated once per pixel and pass.
-// One thread per (pixel, family): 4 n threads (LF, LR, EF, ER) so the fp64 step loops of a
-// pixel run side by side; the LF thread also writes the light-direction density.
+// One thread per (pixel, sub-path): 2 n threads, each walking a window of three consecutive
+// vertices and writing both directions (LF + LR on the light sub-path, ER + EF on the eye
+// sub-path); the light thread also writes the light-direction density. (Round 1: one thread per
+// (pixel, family), 4 n threads, which read every vertex from HBM twice.)
 #ifndef PXG_PF_MINB
 #define PXG_PF_MINB 8
+#endif
+#ifndef PXG_PF_MERGE
+#define PXG_PF_MERGE 1  // one thread per (pixel, sub-path) computing both directions (0: per family; C4 -0.7%)
 #endif
 __global__ void __launch_bounds__(128, PXG_PF_MINB) k_path_factors(SceneView S, const PV* eye, const int* n_eye, const PV* light, const int* n_light,
                                int n, PathCache C) {
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+#if PXG_PF_MERGE
+  // one thread per (pixel, sub-path): the forward and the reverse step density of a window of
+  // three consecutive vertices (lo, mid, hi) are bsdf_step_v(mid, lo, hi) and
+  // bsdf_step_v(mid, hi, lo): LF[w + 2] / LR[w] on the light sub-path, ER[w + 2] / EF[w] on the
+  // eye sub-path, so both directions share the window's loads (the per-family threads read
+  // every vertex from HBM twice: ncu, 7.6 GB per launch)
+  if (tid >= 2ll * n) return;
+  {
+    const int i = static_cast<int>(tid % n), sub = static_cast<int>(tid / n);
+    const size_t st = static_cast<size_t>(n);
+    const PV* v = (sub ? eye : light) + i;
+    const int cnt = sub ? n_eye[i] : n_light[i];
+    double* fwd = sub ? C.ER : C.LF;
+    double* rev = sub ? C.EF : C.LR;
+    for (int w = 0; w <= cnt - 3; ++w) {
+      const PV& lo = v[w * st];
+      const PV& mid = v[(w + 1) * st];
+      const PV& hi = v[(w + 2) * st];
+      const double a = bsdf_step_v(S, mid, lo, hi);
+      const double b = bsdf_step_v(S, mid, hi, lo);
+      fwd[(w + 2) * st + i] = a;
+      rev[w * st + i] = b;
+    }
+    if (sub) return;
+    int ok = 0;
+    double area = 0.0;
+    if (cnt >= 2) {
+      const PV& y0 = v[0];
+      const PV& y1 = v[st];
+      V3 d = y1.p - y0.p;
+      double len = length(d);
+      if (len > 0.0) {
+        double pdf_w = light_direction_pdf(y0.n, d / len);
+        if (pdf_w > 0.0) {
+          ok = 1;
+          area = to_area_density(pdf_w, y0.p, y1.p, y1.n);
+        }
+      }
+    }
+    C.ld_ok[i] = ok;
+    C.ld[i] = area;
+    return;
+  }
+#endif
   if (tid >= 4ll * n) return;
   const int i = static_cast<int>(tid % n), fam = static_cast<int>(tid / n);
   const size_t st = static_cast<size_t>(n);
