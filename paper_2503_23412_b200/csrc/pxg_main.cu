@@ -316,6 +316,7 @@ struct pxg_ctx {
   RqView rq{nullptr, nullptr, 0};
   RayQueue rqA, rqB, rqS;
   unsigned long long* d_node_stat = nullptr;  // reciprocal tree nodes evaluated / consumed, finished runs
+  int* shade_perm[2] = {nullptr, nullptr};    // k_shade_order's per-tile class order: [0] Stage-2 traces, [1] Stage-1 walks
   double* d_rw_ends = nullptr; // its visibility segment endpoints: [wave_blocks][kRW][10][6]
   int dfs_blocks = 0;         // grid-stride warp-DFS grid
   int sel_cap = 0;            // shared-memory capacity (entries) of the pool selection
@@ -495,7 +496,14 @@ void trace_paths(pxg_ctx* c, const PathSet& P, RayQueue in, RayQueue out, cudaSt
       launch_trav<false>(c, in, fetch, st);
     }
     CK(cudaMemsetAsync(out.count, 0, sizeof(int), st));
-    k_shade<<<blocks(P.n, PXG_SHADE_T), PXG_SHADE_T, 0, st>>>(c->S, P, in, out);
+    if (c->shade_perm[0]) {
+      int* perm = c->shade_perm[st == c->stream1 ? 1 : 0];
+      k_shade_order<<<blocks(P.n, kOrderT), kOrderT, 0, st>>>(c->S, in, perm);
+      k_shade_perm<<<blocks(P.n, 128), 128, 0, st>>>(c->S, P, in, out, perm);
+      ++c->launches;
+    } else {
+      k_shade<<<blocks(P.n, PXG_SHADE_T), PXG_SHADE_T, 0, st>>>(c->S, P, in, out);
+    }
     c->launches += 2;
     std::swap(in, out);
   }
@@ -1445,6 +1453,11 @@ int create_impl(const pxg_scene* scn, const pxg_params* params, uint64_t seed, i
         const double budget = (wb ? std::atof(wb) : 32.0) * 1e9;
         c->batch = std::max(1, std::min(c->batch, static_cast<int>(budget / per_pass)));
       }
+    }
+    if (!std::getenv("PXG_SHADE_PERM") || std::atoi(std::getenv("PXG_SHADE_PERM")) != 0) {  // 0: one-kernel k_shade (A/B)
+      const size_t w = (c->proxy_on && c->n_walks > 0) ? static_cast<size_t>(c->n_walks) * c->batch : 0;
+      c->shade_perm[0] = c->alloc<int>(n + kOrderT);
+      c->shade_perm[1] = c->alloc<int>(w + kOrderT);
     }
     if (c->proxy_on && c->n_walks > 0) {
       const size_t w = static_cast<size_t>(c->n_walks) * c->batch;  // the walks of a whole batch

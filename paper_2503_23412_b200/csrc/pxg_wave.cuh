@@ -249,6 +249,57 @@ __global__ void __launch_bounds__(PXG_SHADE_T, PXG_SHADE_MINB) k_shade(SceneView
     push_ray(out, i, no, nd, 1e30);
 }
 
+// ---- two-kernel form of the regrouping (PXG_SHADE_PERM): k_shade_order computes the same
+// class order per tile of kOrderT rays and writes it to HBM (perm[tile base + rank] = queue slot,
+// -1 past the live rays), k_shade_perm shades in that order with small blocks, so a block's
+// registers are released when ITS warps are done instead of when the slowest warp of a
+// 512-thread tile is (ncu: k_shade at 26% achieved occupancy of a theoretical 50%).
+constexpr int kOrderT = 1024;
+__global__ void __launch_bounds__(kOrderT) k_shade_order(SceneView S, RayQueue in, int* perm) {
+  __shared__ int s_cnt[8];
+  const int count = *in.count;
+  const int j0 = blockIdx.x * kOrderT;
+  if (j0 >= count) return;  // block-uniform
+  const int j = j0 + threadIdx.x;
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int cls = 7;  // escaped or past the end of the queue
+  if (j < count) {
+    const int prim = in.hit_prim[j];
+    if (prim >= 0) {
+      const Material& m = S.materials[S.prim_mat[prim]];
+      double wd, wm, wt;
+      lobes(m, wd, wm, wt);
+      cls = ((wd > 0.0) ? 1 : 0) | ((wm > 0.0) ? 2 : 0) | ((wt > 0.0) ? 4 : 0);
+      cls = cls == 0 ? 6 : cls - 1;
+    }
+  }
+  const int pos = atomicAdd(&s_cnt[cls], 1);
+  __syncthreads();
+  int base = 0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k)
+    if (k < cls) base += s_cnt[k];
+  perm[j0 + base + pos] = cls < 7 ? j : -1;
+}
+
+#ifndef PXG_SHADE_PERM_MINB
+#define PXG_SHADE_PERM_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PXG_SHADE_PERM_MINB) k_shade_perm(SceneView S, PathSet P, RayQueue in,
+                                                                         RayQueue out, const int* perm) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int count = *in.count;
+  if ((t & ~(kOrderT - 1)) >= count) return;  // the tile was not ordered (past the queue)
+  const int j = perm[t];
+  if (j < 0) return;
+  const int i = in.path[j];
+  const double4 r0 = in.ray[2 * j], r1 = in.ray[2 * j + 1];
+  V3 no, nd;
+  if (shade_one(S, P, i, v3(r0.x, r0.y, r0.z), v3(r0.w, r1.x, r1.y), in.hit_prim[j], in.hit_t[j], no, nd))
+    push_ray(out, i, no, nd, 1e30);
+}
+
 // Closest hit over a queue (Scene::intersect semantics, scene.cpp:127-168).
 __global__ void __launch_bounds__(128) k_closest(SceneView S, RayQueue Q) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
