@@ -5,7 +5,7 @@ P Stage-2 passes holds the Stage-1 work of more than P passes: the ramp 1, 2, 4,
 look-ahead batch), so each stage is normalised by ITS OWN pass count: Stage-2 kernels by the
 number of k_conn_mis launches, Stage-1 kernels by the passes of the batches in the list
 (k_pool_select's grid = passes of the batch). A Stage-1 batch is a contiguous run of launches
-in the list: pool-walk wavefront (k_light_start, traversal + k_shade per bounce), k_pool_keys,
+in the list: pool-walk wavefront (k_light_start, traversal + k_shade* per bounce), k_pool_keys,
 selection, entries, probes, bounds, the reciprocal rounds, k_pool_finish.
 
   python tools/launch_summary.py launches.csv [top]
@@ -32,7 +32,7 @@ def main():
         if n != "k_pool_keys":
             continue
         a = i
-        while a > 0 and (names[a - 1].startswith("k_trav_persistent") or names[a - 1] == "k_shade"):
+        while a > 0 and (names[a - 1].startswith("k_trav_persistent") or names[a - 1].startswith("k_shade")):
             a -= 1
         if a > 0 and names[a - 1] == "k_light_start":
             a -= 1
