@@ -57,9 +57,20 @@ PXG_HD uint32_t pxg_mulhilo32(uint32_t a, uint32_t b, uint32_t* hi) {
 #endif
 }
 
-/* Philox4x32-10, first output word only. */
+/* Philox4x32-10, first output word only. Under nvcc the function is kept out of line: one
+ * copy per kernel instead of one per draw site (the fp64 kernels draw at 5-10 sites and are
+ * 5,000+ instructions long; ncu shows instruction-fetch stalls second only to memory in
+ * k_shade): C4 +0.75%. -DPXG_PHILOX_NOINLINE=0 inlines it again. */
+#ifndef PXG_PHILOX_NOINLINE
+#define PXG_PHILOX_NOINLINE 1
+#endif
+#if defined(__CUDACC__) && PXG_PHILOX_NOINLINE
+__host__ __device__ __noinline__ static uint32_t pxg_philox_word0(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                                  uint32_t k0, uint32_t k1) {
+#else
 PXG_HD uint32_t pxg_philox_word0(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                  uint32_t k0, uint32_t k1) {
+#endif
   const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
   const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
 #if defined(__CUDA_ARCH__)
